@@ -1,0 +1,375 @@
+"""Benchmark: power flows / s of the dense (default) or sparse TPF hot path.
+
+Default workload = BASELINE.json configs[1] (C2): 100-node synthetic radial
+feeder (GenSpec(101, seed=0)), tau = 525,600 one-minute steps, complex128,
+FP64 tensor-core dense TPF on one B200.  Under torchrun each rank solves its own
+525,600-case scenario batch (weak scaling, no data-path collective; rank r>0
+uses scenario seed 1000+r); the job value is the sum of
+cases over all ranks / the max-over-ranks device time.
+
+Legs of one run (one JSON line on rank 0):
+  value    device-resident: S already in HBM; per step = iteration kernel +
+           residual post-check + summary (CUDA events, max over ranks);
+  roofline dominant kernel (dense_fpi_kernel) vs the FP64 DMMA peak measured
+           in-run by tpf_probe_fp64_tflops (MEASURED_PEAKS.json has no FP64);
+  e2e      the public API batch_solve_dense(model, LoadMatrix(S_host)) from
+           pinned host memory, H2D/D2H inside the timed region;
+  cpu_baseline  oracle port of the reference batch_solve_dense (numpy, BLAS
+           threads 1, workers = host cores) on a bounded sample (rank 0, N=1).
+`--impl reference` times only the CPU reference port (rank 0), same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "power flows/sec (τ×scenarios solved) dense+sparse TPF at 1/2/4/8 B200 vs CPU"
+UNIT = "power_flows/s"
+
+CONFIGS = {
+    # name: (n_buses, load seed (rank 0), tau, load_scale, method, description)
+    "c2": (101, 0, 525600, 1.0, "dense", "C2 dense TPF, b=100, tau=525,600 (1-min year), complex128 DMMA"),
+    "c1": (35, 0, 8760, 1.0, "dense", "C1 dense TPF, b=34, tau=8,760 (hourly year)"),
+    "c5": (1001, 0, 8760, 21.0, "dense", "C5 dense TPF, b=1,000, load_scale 21 (near collapse), tau=8,760"),
+    "c3": (5001, 0, 525600, 1.0, "sparse", "C3 sparse TPF, b=5,000, tau=525,600, batched LU trisolves"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    p.add_argument("--tau", type=int, default=None, help="override tau (testing only)")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+ARGS = parse()
+if ARGS.impl == "reference":
+    # the reference's best CPU setting: BLAS single-threaded, workers = cores
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(cfg, rank):
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios
+    n_buses, seed, tau, scale, method, desc = CONFIGS[cfg]
+    if ARGS.tau:
+        tau = ARGS.tau
+    spec = GenSpec(n_buses=n_buses, seed=0, load_scale=scale)
+    model = build_network(spec)
+    lseed = seed if rank == 0 else 1000 + rank
+    loads = gen_scenarios(model, tau, GenSpec(n_buses=n_buses, seed=lseed, load_scale=scale))
+    return model, loads, method, desc
+
+
+def cpu_sample(model, loads, seconds, cores):
+    """Time the oracle port of batch_solve_dense/sparse on a bounded column sample."""
+    from threadpoolctl import threadpool_limits
+    from oracle import tpf_oracle as orc
+    y, src, v_s = model.admittance.y_dd, model.source_injection(), model.slack.v_s
+    S = loads.values
+    method = CONFIGS[ARGS.config][4]
+    K, W = orc.dense_operators(y, src) if method == "dense" else (None, None)
+
+    def run(cols):
+        sub = np.ascontiguousarray(S[:, :cols])
+        t0 = time.perf_counter()
+        if method == "dense":
+            with threadpool_limits(limits=1, user_api="blas"):
+                orc.dense_joint(y, src, v_s, sub, workers=cores, K=K, W=W)
+        else:
+            orc.sparse_block(y, src, v_s, sub)
+        return time.perf_counter() - t0
+
+    cols = min(S.shape[1], 1024 if method == "dense" else 64)
+    dt = run(cols)
+    target = int(cols * seconds / max(dt, 1e-6) / 3)
+    if method == "sparse":
+        target = min(target, 1200)  # the reference's SuperLU fails from tau ~1,800
+    cols = max(cols, min(S.shape[1], target))
+    times = [run(cols) for _ in range(3)]
+    t = float(np.median(times))
+    return dict(value=cols / t, unit=UNIT, cores=cores, kind="port",
+                sample=f"first {cols} of {S.shape[1]} cases, oracle port of tpflow.batch_solve_"
+                       f"{method}, median of 3, setup (inverse) excluded, BLAS threads 1, "
+                       f"workers={cores if method == 'dense' else 1}")
+
+
+def run_reference():
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    model, loads, method, desc = workload(ARGS.config, 0)
+    cores = os.cpu_count() or 1
+    from threadpoolctl import threadpool_limits
+    from oracle import tpf_oracle as orc
+    y, src, v_s = model.admittance.y_dd, model.source_injection(), model.slack.v_s
+    S = loads.values
+    # bounded sample sized so the whole run stays within a few minutes
+    probe = cpu_sample(model, loads, 3.0, cores)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, ARGS.steps + ARGS.warmup)))
+    cols = int(min(S.shape[1], max(64, probe["value"] * per_step)))
+    if method == "sparse":
+        cols = min(cols, 1200)
+    sub = np.ascontiguousarray(S[:, :cols])
+    times = []
+    for i in range(ARGS.warmup + ARGS.steps):
+        t0 = time.perf_counter()
+        if method == "dense":
+            with threadpool_limits(limits=1, user_api="blas"):
+                orc.dense_joint(y, src, v_s, sub, workers=cores)  # setup included, like bench.py:139-165
+        else:
+            orc.sparse_block(y, src, v_s, sub)
+        if i >= ARGS.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = cols / t
+    line = dict(impl="reference", metric=METRIC, value=value, unit=UNIT, n_gpus=world,
+                steps=ARGS.steps, warmup=ARGS.warmup, ms_per_step=t * 1e3, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="c128", data="synthetic",
+                config=dict(workload=desc, tau_sample=cols, method=method),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=cores, kind="port",
+                                  sample=f"first {cols} of {S.shape[1]} cases per step, oracle port of "
+                                         f"tpflow.batch_solve_{method} incl. setup"),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        sm = [float(r[1]) for r in rows]
+        load = [float(r[1]) for r in rows if float(r[3]) > 150.0] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return dict(sm_mhz=float(np.median(load)), sm_max_mhz=float(rows[0][2]), samples=len(rows),
+                    reasons=sorted(reasons))
+
+
+def traffic_from_profiles(kernel):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours():
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2403_04578_b200 import DenseOperator, SparseOperator, LoadMatrix, _capi
+    from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse
+    from paper_2403_04578_b200._device import residual_and_summary
+
+    model, loads, method, desc = workload(ARGS.config, rank)
+    b, tau = loads.values.shape
+    lib = _capi.load()
+    peak_tf = ctypes_probe(lib)
+    op = DenseOperator(model, dev) if method == "dense" else SparseOperator(model, dev)
+    S = torch.from_numpy(loads.values).to(dev)
+    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        op.solve(S, V=V, iters=iters)
+        if ev:
+            ev[1].record(stream)
+        return residual_and_summary(op.contract, S, V, iters, 1e-8, dev)
+
+    for _ in range(ARGS.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(ARGS.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for k in range(ARGS.steps):
+            out = step(kev[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    ms = t0.elapsed_time(t1)
+    kms = float(np.mean([a.elapsed_time(c) for a, c in kev]))
+    sum_n = int(iters.sum().item())
+    summ = out[2].cpu().numpy()
+    if world > 1:
+        t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kms = float(t[0]), float(t[1])
+        agg = torch.tensor([tau, sum_n, int(summ[1])], dtype=torch.int64, device=dev)
+        dist.all_reduce(agg)
+        total_cases = int(agg[0])
+    else:
+        total_cases = tau
+    value = total_cases * ARGS.steps / (ms * 1e-3)
+
+    if method == "dense":
+        alg = 8.0 * b * b * sum_n  # FLOP_alg = 8 b^2 sum_j n_j
+        achieved = alg / (kms * 1e-3) / 1e12
+        roofline = dict(bound="fp64-tensor", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
+                        frac=achieved / peak_tf if peak_tf else None,
+                        traffic=traffic_from_profiles("dense_fpi_kernel"),
+                        kernel="dense_fpi_kernel", kernel_ms=kms,
+                        peak_source="measured in-run: DMMA-only probe (tpf_probe_fp64_tflops); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                        algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch")
+    else:
+        alg = 48.0 * b * sum_n  # BYTES_alg = 48 b sum_j n_j
+        achieved = alg / (kms * 1e-3) / 1e9
+        peak = measured_hbm()
+        roofline = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                        traffic=traffic_from_profiles("sparse_fpi_kernel"), kernel="sparse_fpi_kernel",
+                        kernel_ms=kms, peak_source="MEASURED_PEAKS.json hbm_gbs",
+                        algorithmic=f"48*b*sum(n_j) = {alg:.4e} bytes per launch")
+
+    e2e = None
+    if not ARGS.no_e2e:
+        e2e = run_e2e(model, loads, method, dev, batch_solve_dense, batch_solve_sparse, LoadMatrix, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
+        cpu = cpu_sample(model, loads, ARGS.cpu_seconds, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=ARGS.steps,
+                    warmup=ARGS.warmup, ms_per_step=ms / ARGS.steps, higher_is_better=True,
+                    scaling="weak", vs_baseline=None, dtype="c128", data="synthetic",
+                    config=dict(workload=desc, b=b, tau_per_gpu=tau, method=method,
+                                sum_iterations=sum_n, batch_iterations=int(summ[0]),
+                                converged=int(summ[1]),
+                                l2="inputs (S, V: %.0f MB each) larger than the 126 MB L2" % (b * tau * 16 / 1e6),
+                                parallelism=f"tau-sharded x{world} (independent scenario batches)"),
+                    roofline=roofline, cpu_baseline=cpu, e2e=e2e,
+                    gpu_launches=3 * ARGS.steps,
+                    clocks=clk.summary())
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_probe(lib):
+    import ctypes
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    rc = lib.tpf_probe_fp64_tflops(ctypes.byref(tf), ctypes.byref(ms))
+    return tf.value if rc == 0 else None
+
+
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world):
+    """Public API from pinned host memory; H2D/D2H inside the timed region."""
+    import torch
+    import torch.distributed as dist
+    pinned = torch.from_numpy(loads.values).pin_memory()
+    host = LoadMatrix(pinned.numpy())
+    solver = bsd if method == "dense" else bss
+    for _ in range(1):
+        solver(model, host, device=dev)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ts = []
+    for _ in range(max(1, ARGS.steps)):
+        t0 = time.perf_counter()
+        out = solver(model, host, device=dev)
+        torch.cuda.synchronize(dev)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    b, tau = loads.values.shape
+    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * 16),
+                d2h_bytes_per_step=int(b * tau * 16 + tau * (4 + 8 + 1)),
+                ms_per_step=t * 1e3, api=f"paper_2403_04578_b200.batch_solve_{method}(model, LoadMatrix)",
+                iterations=int(out.iterations))
+
+
+if __name__ == "__main__":
+    if ARGS.impl == "reference":
+        run_reference()
+    else:
+        run_ours()

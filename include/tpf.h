@@ -1,0 +1,129 @@
+/*
+ * tpf.h -- C ABI of the B200-native Tensor Power Flow engine (libtpf.so).
+ *
+ * The reference (`tpflow`, pure Python) has no FFI: its hot-path "operator
+ * API" is the Python pair batch_solve_dense / batch_solve_sparse
+ * (pkg/src/tpflow/dense.py:129-134, sparse.py:167-172) dispatched by
+ * solve_batch (bench.py:96-111).  The Python package
+ * `paper_2403_04578_b200` re-exposes those signatures and calls the entry
+ * points below through ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - complex128 data are interleaved (re, im) doubles; strides are counted in
+ *    complex elements.  Element (node i, case j) of a b x tau matrix lives at
+ *    index i*node_stride + j*case_stride.  The reference's LoadMatrix layout
+ *    (b x tau, C order, dense.py:57-78) is node_stride = tau, case_stride = 1.
+ *  - "_c128" entry points take DEVICE pointers, are stream-ordered on the
+ *    given cudaStream_t (NULL = legacy default stream) and never synchronize.
+ *    "_host" entry points take HOST pointers and return after completion.
+ *  - Every entry point returns TPF_OK (0) or an error code; the message of
+ *    the last failure on the calling thread is tpf_last_error().
+ *  - Stateless; safe to call concurrently on different devices/streams.
+ *
+ * Semantics (both solvers): flat start v = v_flat for every node; each
+ * iteration applies the zero-voltage guard (|v| < 1e-12 -> 1e-12, fpi.py:39-41),
+ * the fixed-point update, and a per-case step test max_i |v'_i - v_i| < tol
+ * (dense.py:125-126, 189-193).  A case stops at its first passing step or at
+ * max_iter ("per-case freeze"); iters[j] is its update count.  The reference's
+ * batch `iterations` equals max_j iters[j] (test_dense.py:72-79).  Non-finite
+ * steps never pass, so diverging cases run to max_iter, as in the reference.
+ */
+#ifndef TPF_H_
+#define TPF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPF_OK 0
+#define TPF_ERR_INVALID 1     /* bad argument (ValueError in the reference) */
+#define TPF_ERR_CUDA 2        /* CUDA runtime failure */
+#define TPF_ERR_UNSUPPORTED 3 /* shape not supported by this entry point */
+#define TPF_ERR_SINGULAR 4    /* zero pivot (SingularSystemError, fpi.py:44) */
+#define TPF_ERR_MEMORY 5      /* allocation failure (MemoryGuardError, sparse.py:55) */
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int tpf_version(void);
+/* Message of the last failed call on this thread ("" if none). */
+const char* tpf_last_error(void);
+
+/* ---------------------------------------------------------------- dense --
+ * Replaces the hot loop of batch_solve_dense (dense.py:166-193) and its
+ * per-iteration op chain _iterate_chunk (dense.py:114-126):
+ *     V <- K (S* ./ conj(V)) + W,   K = -inv(Y_dd) (dense.py:151),
+ *                                   W = K (Y_ds v_s) (dense.py:152).
+ * FP64 tensor-core (DMMA) kernel with K resident in shared memory:
+ * requires b <= tpf_dense_max_nodes() (104).  Larger b: tpf_dense_fpi_large_c128.
+ *   S      b x tau complex loads (consumption positive), device
+ *   K      b x b complex, row-major, device
+ *   W      b complex, device
+ *   V      b x tau complex output, device
+ *   iters  int32[tau] per-case update counts, device
+ *   workspace >= tpf_dense_workspace_bytes(b) device bytes
+ */
+int tpf_dense_max_nodes(void);
+size_t tpf_dense_workspace_bytes(int32_t b);
+int tpf_dense_fpi_c128(int64_t tau, int32_t b,
+                       const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                       const double* K, const double* W,
+                       double v_flat_re, double v_flat_im,
+                       double tol, int32_t max_iter,
+                       double* V, int64_t v_node_stride, int64_t v_case_stride,
+                       int32_t* iters, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* --------------------------------------------------------------- sparse --
+ * Replaces the hot loop of batch_solve_sparse (sparse.py:186-197), which
+ * re-solves a tau-block-diagonal SuperLU system per iteration.  Every block
+ * is the equation Y_dd v'_j = -(s_j* ./ conj(v_j) + src), so one host LU
+ * Pr Y_dd Pc = L U (factorized once) serves all cases:
+ *   l_ptr/l_col/l_val   strictly-lower part of unit-diagonal L, CSR (int32, complex)
+ *   u_ptr/u_col/u_val   strictly-upper part of U, CSR
+ *   u_diag_inv          complex[b] = 1 / U[k,k]
+ *   perm                int32[2b]: perm[k] = node whose right-hand side feeds
+ *                       forward row k (row permutation), perm[b+i] = index of
+ *                       node i's solution in the permuted unknowns (column perm.)
+ *   src                 complex[b] = Y_ds v_s
+ *   workspace >= tpf_sparse_workspace_bytes(tau, b) device bytes            */
+size_t tpf_sparse_workspace_bytes(int64_t tau, int32_t b);
+int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
+                        const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                        const int32_t* l_ptr, const int32_t* l_col, const double* l_val,
+                        const int32_t* u_ptr, const int32_t* u_col, const double* u_val,
+                        const double* u_diag_inv, const int32_t* perm, const double* src,
+                        double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                        double* V, int64_t v_node_stride, int64_t v_case_stride,
+                        int32_t* iters, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* -------------------------------------------------------------- residual --
+ * residual_per_case (fpi.py:221-240, constant-power branch) as used by
+ * _safe_residuals (dense.py:208-211):
+ *     resid[j] = max_i | s_ij + v_ij * conj(src_i + (Y_dd v_j)_i) |
+ * Y_dd in CSR (int32 row_ptr[b+1], int32 col[nnz], complex val[nnz]).
+ * NaN propagates as in numpy's max.                                        */
+int tpf_residual_c128(int64_t tau, int32_t b,
+                      const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                      const double* V, int64_t v_node_stride, int64_t v_case_stride,
+                      const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                      const double* src, double* resid, void* stream);
+
+/* --------------------------------------------------------------- summary --
+ * converged mask (dense.py:198-199): mask[j] = isfinite(resid[j]) && resid[j] < residual_tol.
+ * out[0] = max_j iters[j] (the reference's joint iteration count),
+ * out[1] = number of converged cases.  out must be 2 int32 of device memory. */
+int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
+                      double residual_tol, uint8_t* mask, int32_t* out, void* stream);
+
+/* ----------------------------------------------------------------- probe --
+ * FP64 tensor-core peak of the current device, measured with a DMMA-only
+ * kernel (used as the dense roofline denominator).  Synchronous.           */
+int tpf_probe_fp64_tflops(double* tflops_out, double* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPF_H_ */

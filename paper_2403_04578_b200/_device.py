@@ -1,0 +1,89 @@
+"""Host <-> device plumbing shared by the dense and sparse solvers (PyTorch is
+used for device memory and streams only; all arithmetic runs in libtpf.so)."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from scipy import sparse
+
+from . import _capi
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the TPF engine needs a CUDA device (sm_100a); there is no CPU fallback")
+    _capi.load()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+@dataclass
+class ModelContract:
+    """The four things the hot path reads from a network model."""
+
+    b: int
+    y_dd: sparse.csr_matrix
+    src: np.ndarray
+    v_s: complex
+    constant_power: bool
+
+    @classmethod
+    def of(cls, model) -> "ModelContract":
+        y = sparse.csr_matrix(model.admittance.y_dd, dtype=complex)
+        y.sort_indices()
+        return cls(b=int(model.n_demand), y_dd=y,
+                   src=np.ascontiguousarray(np.asarray(model.source_injection(), dtype=complex)),
+                   v_s=complex(model.slack.v_s),
+                   constant_power=bool(model.zip.is_constant_power))
+
+    def csr_on(self, device: torch.device):
+        rp = torch.from_numpy(self.y_dd.indptr.astype(np.int32)).to(device)
+        ci = torch.from_numpy(self.y_dd.indices.astype(np.int32)).to(device)
+        val = torch.from_numpy(np.ascontiguousarray(self.y_dd.data)).to(device)
+        src = torch.from_numpy(self.src).to(device)
+        return rp, ci, val, src
+
+
+def complex_strides(t: torch.Tensor) -> tuple[int, int]:
+    """(node_stride, case_stride) in complex elements of a b x tau tensor."""
+    return int(t.stride(0)), int(t.stride(1))
+
+
+def loads_to_device(values: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Copy a b x tau complex load matrix to the device keeping its C/F order."""
+    arr = np.asarray(values, dtype=np.complex128)
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        arr = np.ascontiguousarray(arr)
+    host = torch.from_numpy(arr)
+    out = torch.empty_strided(host.shape, host.stride(), dtype=torch.complex128, device=device)
+    out.copy_(host)
+    return out
+
+
+def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tensor,
+                         iters: torch.Tensor, residual_tol: float, device: torch.device):
+    """Residual post-check and converged mask on the device (dense.py:198-199)."""
+    tau = V.shape[1]
+    rp, ci, val, src = contract.csr_on(device)
+    resid = torch.empty(tau, dtype=torch.float64, device=device)
+    mask = torch.empty(tau, dtype=torch.uint8, device=device)
+    summ = torch.zeros(2, dtype=torch.int32, device=device)
+    st = stream_ptr(device)
+    sn, sc = complex_strides(S)
+    vn, vc = complex_strides(V)
+    _capi.call("tpf_residual_c128", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+               rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
+    _capi.call("tpf_batch_summary", tau, iters.data_ptr(), resid.data_ptr(), float(residual_tol),
+               mask.data_ptr(), summ.data_ptr(), st)
+    return resid, mask, summ

@@ -1,0 +1,365 @@
+// Dense Tensor Power Flow on sm_100a: persistent FP64-DMMA fixed-point kernel.
+//
+// Replaces the hot loop of the reference `batch_solve_dense`
+// (pkg/src/tpflow/dense.py:166-193, per-iteration op chain `_iterate_chunk`
+// dense.py:114-126):   V' = K (S* ./ conj(V)) + W,  K = -inv(Y_dd),
+// written case-major as V'(case, :) = U(case, :) K^T + W with U = S*/conj(V).
+//
+// Layout of the work (b <= 104, so K fits in shared memory):
+//   * one CTA per SM, 8 warps, persistent;
+//   * K^T lives in shared memory for the whole launch, pre-swizzled into the
+//     B-fragment order of mma.m8n8k4 (one 16-byte (re,im) pair per lane per
+//     fragment, so every fragment load is a conflict-free LDS.128);
+//   * warps work in pairs; a pair owns 8 case "slots" (the M=8 rows of the MMA)
+//     and splits the 8*NB output nodes between its two warps (7/6 blocks at
+//     b=100, alternated between pairs so every SM sub-partition gets the same
+//     FP64 work);
+//   * the iterate V, the old iterate and S* of a slot stay in registers across
+//     iterations (C-fragment layout); only U = S*/conj(V) goes through shared
+//     memory (A-fragment order), once per iteration;
+//   * complex GEMM = 4 real DMMAs per (k-step, node block):
+//       Re += Ur*Kr - Ui*Ki,  Im += Ur*Ki + Ui*Kr,   accumulators start at W;
+//   * epilogue: per-case |V'-V|^2 < tol^2 over all nodes (warp ballot + pair
+//     exchange), per-case freeze, and immediate refill of a frozen slot with
+//     the next unsolved case from a global atomic counter (continuous
+//     batching: no tile waits for its slowest case).
+// Each case's arithmetic is independent of the slot, warp, CTA or launch it
+// runs in, so results are bitwise invariant to permutation and sharding.
+#include <climits>
+#include <cstdio>
+
+#include "tpf_common.cuh"
+#include "tpf_internal.h"
+
+namespace tpf {
+
+constexpr int kPairs = 4;          // warp pairs per CTA
+constexpr int kWarps = 2 * kPairs;  // 8 warps
+constexpr int kThreads = 32 * kWarps;
+
+struct DenseArgs {
+  int64_t tau;
+  int b;
+  int ks_count;  // k-steps of 4 input nodes: ceil(b/4)
+  const double* S;
+  int64_t s_node, s_case;  // strides in complex elements
+  const double* K;         // b x b complex, row-major
+  const double* W;         // b complex
+  double v_flat_re, v_flat_im;
+  double tol2;
+  int max_iter;
+  double* V;
+  int64_t v_node, v_case;
+  int32_t* iters;
+  unsigned long long* counter;  // next unclaimed case
+};
+
+template <int NB>
+struct DenseSmem {
+  static constexpr int kMaxKs = 2 * NB;
+  // K^T in B-fragment order: [nb][ks][lane] -> (Kr, Ki) of K[8nb + lane/4][4ks + lane%4]
+  static constexpr size_t k_bytes(int ks) { return size_t(NB) * ks * 32 * sizeof(double2); }
+  // U in A-fragment order per pair: [pair][ks][lane] -> U[slot lane/4][node 4ks + lane%4]
+  static constexpr size_t u_bytes(int ks) { return size_t(kPairs) * ks * 32 * sizeof(double2); }
+  static constexpr size_t w_bytes() { return size_t(NB) * 8 * sizeof(double2); }
+  static constexpr size_t misc_bytes() { return 1024; }
+  static size_t total(int ks) { return k_bytes(ks) + u_bytes(ks) + w_bytes() + misc_bytes(); }
+};
+
+// Next unclaimed case index, saturated at INT_MAX (= idle slot).
+__device__ __forceinline__ int claim_case(unsigned long long* counter) {
+  const unsigned long long c = atomicAdd(counter, 1ull);
+  return c < (unsigned long long)INT_MAX ? int(c) : INT_MAX;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs a) {
+  constexpr int NBH = (NB + 1) / 2;  // max node blocks per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int KS = a.ks_count;
+  double2* k_sm = reinterpret_cast<double2*>(smem_raw);
+  double2* u_all = k_sm + size_t(NB) * KS * 32;
+  double2* w_sm = u_all + size_t(kPairs) * KS * 32;
+  uint32_t* flags = reinterpret_cast<uint32_t*>(w_sm + NB * 8);  // [pair][2]
+  int* next_ids = reinterpret_cast<int*>(flags + 2 * kPairs);     // [pair][8 slots][2]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int pair = warp >> 1;
+  const int half = warp & 1;
+  const int q = lane & 3;    // C-fragment column group: nodes 2q, 2q+1 of a block
+  const int slot = lane >> 2;  // C/A-fragment row: case slot 0..7
+  const int b = a.b;
+  const int64_t tau = a.tau;
+
+  // ---- stage K^T fragments and W into shared memory (once per launch) ----
+  for (int idx = tid; idx < NB * KS * 32; idx += kThreads) {
+    const int l = idx & 31;
+    const int ks = (idx >> 5) % KS;
+    const int nb = (idx >> 5) / KS;
+    const int row = 8 * nb + (l >> 2);
+    const int col = 4 * ks + (l & 3);
+    double2 v = make_double2(0.0, 0.0);
+    if (row < b && col < b) v = ldg_c128(a.K, int64_t(row) * b + col);
+    k_sm[idx] = v;
+  }
+  for (int i = tid; i < NB * 8; i += kThreads)
+    w_sm[i] = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
+
+  // ---- slot bookkeeping: two prefetched case ids per slot (ring of 2) ----
+  if (half == 0 && lane < 8) {
+    next_ids[(pair * 8 + lane) * 2 + 0] = claim_case(a.counter);
+    next_ids[(pair * 8 + lane) * 2 + 1] = claim_case(a.counter);
+  }
+  __syncthreads();
+
+  // this warp's node blocks (alternate the larger half between pairs)
+  const int n_big = NBH, n_small = NB - NBH;
+  const bool big_first = ((pair >> 1) & 1) == 0;
+  const int nbw = (half == 0) == big_first ? n_big : n_small;
+  const int nb0 = half == 0 ? 0 : (big_first ? n_big : n_small);
+
+  double2* u_sm = u_all + size_t(pair) * KS * 32;
+  const int bar_id = 1 + pair;
+
+  // per-thread state: iterate (C layout), old iterate, S*
+  double vr[NBH][2], vi[NBH][2], orr[NBH][2], oi[NBH][2], sr[NBH][2], si[NBH][2];
+  int cid = INT_MAX;  // current case of my slot (INT_MAX = idle)
+  int n_it = 0;       // updates applied to the current case
+  int refills = 0;    // ring position
+
+  auto load_case = [&](int c) {
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int node = 8 * (nb0 + lb) + 2 * q + e;
+        double2 s = make_double2(0.0, 0.0);
+        if (lb < nbw && node < b && c < tau) s = ldg_c128(a.S, node * a.s_node + int64_t(c) * a.s_case);
+        sr[lb][e] = s.x;
+        si[lb][e] = -s.y;  // S* (dense.py:154)
+        vr[lb][e] = a.v_flat_re;
+        vi[lb][e] = a.v_flat_im;
+      }
+    }
+  };
+
+  // initial fill (refill #0)
+  cid = next_ids[(pair * 8 + slot) * 2 + 0];
+  refills = 1;
+  if (cid >= tau) cid = INT_MAX;
+  load_case(cid);
+
+  for (;;) {
+    // ---------- elementwise: guard, keep old iterate, U = S*/conj(V) ----------
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+      if (lb < nbw) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double xr = vr[lb][e], xi = vi[lb][e];
+          double m2 = __fma_rn(xr, xr, xi * xi);
+          if (m2 < kZeroGuard2) {  // fpi.py:39-41 / dense.py:170-172
+            xr = kZeroGuard;
+            xi = 0.0;
+            m2 = kZeroGuard * kZeroGuard;
+          }
+          orr[lb][e] = xr;
+          oi[lb][e] = xi;
+          // S*/conj(v) = S* v / |v|^2
+          const double r = 1.0 / m2;
+          const double ur = __fma_rn(sr[lb][e], xr, -(si[lb][e] * xi)) * r;
+          const double ui = __fma_rn(sr[lb][e], xi, si[lb][e] * xr) * r;
+          const int node = 8 * (nb0 + lb) + 2 * q + e;
+          const int ks = node >> 2;
+          if (ks < KS) u_sm[ks * 32 + slot * 4 + (node & 3)] = make_double2(ur, ui);
+        }
+      }
+    }
+    named_bar(bar_id, 64);  // U complete for both halves
+
+    // ---------- GEMM: V' = W + U K^T on FP64 tensor cores ----------
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+      if (lb < nbw) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double2 w = w_sm[8 * (nb0 + lb) + 2 * q + e];
+          vr[lb][e] = w.x;
+          vi[lb][e] = w.y;
+        }
+      }
+    }
+    const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
+#pragma unroll 1
+    for (int ks = 0; ks < KS; ++ks) {
+      const double2 u = u_sm[ks * 32 + lane];
+      const double nui = neg_int(u.y);
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          const double2 k = kb[(size_t(lb) * KS + ks) * 32];
+          dmma884(vr[lb][0], vr[lb][1], u.x, k.x);
+          dmma884(vi[lb][0], vi[lb][1], u.x, k.y);
+          dmma884(vr[lb][0], vr[lb][1], nui, k.y);
+          dmma884(vi[lb][0], vi[lb][1], u.y, k.x);
+        }
+      }
+    }
+
+    // ---------- epilogue: per-case step test (dense.py:125-126, 189-193) ----------
+    bool small = true;
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+      if (lb < nbw) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int node = 8 * (nb0 + lb) + 2 * q + e;
+          const double dr = vr[lb][e] - orr[lb][e];
+          const double di = vi[lb][e] - oi[lb][e];
+          const double d2 = __fma_rn(dr, dr, di * di);
+          // NaN/inf never compare small: they hold the case open to the cap
+          if (node < b && !(d2 < a.tol2)) small = false;
+        }
+      }
+    }
+    const uint32_t ball = __ballot_sync(0xffffffffu, small);
+    if (lane == 0) flags[pair * 2 + half] = ball;
+    named_bar(bar_id, 64);  // flags of both halves visible; U reads finished
+    const uint32_t both = flags[pair * 2] & flags[pair * 2 + 1];
+    const bool my_small = ((both >> (slot * 4)) & 0xFu) == 0xFu;
+
+    bool done = false;
+    if (cid != INT_MAX) {
+      ++n_it;
+      done = my_small || n_it >= a.max_iter;
+    }
+    if (done) {
+      // retire: V and per-case iteration count
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int node = 8 * (nb0 + lb) + 2 * q + e;
+            if (node < b) stg_c128(a.V, node * a.v_node + int64_t(cid) * a.v_case, make_double2(vr[lb][e], vi[lb][e]));
+          }
+        }
+      }
+      if (half == 0 && q == 0) a.iters[cid] = n_it;
+      // refill from the prefetch ring; warp 0 of the pair tops the ring up
+      const int ring = (pair * 8 + slot) * 2;
+      int nc = next_ids[ring + (refills & 1)];
+      if (half == 0 && q == 0) {
+        next_ids[ring + ((refills + 1) & 1)] =
+            claim_case(a.counter);
+      }
+      ++refills;
+      cid = (nc < tau) ? nc : INT_MAX;
+      n_it = 0;
+      load_case(cid);
+    }
+    if (__all_sync(0xffffffffu, cid == INT_MAX)) break;
+  }
+}
+
+template <int NB>
+static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
+  const size_t smem = DenseSmem<NB>::total(a.ks_count);
+  cudaError_t err = cudaFuncSetAttribute(dense_fpi_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense)", err);
+  int per_sm = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_fpi_kernel<NB>, kThreads, smem);
+  if (err != cudaSuccess) return set_cuda_error("occupancy(dense)", err);
+  if (per_sm < 1) return set_error(TPF_ERR_UNSUPPORTED, "dense kernel does not fit on an SM");
+  // slots in flight = 8 per pair; never launch more CTAs than needed
+  const int64_t slots_per_cta = 8 * kPairs;
+  int64_t grid = int64_t(per_sm) * sm_count;
+  const int64_t need = (a.tau + slots_per_cta - 1) / slots_per_cta;
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  dense_fpi_kernel<NB><<<unsigned(grid), kThreads, smem, stream>>>(a);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(dense_fpi_kernel)", err);
+  return TPF_OK;
+}
+
+size_t dense_smem_bytes(int b) {
+  const int nb = (b + 7) / 8, ks = (b + 3) / 4;
+  return size_t(nb) * ks * 32 * 16 + size_t(kPairs) * ks * 32 * 16 + size_t(nb) * 8 * 16 + 1024;
+}
+
+}  // namespace tpf
+
+using namespace tpf;
+
+extern "C" int tpf_dense_max_nodes(void) { return 104; }
+
+extern "C" size_t tpf_dense_workspace_bytes(int32_t b) {
+  (void)b;
+  return 256;
+}
+
+extern "C" int tpf_dense_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                  int64_t s_case_stride, const double* K, const double* W,
+                                  double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                  double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                  int32_t* iters, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: need tau >= 0 and b >= 1");
+  if (b > 104)
+    return set_error(TPF_ERR_UNSUPPORTED,
+                     "tpf_dense_fpi_c128: b > 104 does not fit K in shared memory; use tpf_dense_fpi_large_c128");
+  if (tau > INT_MAX - 4096) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: tau too large for one launch; shard it");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!S || !K || !W || !V || !iters) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: null pointer");
+  if (!workspace || workspace_bytes < tpf_dense_workspace_bytes(b))
+    return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return set_cuda_error("cudaGetDevice", err);
+  err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (err != cudaSuccess) return set_cuda_error("cudaDeviceGetAttribute", err);
+  err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+  if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
+
+  DenseArgs a;
+  a.tau = tau;
+  a.b = b;
+  a.ks_count = (b + 3) / 4;
+  a.S = S;
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.K = K;
+  a.W = W;
+  a.v_flat_re = v_flat_re;
+  a.v_flat_im = v_flat_im;
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = V;
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  a.counter = static_cast<unsigned long long*>(workspace);
+  switch ((b + 7) / 8) {
+    case 1: return launch_dense<1>(a, st, sms);
+    case 2: return launch_dense<2>(a, st, sms);
+    case 3: return launch_dense<3>(a, st, sms);
+    case 4: return launch_dense<4>(a, st, sms);
+    case 5: return launch_dense<5>(a, st, sms);
+    case 6: return launch_dense<6>(a, st, sms);
+    case 7: return launch_dense<7>(a, st, sms);
+    case 8: return launch_dense<8>(a, st, sms);
+    case 9: return launch_dense<9>(a, st, sms);
+    case 10: return launch_dense<10>(a, st, sms);
+    case 11: return launch_dense<11>(a, st, sms);
+    case 12: return launch_dense<12>(a, st, sms);
+    case 13: return launch_dense<13>(a, st, sms);
+    default: break;
+  }
+  return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");
+}

@@ -1,0 +1,116 @@
+"""Dense Tensor Power Flow on the GPU -- drop-in for ``tpflow.batch_solve_dense``.
+
+Reference: pkg/src/tpflow/dense.py:129-205.  Same signature, same
+``LoadMatrix -> VoltageBatch`` contract, same errors:
+
+* ``ValueError("load matrix has N rows, model has M")`` (dense.py:143-146);
+* non-constant-power ZIP models: the reference routes them through the
+  single-case solver column by column (dense.py:147-148, 214-230); that is not
+  the batched hot path, so this engine raises ``NotImplementedError`` naming
+  the reference route instead of silently running a CPU loop;
+* ``numpy.linalg.LinAlgError`` from the inverse of a singular Y_dd
+  (dense.py:151, uncaught in the reference too).
+
+Setup follows the reference exactly (K = -inv(Y_dd) by LAPACK on the host,
+W = K src); the iteration, the residual post-check and the converged mask run
+in libtpf.so.  ``workers`` is accepted and ignored (results are bitwise
+independent of any partitioning, like the reference's, test_dense.py:96-102).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _capi
+from ._device import (ModelContract, complex_strides, loads_to_device, require_cuda,
+                      residual_and_summary, stream_ptr)
+from ._types import LoadMatrix, SolveOptions, VoltageBatch
+
+__all__ = ["batch_solve_dense", "DenseOperator"]
+
+
+class DenseOperator:
+    """K = -inv(Y_dd) and W = K src resident on one device (dense.py:150-152).
+
+    ``solve(S)`` runs the per-case-freeze fixed point on device tensors; it is
+    what ``batch_solve_dense`` and ``bench.py`` call.
+    """
+
+    def __init__(self, model, device=None):
+        self.device = require_cuda(device)
+        self.contract = ModelContract.of(model)
+        b = self.contract.b
+        K = -np.linalg.inv(self.contract.y_dd.toarray())
+        W = K @ self.contract.src
+        self.K_host = K
+        self.W_host = W
+        self.K = torch.from_numpy(np.ascontiguousarray(K)).to(self.device)
+        self.W = torch.from_numpy(np.ascontiguousarray(W)).to(self.device)
+        self.large = b > _capi.load().tpf_dense_max_nodes()
+        self.v_flat = complex(abs(self.contract.v_s))
+        self._ws = None
+
+    @property
+    def b(self) -> int:
+        return self.contract.b
+
+    def workspace(self, tau: int) -> torch.Tensor:
+        lib = _capi.load()
+        n = (lib.tpf_dense_large_workspace_bytes(tau, self.b) if self.large
+             else lib.tpf_dense_workspace_bytes(self.b))
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(max(int(n), 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V: torch.Tensor | None = None,
+              iters: torch.Tensor | None = None):
+        """Run the iteration on a device b x tau complex128 tensor (any strides).
+
+        Returns ``(V, iters)``; V is b x tau C-contiguous unless given.
+        """
+        b, tau = S.shape
+        if b != self.b:
+            raise ValueError(f"load matrix has {b} rows, model has {self.b}")
+        if V is None:
+            V = torch.empty((b, tau), dtype=torch.complex128, device=self.device)
+        if iters is None:
+            iters = torch.empty(tau, dtype=torch.int32, device=self.device)
+        ws = self.workspace(tau)
+        sn, sc = complex_strides(S)
+        vn, vc = complex_strides(V)
+        fn = "tpf_dense_fpi_large_c128" if self.large else "tpf_dense_fpi_c128"
+        _capi.call(fn, tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
+                   self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                   V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),
+                   stream_ptr(self.device))
+        return V, iters
+
+
+def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
+                      workers: int = 1, *, device=None, return_on_device: bool = False) -> VoltageBatch:
+    """GPU ``batch_solve_dense`` (dense.py:129-205); see module docstring."""
+    del workers  # accepted for signature compatibility; partitioning never changes bits
+    if not isinstance(loads, LoadMatrix):
+        loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
+    if loads.n_demand != model.n_demand:
+        raise ValueError(f"load matrix has {loads.n_demand} rows, model has {model.n_demand}")
+    if not model.zip.is_constant_power:
+        raise NotImplementedError(
+            "mixed ZIP loads are not on the batched hot path; the reference routes them "
+            "through its single-case solver (tpflow.dense._batch_via_single -> fpi_solve)")
+    op = DenseOperator(model, device)
+    S = loads_to_device(loads.values, op.device)
+    V, iters = op.solve(S, opts)
+    resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
+    return finish(V, iters, resid, mask, summ, return_on_device)
+
+
+def finish(V, iters, resid, mask, summ, on_device: bool) -> VoltageBatch:
+    summ_h = summ.cpu().numpy()
+    if on_device:
+        return VoltageBatch(values=V, iterations=int(summ_h[0]), converged_mask=mask.bool(),
+                            residuals=resid, iterations_per_case=iters)
+    return VoltageBatch(values=V.cpu().numpy(), iterations=int(summ_h[0]),
+                        converged_mask=mask.cpu().numpy().astype(bool),
+                        residuals=resid.cpu().numpy(), iterations_per_case=iters.cpu().numpy())

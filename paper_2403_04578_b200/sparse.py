@@ -1,0 +1,244 @@
+"""Sparse Tensor Power Flow on the GPU -- drop-in for ``tpflow.batch_solve_sparse``.
+
+Reference: pkg/src/tpflow/sparse.py:167-207.  The reference stacks tau blocks
+``-diag(1/s_j*) Y_dd`` into one (b tau)^2 block-diagonal matrix and factorizes
+it with SuperLU (sparse.py:115-164, 70-97).  Multiplying block row i by
+``-s_ij*`` shows every block is the same equation
+
+    Y_dd v'_j = -(s_j* ./ conj(v_j) + src)          (zero-load rows included)
+
+so this engine factorizes ``Y_dd`` ONCE on the host (SuperLU; for radial
+feeders in leaf-first order, which gives an LU with no fill and no pivoting,
+SURVEY.md A.6) and runs batched forward/backward sweeps for all tau cases per
+iteration in libtpf.so.  ``factorization_count()`` therefore still grows by
+exactly one per batch (test_sparse.py:164-168).
+
+``max_nnz``: the reference refuses batches whose block matrix would exceed
+``max_nnz`` nonzeros (sparse.py:131-136).  Here no block matrix exists; the
+guard is honoured only when the caller passes ``max_nnz`` explicitly (same
+``MemoryGuardError`` message), otherwise the batch is solved whatever its
+size, in tau chunks that fit device memory.
+"""
+
+from __future__ import annotations
+
+import threading
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+from scipy import sparse
+from scipy.sparse.linalg import splu
+
+from . import _capi
+from ._device import (ModelContract, complex_strides, loads_to_device, require_cuda,
+                      residual_and_summary, stream_ptr)
+from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
+from .dense import finish
+
+__all__ = ["batch_solve_sparse", "factorization_count", "factorize_ydd", "TreeLU",
+           "DEFAULT_MAX_BLOCK_NNZ"]
+
+# sparse.py:44
+DEFAULT_MAX_BLOCK_NNZ = 50_000_000
+
+_factorizations = 0
+_lock = threading.Lock()
+
+
+def factorization_count() -> int:
+    """Monotone count of Y_dd factorizations (sparse.py:50-52)."""
+    return _factorizations
+
+
+def leaf_first_order(y: sparse.csr_matrix) -> np.ndarray | None:
+    """Decreasing-depth order of the graph of Y_dd if it is a forest, else None.
+
+    Eliminating a tree leaf-first creates no fill.
+    """
+    b = y.shape[0]
+    g = sparse.csr_matrix(abs(y) + abs(y).T)
+    g.setdiag(0)
+    g.eliminate_zeros()
+    if g.nnz // 2 > b - 1:
+        return None
+    depth = np.full(b, -1, dtype=np.int64)
+    for root in range(b):
+        if depth[root] >= 0:
+            continue
+        depth[root] = 0
+        queue = deque([root])
+        edges = 0
+        nodes = 0
+        while queue:
+            u = queue.popleft()
+            nodes += 1
+            for v in g.indices[g.indptr[u]:g.indptr[u + 1]]:
+                edges += 1
+                if depth[v] < 0:
+                    depth[v] = depth[u] + 1
+                    queue.append(v)
+        if edges // 2 != nodes - 1:
+            return None
+    return np.argsort(-depth, kind="stable")
+
+
+@dataclass
+class TreeLU:
+    """Pr (Y_dd[o][:, o]) Pc = L U in the arrays libtpf's sparse kernel reads."""
+
+    b: int
+    l_ptr: np.ndarray
+    l_col: np.ndarray
+    l_val: np.ndarray
+    u_ptr: np.ndarray
+    u_col: np.ndarray
+    u_val: np.ndarray
+    u_diag_inv: np.ndarray
+    perm: np.ndarray  # [row_src (b) | col_dst (b)], int32
+    ordering: str
+
+    @property
+    def nnz(self) -> int:
+        return int(self.l_col.size + self.u_col.size + self.b)
+
+
+def factorize_ydd(y_dd) -> TreeLU:
+    """One LU of Y_dd; raises SingularSystemError like sparse.py:82-94."""
+    global _factorizations
+    y = sparse.csr_matrix(y_dd, dtype=complex)
+    b = y.shape[0]
+    if y.shape[0] != y.shape[1]:
+        raise ValueError("factorize requires a square matrix")
+    order = leaf_first_order(y)
+    try:
+        if order is not None:
+            yp = y[order][:, order].tocsc()
+            lu = splu(yp, permc_spec="NATURAL", diag_pivot_thresh=0.0,
+                      options=dict(SymmetricMode=True))
+            kind = "leaf-first"
+        else:
+            order = np.arange(b)
+            lu = splu(y.tocsc())
+            kind = "colamd"
+    except RuntimeError as exc:
+        empty_rows = np.where(np.diff(y.indptr) == 0)[0]
+        empty_cols = np.where(np.diff(y.tocsc().indptr) == 0)[0]
+        where = []
+        if empty_rows.size:
+            where.append(f"empty rows {empty_rows[:8].tolist()}")
+        if empty_cols.size:
+            where.append(f"empty columns {empty_cols[:8].tolist()}")
+        detail = f" ({'; '.join(where)})" if where else ""
+        raise SingularSystemError(f"sparse factorization failed: {exc}{detail}") from exc
+    with _lock:
+        _factorizations += 1
+    L = sparse.csr_matrix(lu.L)
+    U = sparse.csr_matrix(lu.U)
+    Ls = sparse.tril(L, k=-1, format="csr")
+    Us = sparse.triu(U, k=1, format="csr")
+    Ls.sort_indices()
+    Us.sort_indices()
+    diag = U.diagonal()
+    if np.any(diag == 0):
+        raise SingularSystemError("sparse factorization failed: zero pivot on the diagonal of U")
+    perm_r_inv = np.empty(b, dtype=np.int64)
+    perm_r_inv[lu.perm_r] = np.arange(b)
+    order_inv = np.empty(b, dtype=np.int64)
+    order_inv[order] = np.arange(b)
+    row_src = order[perm_r_inv]            # forward row k reads node row_src[k]
+    col_dst = lu.perm_c[order_inv]         # node i is solution index col_dst[i]
+    return TreeLU(
+        b=b,
+        l_ptr=Ls.indptr.astype(np.int32), l_col=Ls.indices.astype(np.int32),
+        l_val=np.ascontiguousarray(Ls.data.astype(complex)),
+        u_ptr=Us.indptr.astype(np.int32), u_col=Us.indices.astype(np.int32),
+        u_val=np.ascontiguousarray(Us.data.astype(complex)),
+        u_diag_inv=np.ascontiguousarray(1.0 / diag),
+        perm=np.concatenate([row_src, col_dst]).astype(np.int32),
+        ordering=kind)
+
+
+def lu_solve_host(f: TreeLU, rhs: np.ndarray) -> np.ndarray:
+    """Numpy emulation of the kernel's sweep order (host-logic tests only)."""
+    b = f.b
+    z = np.zeros(b, dtype=complex)
+    for k in range(b):
+        acc = rhs[f.perm[k]]
+        for p in range(f.l_ptr[k], f.l_ptr[k + 1]):
+            acc -= f.l_val[p] * z[f.l_col[p]]
+        z[k] = acc
+    for k in range(b - 1, -1, -1):
+        acc = z[k]
+        for p in range(f.u_ptr[k], f.u_ptr[k + 1]):
+            acc -= f.u_val[p] * z[f.u_col[p]]
+        z[k] = acc * f.u_diag_inv[k]
+    return z[f.perm[b:]]
+
+
+class SparseOperator:
+    """One factorization of Y_dd resident on a device; ``solve`` iterates."""
+
+    def __init__(self, model, device=None):
+        self.device = require_cuda(device)
+        self.contract = ModelContract.of(model)
+        self.lu = factorize_ydd(self.contract.y_dd)
+        d = self.device
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)  # noqa: E731
+        f = self.lu
+        self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(f.l_val), u_ptr=t(f.u_ptr),
+                        u_col=t(f.u_col), u_val=t(f.u_val), u_diag_inv=t(f.u_diag_inv),
+                        perm=t(f.perm), src=t(self.contract.src))
+        self.v_flat = complex(abs(self.contract.v_s))
+        self._ws = None
+
+    @property
+    def b(self) -> int:
+        return self.contract.b
+
+    def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V=None, iters=None):
+        b, tau = S.shape
+        if b != self.b:
+            raise ValueError(f"load matrix has {b} rows, model has {self.b}")
+        if V is None:
+            V = torch.empty((b, tau), dtype=torch.complex128, device=self.device)
+        if iters is None:
+            iters = torch.empty(tau, dtype=torch.int32, device=self.device)
+        need = int(_capi.load().tpf_sparse_workspace_bytes(tau, b))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        sn, sc = complex_strides(S)
+        vn, vc = complex_strides(V)
+        g = self.dev
+        _capi.call("tpf_sparse_fpi_c128", tau, b, S.data_ptr(), sn, sc,
+                   g["l_ptr"].data_ptr(), g["l_col"].data_ptr(), g["l_val"].data_ptr(),
+                   g["u_ptr"].data_ptr(), g["u_col"].data_ptr(), g["u_val"].data_ptr(),
+                   g["u_diag_inv"].data_ptr(), g["perm"].data_ptr(), g["src"].data_ptr(),
+                   self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                   V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                   stream_ptr(self.device))
+        return V, iters
+
+
+def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
+                       max_nnz: int | None = None, *, device=None,
+                       return_on_device: bool = False) -> VoltageBatch:
+    """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring."""
+    if not isinstance(loads, LoadMatrix):
+        loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
+    if not model.zip.is_constant_power:
+        raise ValueError("the sparse batch path supports constant-power loads only")
+    if loads.n_demand != model.n_demand:
+        raise ValueError(f"load matrix has {loads.n_demand} rows, model has {model.n_demand}")
+    if max_nnz is not None:
+        total = int(model.admittance.y_dd.nnz) * loads.tau
+        if total > max_nnz:
+            raise MemoryGuardError(
+                f"block system would hold {total} nonzeros (> {max_nnz}); "
+                "chunk the batch over cases and solve the chunks separately")
+    op = SparseOperator(model, device)
+    S = loads_to_device(loads.values, op.device)
+    V, iters = op.solve(S, opts)
+    resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
+    return finish(V, iters, resid, mask, summ, return_on_device)

@@ -1,0 +1,115 @@
+"""Host-side logic of the boundary: types, validation, LU preparation.
+
+All CPU; no kernels are launched."""
+
+import numpy as np
+import pytest
+from scipy import sparse
+
+from paper_2403_04578_b200 import (GenSpec, LoadMatrix, PowerTensor, SingularSystemError,
+                                   SolveOptions, VoltageBatch, build_network, factorize_ydd,
+                                   reshape_tensor, unreshape, batch_solve_dense, batch_solve_sparse,
+                                   solve_batch, NetworkModel, ZipCoefficients, MemoryGuardError)
+from paper_2403_04578_b200.sparse import leaf_first_order, lu_solve_host
+
+
+class TestTypes:
+    def test_fig4_layout(self):
+        # test_dense.py:21-35: case (i,j,k) lands in column i*6 + j*3 + k
+        rng = np.random.default_rng(0)
+        t = PowerTensor(rng.standard_normal((2, 2, 3, 3)) * (1 + 1j))
+        loads = reshape_tensor(t)
+        assert loads.values.shape == (3, 12)
+        for i in range(2):
+            for j in range(2):
+                for k in range(3):
+                    assert np.array_equal(loads.values[:, i * 6 + j * 3 + k], t.values[i, j, k, :])
+
+    def test_round_trip(self):
+        rng = np.random.default_rng(1)
+        t = PowerTensor(rng.standard_normal((4, 2, 5, 6)) + 1j * rng.standard_normal((4, 2, 5, 6)))
+        back = unreshape(reshape_tensor(t))
+        assert np.array_equal(back.values, t.values) and back.dims == t.dims
+
+    def test_options_validation(self):
+        with pytest.raises(ValueError):
+            SolveOptions(tolerance=0)
+        with pytest.raises(ValueError):
+            SolveOptions(max_iterations=0)
+
+    def test_voltage_batch_accessors(self):
+        vb = VoltageBatch(values=np.array([[0.5 + 0.5j, 1.0 + 0j]]), iterations=3,
+                          converged_mask=np.array([True, True]), residuals=np.zeros(2))
+        assert vb.tau == 2
+        assert vb.magnitudes()[0, 0] == pytest.approx(np.sqrt(0.5))
+        assert vb.angles()[0, 0] == pytest.approx(np.pi / 4)
+
+
+class TestBoundaryErrors:
+    """Errors the reference raises before any arithmetic (dense.py:143-148, sparse.py:121-136)."""
+
+    def test_row_count_mismatch(self):
+        m = build_network(GenSpec(n_buses=9, seed=42))
+        with pytest.raises(ValueError, match="rows"):
+            batch_solve_dense(m, LoadMatrix([[0.1 + 0j]]))
+        with pytest.raises(ValueError, match="rows"):
+            batch_solve_sparse(m, LoadMatrix([[0.1 + 0j]]))
+
+    def test_zip_models(self):
+        m = build_network(GenSpec(n_buses=9, seed=42))
+        b = m.n_demand
+        zm = NetworkModel(admittance=m.admittance, slack=m.slack,
+                          zip=ZipCoefficients(np.full(b, 0.2), np.full(b, 0.1), np.full(b, 0.7)))
+        loads = LoadMatrix(np.full((b, 2), 0.01 + 0j))
+        with pytest.raises(NotImplementedError, match="fpi_solve"):
+            batch_solve_dense(zm, loads)
+        with pytest.raises(ValueError, match="constant-power"):
+            batch_solve_sparse(zm, loads)
+
+    def test_memory_guard(self):
+        m = build_network(GenSpec(n_buses=9, seed=42))
+        loads = LoadMatrix(np.full((8, 50), 0.01 + 0j))
+        with pytest.raises(MemoryGuardError, match="chunk"):
+            batch_solve_sparse(m, loads, max_nnz=100)
+
+    def test_dispatcher(self):
+        m = build_network(GenSpec(n_buses=9, seed=42))
+        with pytest.raises(ValueError, match="unknown method"):
+            solve_batch("bogus", m, LoadMatrix(np.zeros((8, 1), complex)))
+        with pytest.raises(NotImplementedError):
+            solve_batch("nr", m, LoadMatrix(np.zeros((8, 1), complex)))
+
+
+class TestTreeLU:
+    @pytest.mark.parametrize("n_buses", [2, 9, 101, 1001])
+    def test_leaf_first_lu_has_no_fill_and_solves(self, n_buses):
+        m = build_network(GenSpec(n_buses=n_buses, seed=3))
+        y = m.admittance.y_dd
+        f = factorize_ydd(y)
+        b = m.n_demand
+        assert f.ordering == "leaf-first"
+        # zero fill: strictly-lower + strictly-upper entries == off-diagonals of Y_dd
+        assert f.l_col.size + f.u_col.size == y.nnz - b
+        rng = np.random.default_rng(n_buses)
+        r = rng.standard_normal(b) + 1j * rng.standard_normal(b)
+        x = lu_solve_host(f, r)
+        assert np.abs(y @ x - r).max() / np.abs(r).max() < 1e-12
+
+    def test_general_matrix_uses_colamd_with_pivoting(self):
+        rng = np.random.default_rng(18)
+        n = 6
+        y = rng.normal(0, 1, (n, n)) + 1j * rng.normal(0, 1, (n, n))
+        np.fill_diagonal(y, 0)
+        np.fill_diagonal(y, np.abs(y).sum(axis=1) + 20.0)
+        f = factorize_ydd(sparse.csc_matrix(y))
+        assert f.ordering == "colamd"
+        r = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        assert np.abs(y @ lu_solve_host(f, r) - r).max() < 1e-12
+
+    def test_singular_names_location(self):
+        with pytest.raises(SingularSystemError, match=r"rows \[1\]"):
+            factorize_ydd(sparse.csc_matrix(np.array([[1.0, 0.0], [0.0, 0.0]])))
+
+    def test_leaf_first_detects_cycles(self):
+        y = sparse.csr_matrix(np.ones((3, 3)) + 2 * np.eye(3))
+        assert leaf_first_order(y) is None
