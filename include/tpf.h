@@ -56,7 +56,7 @@ const char* tpf_last_error(void);
  *     V <- K (S* ./ conj(V)) + W,   K = -inv(Y_dd) (dense.py:151),
  *                                   W = K (Y_ds v_s) (dense.py:152).
  * FP64 tensor-core (DMMA) kernel with K resident in shared memory:
- * requires b <= tpf_dense_max_nodes() (104).  Larger b: tpf_dense_fpi_large_c128.
+ * requires b <= tpf_dense_max_nodes() (104); larger b: the _large_ entry below.
  *   S      b x tau complex loads (consumption positive), device
  *   K      b x b complex, row-major, device
  *   W      b complex, device
@@ -74,6 +74,21 @@ int tpf_dense_fpi_c128(int64_t tau, int32_t b,
                        double* V, int64_t v_node_stride, int64_t v_case_stride,
                        int32_t* iters, void* workspace, size_t workspace_bytes,
                        void* stream);
+
+/* Dense TPF for b > 104 (K streamed from L2; config C5, b = 1,000): an
+ * iteration-synchronous loop over a compacted active set of unconverged cases,
+ * tiled FP64-DMMA GEMM per iteration.  Same arguments and semantics as
+ * tpf_dense_fpi_c128; works for any b >= 1.
+ *   workspace >= tpf_dense_large_workspace_bytes(tau, b) device bytes      */
+size_t tpf_dense_large_workspace_bytes(int64_t tau, int32_t b);
+int tpf_dense_fpi_large_c128(int64_t tau, int32_t b,
+                             const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                             const double* K, const double* W,
+                             double v_flat_re, double v_flat_im,
+                             double tol, int32_t max_iter,
+                             double* V, int64_t v_node_stride, int64_t v_case_stride,
+                             int32_t* iters, void* workspace, size_t workspace_bytes,
+                             void* stream);
 
 /* --------------------------------------------------------------- sparse --
  * Replaces the hot loop of batch_solve_sparse (sparse.py:186-197), which
@@ -117,6 +132,38 @@ int tpf_residual_c128(int64_t tau, int32_t b,
  * out[1] = number of converged cases.  out must be 2 int32 of device memory. */
 int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
                       double residual_tol, uint8_t* mask, int32_t* out, void* stream);
+
+/* ------------------------------------------------------- host pipelines --
+ * The whole batch_solve_dense / batch_solve_sparse call on HOST buffers
+ * (the reference's LoadMatrix in, VoltageBatch arrays out): H2D of S, the
+ * iteration, the residual post-check and the D2H of V run in tau-chunks on
+ * three CUDA streams so PCIe transfers overlap the solve.  Host S and V must be
+ * node-major (case stride 1, the reference layout) or case-major (node stride
+ * 1); pageable buffers are page-locked for the duration of the call.
+ * K, W, Y_dd CSR, src and the LU arrays are host arrays (as in the _c128
+ * entry points).  iters/resid/mask may be NULL; summary (2 int32, host) gets
+ * {max iterations, converged count}.  chunk_cases <= 0 picks a default.
+ * Synchronous: returns when every output is on the host.                  */
+int tpf_dense_solve_host_c128(int64_t tau, int32_t b,
+                              const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                              const double* K, const double* W,
+                              const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                              const double* src, double v_flat_re, double v_flat_im,
+                              double tol, int32_t max_iter, double residual_tol,
+                              double* V, int64_t v_node_stride, int64_t v_case_stride,
+                              int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
+                              int64_t chunk_cases, int32_t device);
+int tpf_sparse_solve_host_c128(int64_t tau, int32_t b,
+                               const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                               const int32_t* l_ptr, const int32_t* l_col, const double* l_val,
+                               const int32_t* u_ptr, const int32_t* u_col, const double* u_val,
+                               const double* u_diag_inv, const int32_t* perm,
+                               const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                               const double* src, double v_flat_re, double v_flat_im,
+                               double tol, int32_t max_iter, double residual_tol,
+                               double* V, int64_t v_node_stride, int64_t v_case_stride,
+                               int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
+                               int64_t chunk_cases, int32_t device);
 
 /* ----------------------------------------------------------------- probe --
  * FP64 tensor-core peak of the current device, measured with a DMMA-only

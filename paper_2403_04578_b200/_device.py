@@ -87,3 +87,28 @@ def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tens
     _capi.call("tpf_batch_summary", tau, iters.data_ptr(), resid.data_ptr(), float(residual_tol),
                mask.data_ptr(), summ.data_ptr(), st)
     return resid, mask, summ
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """Page-locked host array from torch's caching host allocator (DMA-able, reused)."""
+    tdt = {np.complex128: torch.complex128, np.float64: torch.float64, np.int32: torch.int32,
+           np.uint8: torch.uint8}[np.dtype(dtype).type]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
+def host_loads(values) -> tuple[np.ndarray, int, int]:
+    """The load matrix as C- or F-contiguous complex128 plus its complex strides."""
+    arr = np.asarray(values, dtype=np.complex128)
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        arr = np.ascontiguousarray(arr)
+    return arr, arr.strides[0] // 16, arr.strides[1] // 16
+
+
+def host_csr(contract: ModelContract):
+    y = contract.y_dd
+    return (np.ascontiguousarray(y.indptr, dtype=np.int32), np.ascontiguousarray(y.indices, dtype=np.int32),
+            np.ascontiguousarray(y.data, dtype=np.complex128))
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data

@@ -1,0 +1,292 @@
+// Dense Tensor Power Flow for feeders too large for a shared-memory-resident K
+// (b > 104; config C5 is b = 1,000, K = 16 MB, which lives in the 126 MB L2).
+//
+// Same update as tpf_dense.cu (dense.py:114-126), organised as an
+// iteration-synchronous loop over a compacted ACTIVE SET of cases, because
+// near voltage collapse the per-case iteration counts are heavy-tailed
+// (C5: batch 58 iterations, per-case mean 10.4): every iteration only the
+// still-unconverged cases enter the GEMM.
+//
+// Per iteration (three launches, all early-exit when the active set is empty):
+//   prep    U[k, a] = S*_{k,c} / conj(v_{k,c}) for active case c = act[a]
+//           (zero-voltage guard), node-major so the writes coalesce over a;
+//   gemm    V'[a, n] = W[n] + sum_k U[k, a] K[n, k] on FP64 tensor cores:
+//           64x64 complex CTA tiles, 16-node k-slabs double-buffered through
+//           shared memory with cp.async (zero-filled at the edges), 8 warps of
+//           32x16 complex each, 4 real DMMA.8x8x4 per complex fragment; the
+//           epilogue reads the old iterate, writes the new one in place and
+//           flags the case if any |dv|^2 >= tol^2 (or non-finite);
+//   compact count the update, keep flagged cases below max_iter.
+// The k-order of every dot product is fixed, so a case's bits do not depend
+// on its position in the active set (permutation / shard invariance).
+#include <climits>
+
+#include "tpf_common.cuh"
+#include "tpf_internal.h"
+
+namespace tpf {
+namespace {
+
+constexpr int TM = 64;   // cases per CTA tile
+constexpr int TN = 64;   // output nodes per CTA tile
+constexpr int TK = 16;   // input nodes per k-slab (4 k-steps)
+constexpr int KSTEPS = TK / 4;
+constexpr int MF = TM / 8, NF = TN / 8;
+constexpr int LTHREADS = 256;
+
+struct LargeArgs {
+  int64_t tau;
+  int b;
+  const double2* S;
+  int64_t s_node, s_case;
+  const double2* K;  // b x b row-major
+  const double2* W;
+  double2 v_flat;
+  double tol2;
+  int max_iter;
+  double2* V;
+  int64_t v_node, v_case;
+  int32_t* iters;
+  // workspace
+  int32_t* act[2];
+  int32_t* count;  // [2]: active counts of the two lists
+  int32_t* bad;    // per active position
+  double2* U;      // b x tau, node-major, ld = tau
+};
+
+__global__ void init_kernel(LargeArgs a) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j == 0) {
+    a.count[0] = int(a.tau);
+    a.count[1] = 0;
+  }
+  if (j >= a.tau) return;
+  a.act[0][j] = int(j);
+  a.iters[j] = 0;
+  for (int i = 0; i < a.b; ++i) a.V[i * a.v_node + j * a.v_case] = a.v_flat;
+}
+
+__global__ void prep_kernel(LargeArgs a, int cur) {
+  const int n_act = a.count[cur];
+  const int* act = a.act[cur];
+  // the output list of this iteration's compaction was the input of the previous one
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.count[cur ^ 1] = 0;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < int64_t(n_act) * a.b;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int k = int(idx / n_act);
+    const int p = int(idx - int64_t(k) * n_act);
+    const int c = act[p];
+    double2 v = a.V[k * a.v_node + int64_t(c) * a.v_case];
+    double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+    if (m2 < kZeroGuard2) {
+      v = make_double2(kZeroGuard, 0.0);
+      m2 = kZeroGuard * kZeroGuard;
+    }
+    const double2 s = __ldg(a.S + k * a.s_node + int64_t(c) * a.s_case);
+    const double r = 1.0 / m2;
+    const double ur = __fma_rn(s.x, v.x, s.y * v.y) * r;  // conj(s) v / |v|^2
+    const double ui = __fma_rn(s.x, v.y, -(s.y * v.x)) * r;
+    a.U[int64_t(k) * a.tau + p] = make_double2(ur, ui);
+    if (k == 0) a.bad[p] = 0;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = pred ? 16 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
+  const int n_act = a.count[cur];
+  const int m0 = blockIdx.x * TM;
+  if (m0 >= n_act) return;
+  const int n0 = blockIdx.y * TN;
+  const int b = a.b;
+  // fragment-ordered slabs: A[ks][mf][lane], B[ks][nf][lane]
+  extern __shared__ __align__(16) double2 dyn_smem[];
+  double2 (*As)[KSTEPS * MF * 32] = reinterpret_cast<double2 (*)[KSTEPS * MF * 32]>(dyn_smem);
+  double2 (*Bs)[KSTEPS * NF * 32] = reinterpret_cast<double2 (*)[KSTEPS * NF * 32]>(dyn_smem + 2 * KSTEPS * MF * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2;  // 0..1 -> 32 cases
+  const int wn = warp & 3;   // 0..3 -> 16 nodes
+
+  auto load_slab = [&](int stage, int k0) {
+    // A: TM x TK elements, element e: m = e % TM (fast, coalesced over cases), kk = e / TM
+    for (int e = tid; e < TM * TK; e += LTHREADS) {
+      const int m = e % TM, kk = e / TM;
+      const int gm = m0 + m, gk = k0 + kk;
+      const bool ok = gm < n_act && gk < b;
+      const double2* src = ok ? a.U + int64_t(gk) * a.tau + gm : a.U;
+      const int ks = kk >> 2, mf = m >> 3;
+      cp_async16(&As[stage][(ks * MF + mf) * 32 + (m & 7) * 4 + (kk & 3)], src, ok);
+    }
+    // B: K[n][k], element e: kk = e % TK (fast, contiguous in a K row), n = e / TK
+    for (int e = tid; e < TN * TK; e += LTHREADS) {
+      const int kk = e % TK, n = e / TK;
+      const int gn = n0 + n, gk = k0 + kk;
+      const bool ok = gn < b && gk < b;
+      const double2* src = ok ? a.K + int64_t(gn) * b + gk : a.K;
+      const int ks = kk >> 2, nf = n >> 3;
+      cp_async16(&Bs[stage][(ks * NF + nf) * 32 + (n & 7) * 4 + (kk & 3)], src, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  double cr[4][2][2], ci[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+  const int nslabs = (b + TK - 1) / TK;
+  load_slab(0, 0);
+  for (int s = 0; s < nslabs; ++s) {
+    const int stage = s & 1;
+    if (s + 1 < nslabs) {
+      load_slab(stage ^ 1, (s + 1) * TK);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      double2 af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[stage][(ks * MF + wm * 4 + i) * 32 + lane];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[stage][(ks * NF + wn * 2 + j) * 32 + lane];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double nui = neg_int(af[i].y);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma884(cr[i][j][0], cr[i][j][1], af[i].x, bf[j].x);
+          dmma884(ci[i][j][0], ci[i][j][1], af[i].x, bf[j].y);
+          dmma884(cr[i][j][0], cr[i][j][1], nui, bf[j].y);
+          dmma884(ci[i][j][0], ci[i][j][1], af[i].y, bf[j].x);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // epilogue: V' = acc + W, step test against the (guarded) old iterate, in-place update
+  const int* act = a.act[cur];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+    bool row_bad = false;
+    const bool mvalid = m < n_act;
+    const int c = mvalid ? act[m] : 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + e;
+        if (mvalid && n < b) {
+          double2* vp = a.V + n * a.v_node + int64_t(c) * a.v_case;
+          double2 old = *vp;
+          if (__fma_rn(old.x, old.x, old.y * old.y) < kZeroGuard2) old = make_double2(kZeroGuard, 0.0);
+          const double2 w = __ldg(a.W + n);
+          const double2 nv = make_double2(cr[i][j][e] + w.x, ci[i][j][e] + w.y);
+          const double dr = nv.x - old.x, di = nv.y - old.y;
+          if (!(__fma_rn(dr, dr, di * di) < a.tol2)) row_bad = true;
+          *vp = nv;
+        }
+      }
+    }
+    row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 1);
+    row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 2);
+    if (row_bad && mvalid && (lane & 3) == 0) atomicOr(a.bad + m, 1);
+  }
+}
+
+__global__ void compact_kernel(LargeArgs a, int cur) {
+  const int n_act = a.count[cur];
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_act) return;
+  const int c = a.act[cur][p];
+  const int it = a.iters[c] + 1;
+  a.iters[c] = it;
+  if (a.bad[p] && it < a.max_iter) {
+    const int q = atomicAdd(a.count + (cur ^ 1), 1);
+    a.act[cur ^ 1][q] = c;
+  }
+}
+
+}  // namespace
+}  // namespace tpf
+
+using namespace tpf;
+
+extern "C" size_t tpf_dense_large_workspace_bytes(int64_t tau, int32_t b) {
+  const size_t t = size_t(tau > 0 ? tau : 1);
+  return 256 + 3 * t * 4 + 64 + t * size_t(b) * 16 + 1024;
+}
+
+extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                        int64_t s_case_stride, const double* K, const double* W, double v_flat_re,
+                                        double v_flat_im, double tol, int32_t max_iter, double* V,
+                                        int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: need tau >= 0 and b >= 1");
+  if (tau > INT_MAX / 2) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: tau too large; shard it");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!S || !K || !W || !V || !iters || !workspace)
+    return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: null pointer");
+  if (workspace_bytes < tpf_dense_large_workspace_bytes(tau, b))
+    return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LargeArgs a;
+  a.tau = tau;
+  a.b = b;
+  a.S = reinterpret_cast<const double2*>(S);
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.K = reinterpret_cast<const double2*>(K);
+  a.W = reinterpret_cast<const double2*>(W);
+  a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = reinterpret_cast<double2*>(V);
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  char* w = static_cast<char*>(workspace);
+  auto take = [&](size_t n) {
+    char* p = w;
+    w += (n + 255) / 256 * 256;
+    return p;
+  };
+  a.count = reinterpret_cast<int32_t*>(take(64));
+  a.act[0] = reinterpret_cast<int32_t*>(take(size_t(tau) * 4));
+  a.act[1] = reinterpret_cast<int32_t*>(take(size_t(tau) * 4));
+  a.bad = reinterpret_cast<int32_t*>(take(size_t(tau) * 4));
+  a.U = reinterpret_cast<double2*>(take(size_t(tau) * b * 16));
+  if (size_t(w - static_cast<char*>(workspace)) > workspace_bytes)
+    return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: workspace too small");
+
+  const unsigned tb = unsigned((tau + 255) / 256);
+  init_kernel<<<tb, 256, 0, st>>>(a);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const dim3 ggrid(unsigned((tau + TM - 1) / TM), unsigned((b + TN - 1) / TN));
+  const unsigned pgrid = unsigned(sms) * 8;
+  const int gsmem = int(2 * KSTEPS * (MF + NF) * 32 * sizeof(double2));
+  cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
+  if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(gemm_kernel)", aerr);
+  for (int it = 0; it < max_iter; ++it) {
+    const int cur = it & 1;
+    prep_kernel<<<pgrid, 256, 0, st>>>(a, cur);
+    gemm_kernel<<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
+    compact_kernel<<<tb, 256, 0, st>>>(a, cur);
+  }
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(dense large)", err);
+  return TPF_OK;
+}

@@ -1,0 +1,380 @@
+// End-to-end host pipeline: the C-ABI entry points that take HOST buffers.
+//
+// A full reference-sized batch (C2: 841 MB of loads in, 841 MB of voltages out)
+// is moved over PCIe in tau-chunks on three streams so that the H2D copy of
+// chunk i+1, the solve of chunk i and the D2H copy of chunk i-1 overlap:
+//
+//   in   : [H2D 0][H2D 1][H2D 2] ...
+//   comp :        [solve 0][solve 1] ...      (iteration kernel + residual)
+//   out  :                 [D2H 0 ][D2H 1 ] ...
+//
+// Two device slots per stream stage; events order slot reuse.  Per-case
+// outputs (iters, residuals, mask) stay device-resident until one final
+// summary kernel and copy.  Pageable host buffers are page-locked in place for
+// the duration of the call (cudaHostRegister) so every copy is a DMA.
+#include <cstring>
+#include <vector>
+
+#include "tpf_common.cuh"
+#include "tpf_internal.h"
+
+namespace tpf {
+namespace {
+
+struct HostPin {
+  void* ptr = nullptr;
+  bool registered = false;
+  int pin(const void* p, size_t bytes, bool read_only) {
+    cudaPointerAttributes attr;
+    cudaError_t err = cudaPointerGetAttributes(&attr, p);
+    if (err == cudaSuccess && (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged)) return TPF_OK;
+    cudaGetLastError();  // clear a pageable-pointer query error
+    unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+    err = cudaHostRegister(const_cast<void*>(p), bytes, flags);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      return TPF_OK;  // fall back to pageable copies (correct, slower)
+    }
+    ptr = const_cast<void*>(p);
+    registered = true;
+    return TPF_OK;
+  }
+  ~HostPin() {
+    if (registered) cudaHostUnregister(ptr);
+  }
+};
+
+// Layout of a b x tau complex host matrix: either node-major (case stride 1,
+// the reference LoadMatrix / VoltageBatch layout) or case-major (node stride 1).
+struct HostLayout {
+  bool case_contig;  // case stride == 1
+  int64_t ld;        // stride of the other index
+  int ok(int64_t b, int64_t tau, int64_t node_stride, int64_t case_stride) {
+    if (case_stride == 1 && node_stride >= tau) {
+      case_contig = true;
+      ld = node_stride;
+      return 1;
+    }
+    if (node_stride == 1 && case_stride >= b) {
+      case_contig = false;
+      ld = case_stride;
+      return 1;
+    }
+    return 0;
+  }
+  size_t span_bytes(int64_t b, int64_t tau) const {
+    return case_contig ? size_t(ld) * (b - 1) * 16 + size_t(tau) * 16 : size_t(ld) * (tau - 1) * 16 + size_t(b) * 16;
+  }
+};
+
+// Copy cases [lo, hi) between a host matrix and a device chunk buffer laid out
+// the same way (node-major chunk: ld = chunk; case-major chunk: ld = b).
+cudaError_t copy_chunk(bool h2d, const HostLayout& L, double* host, double* dev, int64_t b, int64_t lo, int64_t n,
+                       int64_t chunk, cudaStream_t st) {
+  if (L.case_contig) {
+    char* h = reinterpret_cast<char*>(host) + size_t(lo) * 16;
+    if (h2d)
+      return cudaMemcpy2DAsync(dev, size_t(chunk) * 16, h, size_t(L.ld) * 16, size_t(n) * 16, size_t(b),
+                               cudaMemcpyHostToDevice, st);
+    return cudaMemcpy2DAsync(h, size_t(L.ld) * 16, dev, size_t(chunk) * 16, size_t(n) * 16, size_t(b),
+                             cudaMemcpyDeviceToHost, st);
+  }
+  char* h = reinterpret_cast<char*>(host) + size_t(lo) * size_t(L.ld) * 16;
+  if (L.ld == b) {
+    return h2d ? cudaMemcpyAsync(dev, h, size_t(n) * b * 16, cudaMemcpyHostToDevice, st)
+               : cudaMemcpyAsync(h, dev, size_t(n) * b * 16, cudaMemcpyDeviceToHost, st);
+  }
+  if (h2d)
+    return cudaMemcpy2DAsync(dev, size_t(b) * 16, h, size_t(L.ld) * 16, size_t(b) * 16, size_t(n),
+                             cudaMemcpyHostToDevice, st);
+  return cudaMemcpy2DAsync(h, size_t(L.ld) * 16, dev, size_t(b) * 16, size_t(b) * 16, size_t(n),
+                           cudaMemcpyDeviceToHost, st);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Streams {
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  bool ok = false;
+  cudaError_t init() {
+    for (auto& x : s) {
+      cudaError_t e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    for (int k = 0; k < 2; ++k) {
+      cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&comp_done[k], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
+    }
+    ok = true;
+    return cudaSuccess;
+  }
+  ~Streams() {
+    if (!ok) return;
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(in_done[k]);
+      cudaEventDestroy(comp_done[k]);
+      cudaEventDestroy(out_done[k]);
+    }
+    for (auto& x : s)
+      if (x) cudaStreamDestroy(x);
+  }
+};
+
+#define TPF_CK(expr, where)                           \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return set_cuda_error(where, _e); \
+  } while (0)
+
+template <class T>
+cudaError_t upload(DevBuf& d, const T* h, size_t n, cudaStream_t st) {
+  cudaError_t e = d.alloc(n * sizeof(T));
+  if (e != cudaSuccess || n == 0) return e;
+  return cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
+// Solver callback: run the iteration on device chunk (S_dev -> V_dev) for n cases.
+struct ChunkSolver {
+  virtual ~ChunkSolver() = default;
+  virtual int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc,
+                    int32_t* iters, cudaStream_t st) = 0;
+};
+
+int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64_t s_node, int64_t s_case,
+                 const int32_t* rp, const int32_t* ci, const double* yv, const double* src, double residual_tol,
+                 double* V, int64_t v_node, int64_t v_case, int32_t* iters, double* resid, uint8_t* mask,
+                 int32_t* summary, int64_t chunk, const Streams& ss, cudaStream_t setup) {
+  HostLayout LS, LV;
+  if (!LS.ok(b, tau, s_node, s_case)) return set_error(TPF_ERR_INVALID, "host S must be node-major or case-major");
+  if (!LV.ok(b, tau, v_node, v_case)) return set_error(TPF_ERR_INVALID, "host V must be node-major or case-major");
+  HostPin pin_s, pin_v, pin_i, pin_r, pin_m;
+  pin_s.pin(S, LS.span_bytes(b, tau), true);
+  pin_v.pin(V, LV.span_bytes(b, tau), false);
+  if (iters) pin_i.pin(iters, size_t(tau) * 4, false);
+  if (resid) pin_r.pin(resid, size_t(tau) * 8, false);
+  if (mask) pin_m.pin(mask, size_t(tau), false);
+
+  const int nnz = 0;
+  (void)nnz;
+  DevBuf d_rp, d_ci, d_yv, d_src, d_it, d_res, d_mask, d_sum, d_S[2], d_V[2];
+  int64_t ynnz = 0;
+  {
+    // row_ptr lives on the host: read nnz from it
+    ynnz = rp[b];
+  }
+  TPF_CK(upload(d_rp, rp, size_t(b) + 1, setup), "upload(row_ptr)");
+  TPF_CK(upload(d_ci, ci, size_t(ynnz), setup), "upload(col)");
+  TPF_CK(upload(d_yv, yv, size_t(ynnz) * 2, setup), "upload(val)");
+  TPF_CK(upload(d_src, src, size_t(b) * 2, setup), "upload(src)");
+  TPF_CK(d_it.alloc(size_t(tau) * 4), "cudaMalloc(iters)");
+  TPF_CK(d_res.alloc(size_t(tau) * 8), "cudaMalloc(resid)");
+  TPF_CK(d_mask.alloc(size_t(tau)), "cudaMalloc(mask)");
+  TPF_CK(d_sum.alloc(64), "cudaMalloc(summary)");
+  for (int k = 0; k < 2; ++k) {
+    TPF_CK(d_S[k].alloc(size_t(chunk) * b * 16), "cudaMalloc(S chunk)");
+    TPF_CK(d_V[k].alloc(size_t(chunk) * b * 16), "cudaMalloc(V chunk)");
+  }
+  cudaEvent_t setup_done;
+  TPF_CK(cudaEventCreateWithFlags(&setup_done, cudaEventDisableTiming), "cudaEventCreate");
+  cudaEventRecord(setup_done, setup);
+  cudaStream_t sin = ss.s[0], scomp = ss.s[1], sout = ss.s[2];
+  cudaStreamWaitEvent(scomp, setup_done, 0);
+  // device chunk strides mirror the host layout so each chunk copy is one 2-D DMA
+  const int64_t dsn_S = LS.case_contig ? chunk : 1, dsc_S = LS.case_contig ? 1 : b;
+  const int64_t dsn_V = LV.case_contig ? chunk : 1, dsc_V = LV.case_contig ? 1 : b;
+  const int64_t nchunks = (tau + chunk - 1) / chunk;
+  int rc = TPF_OK;
+  for (int64_t c = 0; c < nchunks && rc == TPF_OK; ++c) {
+    const int k = int(c & 1);
+    const int64_t lo = c * chunk, n = (tau - lo < chunk) ? tau - lo : chunk;
+    if (c >= 2) cudaStreamWaitEvent(sin, ss.comp_done[k], 0);
+    TPF_CK(copy_chunk(true, LS, const_cast<double*>(S), d_S[k].as<double>(), b, lo, n, chunk, sin), "H2D(S chunk)");
+    cudaEventRecord(ss.in_done[k], sin);
+    cudaStreamWaitEvent(scomp, ss.in_done[k], 0);
+    if (c >= 2) cudaStreamWaitEvent(scomp, ss.out_done[k], 0);
+    rc = solver.solve(n, d_S[k].as<double>(), dsn_S, dsc_S, d_V[k].as<double>(), dsn_V, dsc_V,
+                      d_it.as<int32_t>() + lo, scomp);
+    if (rc != TPF_OK) break;
+    rc = tpf_residual_c128(n, b, d_S[k].as<double>(), dsn_S, dsc_S, d_V[k].as<double>(), dsn_V, dsc_V,
+                           d_rp.as<int32_t>(), d_ci.as<int32_t>(), d_yv.as<double>(), d_src.as<double>(),
+                           d_res.as<double>() + lo, scomp);
+    if (rc != TPF_OK) break;
+    cudaEventRecord(ss.comp_done[k], scomp);
+    cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
+    TPF_CK(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
+    cudaEventRecord(ss.out_done[k], sout);
+  }
+  if (rc == TPF_OK) {
+    rc = tpf_batch_summary(tau, d_it.as<int32_t>(), d_res.as<double>(), residual_tol, d_mask.as<uint8_t>(),
+                           d_sum.as<int32_t>(), scomp);
+  }
+  if (rc == TPF_OK) {
+    cudaEvent_t fin;
+    cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+    cudaEventRecord(fin, scomp);
+    cudaStreamWaitEvent(sout, fin, 0);
+    if (iters) cudaMemcpyAsync(iters, d_it.p, size_t(tau) * 4, cudaMemcpyDeviceToHost, sout);
+    if (resid) cudaMemcpyAsync(resid, d_res.p, size_t(tau) * 8, cudaMemcpyDeviceToHost, sout);
+    if (mask) cudaMemcpyAsync(mask, d_mask.p, size_t(tau), cudaMemcpyDeviceToHost, sout);
+    if (summary) cudaMemcpyAsync(summary, d_sum.p, 8, cudaMemcpyDeviceToHost, sout);
+    cudaEventDestroy(fin);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(sin), e2 = cudaStreamSynchronize(scomp), e3 = cudaStreamSynchronize(sout);
+  cudaEventDestroy(setup_done);
+  if (rc != TPF_OK) return rc;
+  if (e1 != cudaSuccess) return set_cuda_error("pipeline(in)", e1);
+  if (e2 != cudaSuccess) return set_cuda_error("pipeline(compute)", e2);
+  if (e3 != cudaSuccess) return set_cuda_error("pipeline(out)", e3);
+  return TPF_OK;
+}
+
+int64_t pick_chunk(int64_t tau, int64_t requested) {
+  if (requested > 0) return requested < tau ? requested : (tau > 0 ? tau : 1);
+  int64_t c = (tau + 15) / 16;  // ~16 chunks: fill/drain costs ~1/8 of the transfer time
+  if (c < 16384) c = 16384;
+  c = (c + 4095) / 4096 * 4096;
+  return c < tau ? c : (tau > 0 ? tau : 1);
+}
+
+struct DenseChunk : ChunkSolver {
+  int b;
+  const double *K, *W;
+  double vre, vim, tol;
+  int max_iter;
+  void* ws;
+  size_t ws_bytes;
+  int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+            cudaStream_t st) override {
+    return tpf_dense_fpi_c128(n, b, S, sn, sc, K, W, vre, vim, tol, max_iter, V, vn, vc, it, ws, ws_bytes, st);
+  }
+};
+
+struct SparseChunk : ChunkSolver {
+  int b;
+  const int32_t *lp, *lc, *up, *uc, *perm;
+  const double *lv, *uv, *ud, *src;
+  double vre, vim, tol;
+  int max_iter;
+  void* ws;
+  size_t ws_bytes;
+  int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+            cudaStream_t st) override {
+    return tpf_sparse_fpi_c128(n, b, S, sn, sc, lp, lc, lv, up, uc, uv, ud, perm, src, vre, vim, tol, max_iter, V,
+                               vn, vc, it, ws, ws_bytes, st);
+  }
+};
+
+}  // namespace
+}  // namespace tpf
+
+using namespace tpf;
+
+extern "C" int tpf_dense_solve_host_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                         int64_t s_case_stride, const double* K, const double* W,
+                                         const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                         const double* ydd_val, const double* src, double v_flat_re,
+                                         double v_flat_im, double tol, int32_t max_iter, double residual_tol,
+                                         double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                         double* resid, uint8_t* mask, int32_t* summary, int64_t chunk_cases,
+                                         int32_t device) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_solve_host_c128: need tau >= 0, b >= 1");
+  if (!S || !K || !W || !ydd_row_ptr || !src || !V) return set_error(TPF_ERR_INVALID, "null pointer");
+  TPF_CK(cudaSetDevice(device), "cudaSetDevice");
+  if (summary) summary[0] = summary[1] = 0;
+  if (tau == 0) return TPF_OK;
+  Streams ss;
+  TPF_CK(ss.init(), "cudaStreamCreate");
+  const bool large = b > tpf_dense_max_nodes();
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  DevBuf dK, dW, dws;
+  TPF_CK(upload(dK, K, size_t(b) * b * 2, ss.s[1]), "upload(K)");
+  TPF_CK(upload(dW, W, size_t(b) * 2, ss.s[1]), "upload(W)");
+  size_t wsb = large ? tpf_dense_large_workspace_bytes(chunk, b) : tpf_dense_workspace_bytes(b);
+  TPF_CK(dws.alloc(wsb), "cudaMalloc(workspace)");
+  struct LargeChunk : DenseChunk {
+    int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+              cudaStream_t st) override {
+      return tpf_dense_fpi_large_c128(n, b, S, sn, sc, K, W, vre, vim, tol, max_iter, V, vn, vc, it, ws, ws_bytes,
+                                      st);
+    }
+  };
+  DenseChunk small_solver;
+  LargeChunk large_solver;
+  DenseChunk& sv = large ? static_cast<DenseChunk&>(large_solver) : small_solver;
+  sv.b = b;
+  sv.K = dK.as<double>();
+  sv.W = dW.as<double>();
+  sv.vre = v_flat_re;
+  sv.vim = v_flat_im;
+  sv.tol = tol;
+  sv.max_iter = max_iter;
+  sv.ws = dws.p;
+  sv.ws_bytes = wsb;
+  return run_pipeline(sv, tau, b, S, s_node_stride, s_case_stride, ydd_row_ptr, ydd_col, ydd_val, src, residual_tol,
+                      V, v_node_stride, v_case_stride, iters, resid, mask, summary, chunk, ss, ss.s[1]);
+}
+
+extern "C" int tpf_sparse_solve_host_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                          int64_t s_case_stride, const int32_t* l_ptr, const int32_t* l_col,
+                                          const double* l_val, const int32_t* u_ptr, const int32_t* u_col,
+                                          const double* u_val, const double* u_diag_inv, const int32_t* perm,
+                                          const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                          const double* ydd_val, const double* src, double v_flat_re,
+                                          double v_flat_im, double tol, int32_t max_iter, double residual_tol,
+                                          double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                          double* resid, uint8_t* mask, int32_t* summary, int64_t chunk_cases,
+                                          int32_t device) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_sparse_solve_host_c128: need tau >= 0, b >= 1");
+  if (!S || !l_ptr || !u_ptr || !perm || !ydd_row_ptr || !src || !V) return set_error(TPF_ERR_INVALID, "null pointer");
+  TPF_CK(cudaSetDevice(device), "cudaSetDevice");
+  if (summary) summary[0] = summary[1] = 0;
+  if (tau == 0) return TPF_OK;
+  Streams ss;
+  TPF_CK(ss.init(), "cudaStreamCreate");
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t lnnz = l_ptr[b], unnz = u_ptr[b];
+  DevBuf dlp, dlc, dlv, dup, duc, duv, dud, dperm, dsrc, dws;
+  cudaStream_t st = ss.s[1];
+  TPF_CK(upload(dlp, l_ptr, size_t(b) + 1, st), "upload(L)");
+  TPF_CK(upload(dlc, l_col, size_t(lnnz), st), "upload(L)");
+  TPF_CK(upload(dlv, l_val, size_t(lnnz) * 2, st), "upload(L)");
+  TPF_CK(upload(dup, u_ptr, size_t(b) + 1, st), "upload(U)");
+  TPF_CK(upload(duc, u_col, size_t(unnz), st), "upload(U)");
+  TPF_CK(upload(duv, u_val, size_t(unnz) * 2, st), "upload(U)");
+  TPF_CK(upload(dud, u_diag_inv, size_t(b) * 2, st), "upload(U)");
+  TPF_CK(upload(dperm, perm, size_t(b) * 2, st), "upload(perm)");
+  TPF_CK(upload(dsrc, src, size_t(b) * 2, st), "upload(src)");
+  const size_t wsb = tpf_sparse_workspace_bytes(chunk, b);
+  TPF_CK(dws.alloc(wsb), "cudaMalloc(workspace)");
+  SparseChunk sv;
+  sv.b = b;
+  sv.lp = dlp.as<int32_t>();
+  sv.lc = dlc.as<int32_t>();
+  sv.lv = dlv.as<double>();
+  sv.up = dup.as<int32_t>();
+  sv.uc = duc.as<int32_t>();
+  sv.uv = duv.as<double>();
+  sv.ud = dud.as<double>();
+  sv.perm = dperm.as<int32_t>();
+  sv.src = dsrc.as<double>();
+  sv.vre = v_flat_re;
+  sv.vim = v_flat_im;
+  sv.tol = tol;
+  sv.max_iter = max_iter;
+  sv.ws = dws.p;
+  sv.ws_bytes = wsb;
+  return run_pipeline(sv, tau, b, S, s_node_stride, s_case_stride, ydd_row_ptr, ydd_col, ydd_val, src, residual_tol,
+                      V, v_node_stride, v_case_stride, iters, resid, mask, summary, chunk, ss, st);
+}

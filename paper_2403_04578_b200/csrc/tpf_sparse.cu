@@ -138,7 +138,7 @@ extern "C" int tpf_sparse_fpi_c128(int64_t tau, int32_t b, const double* S, int6
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
   if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
   if (tau == 0) return TPF_OK;
-  if (!S || !l_ptr || !u_ptr || !u_val || !u_diag_inv || !perm || !src || !V || !iters || !workspace)
+  if (!S || !l_ptr || !u_ptr || !u_diag_inv || !perm || !src || !V || !iters || !workspace)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_fpi_c128: null pointer");
   if (workspace_bytes < tpf_sparse_workspace_bytes(tau, b))
     return set_error(TPF_ERR_INVALID, "tpf_sparse_fpi_c128: workspace too small");

@@ -23,8 +23,8 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, loads_to_device, require_cuda,
-                      residual_and_summary, stream_ptr)
+from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
+                      loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
 from ._types import LoadMatrix, SolveOptions, VoltageBatch
 
 __all__ = ["batch_solve_dense", "DenseOperator"]
@@ -88,8 +88,15 @@ class DenseOperator:
 
 
 def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
-                      workers: int = 1, *, device=None, return_on_device: bool = False) -> VoltageBatch:
-    """GPU ``batch_solve_dense`` (dense.py:129-205); see module docstring."""
+                      workers: int = 1, *, device=None, return_on_device: bool = False,
+                      chunk_cases: int = 0) -> VoltageBatch:
+    """GPU ``batch_solve_dense`` (dense.py:129-205); see module docstring.
+
+    Host (numpy) loads go through the native chunked H2D/solve/D2H pipeline
+    (``tpf_dense_solve_host_c128``) and come back as numpy arrays.  With
+    ``return_on_device=True`` the loads are copied once and the result stays
+    on the device as torch tensors.
+    """
     del workers  # accepted for signature compatibility; partitioning never changes bits
     if not isinstance(loads, LoadMatrix):
         loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
@@ -99,6 +106,8 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
         raise NotImplementedError(
             "mixed ZIP loads are not on the batched hot path; the reference routes them "
             "through its single-case solver (tpflow.dense._batch_via_single -> fpi_solve)")
+    if not return_on_device:
+        return _solve_host_pipeline(model, loads, opts, device, chunk_cases)
     op = DenseOperator(model, device)
     S = loads_to_device(loads.values, op.device)
     V, iters = op.solve(S, opts)
@@ -114,3 +123,25 @@ def finish(V, iters, resid, mask, summ, on_device: bool) -> VoltageBatch:
     return VoltageBatch(values=V.cpu().numpy(), iterations=int(summ_h[0]),
                         converged_mask=mask.cpu().numpy().astype(bool),
                         residuals=resid.cpu().numpy(), iterations_per_case=iters.cpu().numpy())
+
+
+def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int):
+    dev = require_cuda(device)
+    c = ModelContract.of(model)
+    K = np.ascontiguousarray(-np.linalg.inv(c.y_dd.toarray()))  # dense.py:151
+    W = np.ascontiguousarray(K @ c.src)                          # dense.py:152
+    rp, ci, yv = host_csr(c)
+    S, sn, sc = host_loads(loads.values)
+    b, tau = S.shape
+    V = host_empty((b, tau), np.complex128)  # C-contiguous like dense.py:201
+    iters = host_empty((tau,), np.int32)
+    resid = host_empty((tau,), np.float64)
+    mask = host_empty((tau,), np.uint8)
+    summ = np.zeros(2, dtype=np.int32)
+    v_flat = complex(abs(c.v_s))
+    _capi.call("tpf_dense_solve_host_c128", tau, b, ptr(S), sn, sc, ptr(K), ptr(W), ptr(rp), ptr(ci),
+               ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
+               int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
+               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index)
+    return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
+                        residuals=resid, iterations_per_case=iters)

@@ -32,8 +32,8 @@ from scipy import sparse
 from scipy.sparse.linalg import splu
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, loads_to_device, require_cuda,
-                      residual_and_summary, stream_ptr)
+from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
+                      loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
 from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
 from .dense import finish
 
@@ -185,7 +185,11 @@ class SparseOperator:
         self.contract = ModelContract.of(model)
         self.lu = factorize_ydd(self.contract.y_dd)
         d = self.device
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(d)  # noqa: E731
+        def t(a):  # never hand a 0-element (null) buffer to the C ABI
+            a = np.ascontiguousarray(a)
+            if a.size == 0:
+                a = np.zeros(1, dtype=a.dtype)
+            return torch.from_numpy(a).to(d)
         f = self.lu
         self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(f.l_val), u_ptr=t(f.u_ptr),
                         u_col=t(f.u_col), u_val=t(f.u_val), u_diag_inv=t(f.u_diag_inv),
@@ -223,7 +227,7 @@ class SparseOperator:
 
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
                        max_nnz: int | None = None, *, device=None,
-                       return_on_device: bool = False) -> VoltageBatch:
+                       return_on_device: bool = False, chunk_cases: int = 0) -> VoltageBatch:
     """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring."""
     if not isinstance(loads, LoadMatrix):
         loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
@@ -237,8 +241,38 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
             raise MemoryGuardError(
                 f"block system would hold {total} nonzeros (> {max_nnz}); "
                 "chunk the batch over cases and solve the chunks separately")
+    if not return_on_device:
+        return _solve_host_pipeline(model, loads, opts, device, chunk_cases)
     op = SparseOperator(model, device)
     S = loads_to_device(loads.values, op.device)
     V, iters = op.solve(S, opts)
     resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
     return finish(V, iters, resid, mask, summ, return_on_device)
+
+
+def _nonempty(a):
+    a = np.ascontiguousarray(a)
+    return a if a.size else np.zeros(1, dtype=a.dtype)
+
+
+def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int):
+    dev = require_cuda(device)
+    c = ModelContract.of(model)
+    f = factorize_ydd(c.y_dd)
+    rp, ci, yv = host_csr(c)
+    S, sn, sc = host_loads(loads.values)
+    b, tau = S.shape
+    V = host_empty((b, tau), np.complex128)
+    iters = host_empty((tau,), np.int32)
+    resid = host_empty((tau,), np.float64)
+    mask = host_empty((tau,), np.uint8)
+    summ = np.zeros(2, dtype=np.int32)
+    v_flat = complex(abs(c.v_s))
+    arrs = [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val, f.u_diag_inv,
+                                    f.perm)]
+    _capi.call("tpf_sparse_solve_host_c128", tau, b, ptr(S), sn, sc, *[ptr(x) for x in arrs],
+               ptr(rp), ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
+               int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
+               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index)
+    return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
+                        residuals=resid, iterations_per_case=iters)

@@ -139,3 +139,50 @@ def test_dense_full_c2_properties():
     Vg = V[:, torch.from_numpy(cols).cuda()].cpu().numpy()
     assert np.array_equal(it[cols], no)
     assert np.abs(Vg - Vo).max() < 1e-12
+
+
+def test_host_pipeline_matches_device_path_bitwise(golden):
+    """The native chunked H2D/solve/D2H pipeline (several chunks) == one device solve."""
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_dense
+    g = golden("c2_slice192")
+    host = batch_solve_dense(g.model, LoadMatrix(g.S), g.opts(), chunk_cases=50)
+    dev = batch_solve_dense(g.model, LoadMatrix(g.S), g.opts(), return_on_device=True)
+    assert np.array_equal(host.values, dev.values.cpu().numpy())
+    assert np.array_equal(host.iterations_per_case, dev.iterations_per_case.cpu().numpy())
+    assert np.array_equal(host.residuals, dev.residuals.cpu().numpy())
+    assert host.iterations == dev.iterations
+
+
+def test_large_b_c5_matches_reference(golden):
+    """b=1,000 near voltage collapse (config C5): active-set DMMA path vs reference."""
+    g = golden("c5_slice32")
+    out = solve(g)
+    assert out.iterations == int(g["dense_iterations"]) == 58
+    assert np.array_equal(out.converged_mask, g["dense_mask"])
+    assert np.abs(out.values - g["dense_V"]).max() <= V_TOL
+    y, src, v_s = g.args
+    V, n_case, mask, _ = orc.dense_per_case(y, src, v_s, g.S)
+    assert np.array_equal(out.iterations_per_case, n_case)
+    assert np.abs(out.values - V).max() < 1e-11
+
+
+def test_large_b_path_on_small_feeder_matches_small_kernel(golden):
+    """The generic large-b kernel agrees with the shared-memory kernel where both apply."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator
+    g = golden("acc3_b100_t100")
+    op = DenseOperator(g.model)
+    S = torch.from_numpy(g.S).cuda()
+    V1, it1 = op.solve(S)
+    op.large = True
+    V2, it2 = op.solve(S)
+    assert torch.equal(it1, it2)
+    assert (V1 - V2).abs().max().item() < 1e-13
+
+
+def test_large_b_permutation_invariance_bitwise(golden):
+    g = golden("c5_slice32")
+    perm = np.random.default_rng(5).permutation(g.S.shape[1])
+    a = solve(g)
+    b = solve(g, S=np.ascontiguousarray(g.S[:, perm]))
+    assert np.array_equal(b.values, a.values[:, perm])

@@ -68,3 +68,12 @@ def test_c3_feeder_per_case_vs_oracle(golden):
         assert ok and out.converged_mask[j]
         assert abs(int(out.iterations_per_case[j]) - n) <= 1
         assert np.abs(out.values[:, j] - v).max() < 1e-10
+
+
+def test_host_pipeline_matches_device_path_bitwise(golden):
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_sparse
+    g = golden("c1_slice512")
+    host = batch_solve_sparse(g.model, LoadMatrix(g.S), g.opts(), chunk_cases=100)
+    dev = batch_solve_sparse(g.model, LoadMatrix(g.S), g.opts(), return_on_device=True)
+    assert np.array_equal(host.values, dev.values.cpu().numpy())
+    assert np.array_equal(host.iterations_per_case, dev.iterations_per_case.cpu().numpy())
