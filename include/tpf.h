@@ -143,7 +143,12 @@ int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
  * K, W, Y_dd CSR, src and the LU arrays are host arrays (as in the _c128
  * entry points).  iters/resid/mask may be NULL; summary (2 int32, host) gets
  * {max iterations, converged count}.  chunk_cases <= 0 picks a default.
+ * workspace: device scratch of >= tpf_*_solve_host_workspace_bytes(...)
+ * bytes, or NULL to let the call cudaMalloc/cudaFree its own.
  * Synchronous: returns when every output is on the host.                  */
+size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz);
+size_t tpf_sparse_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz,
+                                             int64_t l_nnz, int64_t u_nnz);
 int tpf_dense_solve_host_c128(int64_t tau, int32_t b,
                               const double* S, int64_t s_node_stride, int64_t s_case_stride,
                               const double* K, const double* W,
@@ -152,7 +157,7 @@ int tpf_dense_solve_host_c128(int64_t tau, int32_t b,
                               double tol, int32_t max_iter, double residual_tol,
                               double* V, int64_t v_node_stride, int64_t v_case_stride,
                               int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
-                              int64_t chunk_cases, int32_t device);
+                              int64_t chunk_cases, int32_t device, void* workspace, size_t workspace_bytes);
 int tpf_sparse_solve_host_c128(int64_t tau, int32_t b,
                                const double* S, int64_t s_node_stride, int64_t s_case_stride,
                                const int32_t* l_ptr, const int32_t* l_col, const double* l_val,
@@ -163,7 +168,7 @@ int tpf_sparse_solve_host_c128(int64_t tau, int32_t b,
                                double tol, int32_t max_iter, double residual_tol,
                                double* V, int64_t v_node_stride, int64_t v_case_stride,
                                int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
-                               int64_t chunk_cases, int32_t device);
+                               int64_t chunk_cases, int32_t device, void* workspace, size_t workspace_bytes);
 
 /* ----------------------------------------------------------------- probe --
  * FP64 tensor-core peak of the current device, measured with a DMMA-only

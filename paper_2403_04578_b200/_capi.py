@@ -48,12 +48,14 @@ SIGNATURES = {
     "tpf_dense_solve_host_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
-        _c_ptr, _c_i64, _c_i32]),
+        _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
     "tpf_sparse_solve_host_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
-        _c_ptr, _c_i64, _c_i32]),
+        _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
+    "tpf_dense_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64]),
+    "tpf_sparse_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64, _c_i64, _c_i64]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),
 }
 

@@ -112,3 +112,16 @@ def host_csr(contract: ModelContract):
 
 def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
+
+
+_WS: dict = {}
+
+
+def device_workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+    """Grow-only per-device scratch reused across host-pipeline calls."""
+    ws = _WS.get(device)
+    if ws is None or ws.numel() < nbytes:
+        _WS.pop(device, None)
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+        _WS[device] = ws
+    return ws

@@ -145,11 +145,30 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     }
   };
 
+  // Warm L2 with this thread's entries of the case its slot will take next, so
+  // the refill load after a freeze hits L2 instead of HBM.
+  auto prefetch_case = [&](int c) {
+    if (c >= tau) return;
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int node = 8 * (nb0 + lb) + 2 * q + e;
+        if (lb < nbw && node < b) {
+          const double* p = a.S + 2 * (node * a.s_node + int64_t(c) * a.s_case);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
+  };
+
   // initial fill (refill #0)
   cid = next_ids[(pair * 8 + slot) * 2 + 0];
   refills = 1;
   if (cid >= tau) cid = INT_MAX;
   load_case(cid);
+  prefetch_case(next_ids[(pair * 8 + slot) * 2 + 1]);
+  bool want_prefetch = false;
 
   for (;;) {
     // ---------- elementwise: guard, keep old iterate, U = S*/conj(V) ----------
@@ -178,6 +197,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       }
     }
     named_bar(bar_id, 64);  // U complete for both halves
+    if (want_prefetch) {  // the ring entry written after the last refill is visible now
+      prefetch_case(next_ids[(pair * 8 + slot) * 2 + (refills & 1)]);
+      want_prefetch = false;
+    }
 
     // ---------- GEMM: V' = W + U K^T on FP64 tensor cores ----------
 #pragma unroll
@@ -259,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       cid = (nc < tau) ? nc : INT_MAX;
       n_it = 0;
       load_case(cid);
+      want_prefetch = cid != INT_MAX;
     }
     if (__all_sync(0xffffffffu, cid == INT_MAX)) break;
   }

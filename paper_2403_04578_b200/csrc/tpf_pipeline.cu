@@ -91,12 +91,32 @@ cudaError_t copy_chunk(bool h2d, const HostLayout& L, double* host, double* dev,
                            cudaMemcpyDeviceToHost, st);
 }
 
+// Device buffer carved from a caller workspace (no allocation) or, when the
+// caller passes none, owned via cudaMalloc/cudaFree.
+struct Arena {
+  char* base = nullptr;
+  size_t size = 0, used = 0;
+};
+thread_local Arena* g_arena = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
+  bool owned = false;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (owned && p) cudaFree(p);
   }
-  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
+  cudaError_t alloc(size_t n) {
+    n = (n ? n : 16);
+    if (g_arena) {
+      const size_t need = (n + 255) / 256 * 256;
+      if (g_arena->used + need > g_arena->size) return cudaErrorMemoryAllocation;
+      p = g_arena->base + g_arena->used;
+      g_arena->used += need;
+      return cudaSuccess;
+    }
+    owned = true;
+    return cudaMalloc(&p, n);
+  }
   template <class T>
   T* as() const {
     return static_cast<T*>(p);
@@ -240,6 +260,27 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
   return TPF_OK;
 }
 
+struct ArenaScope {
+  Arena a;
+  ArenaScope(void* ws, size_t bytes) {
+    if (ws) {
+      a.base = static_cast<char*>(ws);
+      a.size = bytes;
+      g_arena = &a;
+    }
+  }
+  ~ArenaScope() { g_arena = nullptr; }
+};
+
+// Device bytes a host pipeline call carves from its workspace (see the
+// run_pipeline allocations): per-case outputs, two S and V chunk slots,
+// model arrays and the solver workspace.
+size_t pipeline_bytes(int64_t tau, int b, int64_t chunk, size_t model_bytes, size_t solver_ws) {
+  auto r = [](size_t n) { return (n + 255) / 256 * 256 + 256; };
+  return r(size_t(tau) * 4) + r(size_t(tau) * 8) + r(size_t(tau)) + r(64) + 4 * r(size_t(chunk) * b * 16) +
+         model_bytes + r(solver_ws) + 4096;
+}
+
 int64_t pick_chunk(int64_t tau, int64_t requested) {
   if (requested > 0) return requested < tau ? requested : (tau > 0 ? tau : 1);
   int64_t c = (tau + 15) / 16;  // ~16 chunks: fill/drain costs ~1/8 of the transfer time
@@ -281,6 +322,22 @@ struct SparseChunk : ChunkSolver {
 
 using namespace tpf;
 
+extern "C" size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
+                                                       int64_t ydd_nnz) {
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const bool large = b > tpf_dense_max_nodes();
+  const size_t solver = large ? tpf_dense_large_workspace_bytes(chunk, b) : tpf_dense_workspace_bytes(b);
+  const size_t model = size_t(b) * b * 16 + size_t(b) * 48 + size_t(ydd_nnz) * 20 + 16 * 512;
+  return pipeline_bytes(tau, b, chunk, model, solver);
+}
+
+extern "C" size_t tpf_sparse_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
+                                                        int64_t ydd_nnz, int64_t l_nnz, int64_t u_nnz) {
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const size_t model = size_t(b) * 64 + size_t(ydd_nnz + l_nnz + u_nnz) * 20 + 24 * 512;
+  return pipeline_bytes(tau, b, chunk, model, tpf_sparse_workspace_bytes(chunk, b));
+}
+
 extern "C" int tpf_dense_solve_host_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
                                          int64_t s_case_stride, const double* K, const double* W,
                                          const int32_t* ydd_row_ptr, const int32_t* ydd_col,
@@ -288,12 +345,15 @@ extern "C" int tpf_dense_solve_host_c128(int64_t tau, int32_t b, const double* S
                                          double v_flat_im, double tol, int32_t max_iter, double residual_tol,
                                          double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                                          double* resid, uint8_t* mask, int32_t* summary, int64_t chunk_cases,
-                                         int32_t device) {
+                                         int32_t device, void* workspace, size_t workspace_bytes) {
   if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_solve_host_c128: need tau >= 0, b >= 1");
   if (!S || !K || !W || !ydd_row_ptr || !src || !V) return set_error(TPF_ERR_INVALID, "null pointer");
   TPF_CK(cudaSetDevice(device), "cudaSetDevice");
   if (summary) summary[0] = summary[1] = 0;
   if (tau == 0) return TPF_OK;
+  if (workspace && workspace_bytes < tpf_dense_solve_host_workspace_bytes(tau, b, chunk_cases, ydd_row_ptr[b]))
+    return set_error(TPF_ERR_INVALID, "tpf_dense_solve_host_c128: workspace too small");
+  ArenaScope arena(workspace, workspace_bytes);
   Streams ss;
   TPF_CK(ss.init(), "cudaStreamCreate");
   const bool large = b > tpf_dense_max_nodes();
@@ -335,12 +395,16 @@ extern "C" int tpf_sparse_solve_host_c128(int64_t tau, int32_t b, const double* 
                                           double v_flat_im, double tol, int32_t max_iter, double residual_tol,
                                           double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                                           double* resid, uint8_t* mask, int32_t* summary, int64_t chunk_cases,
-                                          int32_t device) {
+                                          int32_t device, void* workspace, size_t workspace_bytes) {
   if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_sparse_solve_host_c128: need tau >= 0, b >= 1");
   if (!S || !l_ptr || !u_ptr || !perm || !ydd_row_ptr || !src || !V) return set_error(TPF_ERR_INVALID, "null pointer");
   TPF_CK(cudaSetDevice(device), "cudaSetDevice");
   if (summary) summary[0] = summary[1] = 0;
   if (tau == 0) return TPF_OK;
+  if (workspace && workspace_bytes < tpf_sparse_solve_host_workspace_bytes(tau, b, chunk_cases, ydd_row_ptr[b],
+                                                                            l_ptr[b], u_ptr[b]))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_solve_host_c128: workspace too small");
+  ArenaScope arena(workspace, workspace_bytes);
   Streams ss;
   TPF_CK(ss.init(), "cudaStreamCreate");
   const int64_t chunk = pick_chunk(tau, chunk_cases);

@@ -24,7 +24,7 @@ import torch
 
 from . import _capi
 from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
-                      loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
+                      device_workspace, loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
 from ._types import LoadMatrix, SolveOptions, VoltageBatch
 
 __all__ = ["batch_solve_dense", "DenseOperator"]
@@ -139,9 +139,12 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, c
     mask = host_empty((tau,), np.uint8)
     summ = np.zeros(2, dtype=np.int32)
     v_flat = complex(abs(c.v_s))
+    lib = _capi.load()
+    ws = device_workspace(dev, lib.tpf_dense_solve_host_workspace_bytes(tau, b, int(chunk_cases), yv.size))
+    torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
     _capi.call("tpf_dense_solve_host_c128", tau, b, ptr(S), sn, sc, ptr(K), ptr(W), ptr(rp), ptr(ci),
                ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
                int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
-               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index)
+               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
     return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
                         residuals=resid, iterations_per_case=iters)

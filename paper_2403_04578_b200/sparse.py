@@ -33,7 +33,7 @@ from scipy.sparse.linalg import splu
 
 from . import _capi
 from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
-                      loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
+                      device_workspace, loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
 from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
 from .dense import finish
 
@@ -270,9 +270,13 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, c
     v_flat = complex(abs(c.v_s))
     arrs = [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val, f.u_diag_inv,
                                     f.perm)]
+    lib = _capi.load()
+    ws = device_workspace(dev, lib.tpf_sparse_solve_host_workspace_bytes(
+        tau, b, int(chunk_cases), yv.size, f.l_col.size, f.u_col.size))
+    torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
     _capi.call("tpf_sparse_solve_host_c128", tau, b, ptr(S), sn, sc, *[ptr(x) for x in arrs],
                ptr(rp), ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
                int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
-               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index)
+               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
     return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
                         residuals=resid, iterations_per_case=iters)
