@@ -46,3 +46,42 @@ __device__ __forceinline__ double nanmax(double m, double x) {
 }
 
 }  // namespace tpf
+
+namespace tpf {
+// ---- Tensor Memory as a per-thread register extension (sm_100a) ----------
+// A warp may touch only its lane quadrant (warp % 4); with the 32x32b shape
+// thread t of the warp reads/writes TMEM lane 32*(warp%4)+t, N consecutive
+// 32-bit columns per instruction.
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(ncols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 4 doubles <-> 8 columns
+__device__ __forceinline__ void tmem_st4d(uint32_t taddr, double a, double b, double c, double d) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)), "r"(__double2hiint(b)),
+      "r"(__double2loint(c)), "r"(__double2hiint(c)), "r"(__double2loint(d)), "r"(__double2hiint(d))
+      : "memory");
+}
+struct D4 {
+  uint32_t r[8];
+  __device__ __forceinline__ double get(int i) const { return __hiloint2double(int(r[2 * i + 1]), int(r[2 * i])); }
+};
+__device__ __forceinline__ void tmem_ld4d(uint32_t taddr, D4& o) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(o.r[0]), "=r"(o.r[1]), "=r"(o.r[2]), "=r"(o.r[3]), "=r"(o.r[4]), "=r"(o.r[5]), "=r"(o.r[6]),
+                 "=r"(o.r[7])
+               : "r"(taddr)
+               : "memory");
+}
+}  // namespace tpf

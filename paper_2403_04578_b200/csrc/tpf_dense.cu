@@ -72,9 +72,53 @@ __device__ __forceinline__ int claim_case(unsigned long long* counter) {
   return c < (unsigned long long)INT_MAX ? int(c) : INT_MAX;
 }
 
+// One k-step of the complex GEMM for NBW node blocks: two passes so that the
+// two DMMAs accumulating into the same fragment are 2*NBW instructions apart.
+template <int NBH, int NBW>
+__device__ __forceinline__ void kstep(double (&vr)[NBH][2], double (&vi)[NBH][2], const double2& u,
+                                      const double2 (&kf)[NBW]) {
+  const double nui = neg_int(u.y);
+#pragma unroll
+  for (int lb = 0; lb < NBW; ++lb) {
+    dmma884(vr[lb][0], vr[lb][1], u.x, kf[lb].x);
+    dmma884(vi[lb][0], vi[lb][1], u.x, kf[lb].y);
+  }
+#pragma unroll
+  for (int lb = 0; lb < NBW; ++lb) {
+    dmma884(vr[lb][0], vr[lb][1], nui, kf[lb].y);
+    dmma884(vi[lb][0], vi[lb][1], u.y, kf[lb].x);
+  }
+}
+
+template <int NBW>
+__device__ __forceinline__ void load_frags(double2& u, double2 (&kf)[NBW], const double2* kb, const double2* ub,
+                                           int ks, int KS) {
+  u = ub[ks * 32];
+#pragma unroll
+  for (int lb = 0; lb < NBW; ++lb) kf[lb] = kb[(size_t(lb) * KS + ks) * 32];
+}
+
+// V' += U K^T for this warp's NBW node blocks; fragments ping-pong between two
+// register sets so the next k-step's shared-memory loads overlap the DMMAs.
+template <int NBH, int NBW>
+__device__ __forceinline__ void gemm_warp(double (&vr)[NBH][2], double (&vi)[NBH][2], const double2* kb,
+                                          const double2* ub, int KS) {
+  double2 u0, u1, k0[NBW], k1[NBW];
+  load_frags<NBW>(u0, k0, kb, ub, 0, KS);
+#pragma unroll 1
+  for (int ks = 0; ks < KS; ks += 2) {
+    const bool odd = ks + 1 < KS;
+    if (odd) load_frags<NBW>(u1, k1, kb, ub, ks + 1, KS);
+    kstep<NBH, NBW>(vr, vi, u0, k0);
+    if (ks + 2 < KS) load_frags<NBW>(u0, k0, kb, ub, ks + 2, KS);
+    if (odd) kstep<NBH, NBW>(vr, vi, u1, k1);
+  }
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs a) {
   constexpr int NBH = (NB + 1) / 2;  // max node blocks per warp
+  constexpr uint32_t kTmemCols = 256;  // 2 warps per lane quadrant x 128 columns
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int KS = a.ks_count;
   double2* k_sm = reinterpret_cast<double2*>(smem_raw);
@@ -82,16 +126,19 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
   double2* w_sm = u_all + size_t(kPairs) * KS * 32;
   uint32_t* flags = reinterpret_cast<uint32_t*>(w_sm + NB * 8);  // [pair][2]
   int* next_ids = reinterpret_cast<int*>(flags + 2 * kPairs);     // [pair][8 slots][2]
+  uint32_t* tmem_base_sm = reinterpret_cast<uint32_t*>(next_ids + kPairs * 16);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int pair = warp >> 1;
   const int half = warp & 1;
-  const int q = lane & 3;    // C-fragment column group: nodes 2q, 2q+1 of a block
+  const int q = lane & 3;      // C-fragment column group: nodes 2q, 2q+1 of a block
   const int slot = lane >> 2;  // C/A-fragment row: case slot 0..7
   const int b = a.b;
   const int64_t tau = a.tau;
+
+  if (warp == 0) tmem_alloc(tmem_base_sm, kTmemCols);
 
   // ---- stage K^T fragments and W into shared memory (once per launch) ----
   for (int idx = tid; idx < NB * KS * 32; idx += kThreads) {
@@ -104,15 +151,25 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     if (row < b && col < b) v = ldg_c128(a.K, int64_t(row) * b + col);
     k_sm[idx] = v;
   }
-  for (int i = tid; i < NB * 8; i += kThreads)
-    w_sm[i] = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
+  for (int i = tid; i < NB * 8; i += kThreads) {
+    const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
+    reinterpret_cast<double*>(w_sm)[i] = w.x;           // re plane
+    reinterpret_cast<double*>(w_sm)[NB * 8 + i] = w.y;  // im plane
+  }
 
   // ---- slot bookkeeping: two prefetched case ids per slot (ring of 2) ----
   if (half == 0 && lane < 8) {
     next_ids[(pair * 8 + lane) * 2 + 0] = claim_case(a.counter);
     next_ids[(pair * 8 + lane) * 2 + 1] = claim_case(a.counter);
   }
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+
+  // TMEM holds, per thread, S* (columns [0,8*NBH)) and the old iterate
+  // (columns [8*NBH, 16*NBH)) of its C-fragment entries: 4 doubles per block.
+  const uint32_t tm = *tmem_base_sm + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 128);
+  const uint32_t tm_s = tm, tm_o = tm + 8 * NBH;
 
   // this warp's node blocks (alternate the larger half between pairs)
   const int n_big = NBH, n_small = NB - NBH;
@@ -123,25 +180,33 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
   double2* u_sm = u_all + size_t(pair) * KS * 32;
   const int bar_id = 1 + pair;
 
-  // per-thread state: iterate (C layout), old iterate, S*
-  double vr[NBH][2], vi[NBH][2], orr[NBH][2], oi[NBH][2], sr[NBH][2], si[NBH][2];
+  double vr[NBH][2], vi[NBH][2];  // iterate / accumulators (C layout)
   int cid = INT_MAX;  // current case of my slot (INT_MAX = idle)
   int n_it = 0;       // updates applied to the current case
   int refills = 0;    // ring position
 
-  auto load_case = [&](int c) {
-#pragma unroll
-    for (int lb = 0; lb < NBH; ++lb) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int node = 8 * (nb0 + lb) + 2 * q + e;
-        double2 s = make_double2(0.0, 0.0);
-        if (lb < nbw && node < b && c < tau) s = ldg_c128(a.S, node * a.s_node + int64_t(c) * a.s_case);
-        sr[lb][e] = s.x;
-        si[lb][e] = -s.y;  // S* (dense.py:154)
-        vr[lb][e] = a.v_flat_re;
-        vi[lb][e] = a.v_flat_im;
+  // S* entries of case c for block lb of this thread (zeros for padding / idle)
+  auto fetch_s = [&](int c, int lb, double& s0r, double& s0i, double& s1r, double& s1i) {
+    s0r = s0i = s1r = s1i = 0.0;
+    const int node = 8 * (nb0 + lb) + 2 * q;
+    if (c < tau) {
+      if (node < b) {
+        const double2 s = ldg_c128(a.S, node * a.s_node + int64_t(c) * a.s_case);
+        s0r = s.x;
+        s0i = -s.y;  // S* (dense.py:154)
       }
+      if (node + 1 < b) {
+        const double2 s = ldg_c128(a.S, (node + 1) * a.s_node + int64_t(c) * a.s_case);
+        s1r = s.x;
+        s1i = -s.y;
+      }
+    }
+  };
+  auto flat_start = [&](int lb) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      vr[lb][e] = a.v_flat_re;
+      vi[lb][e] = a.v_flat_im;
     }
   };
 
@@ -166,36 +231,56 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
   cid = next_ids[(pair * 8 + slot) * 2 + 0];
   refills = 1;
   if (cid >= tau) cid = INT_MAX;
-  load_case(cid);
+#pragma unroll
+  for (int lb = 0; lb < NBH; ++lb) {
+    if (lb < nbw) {
+      double s0r, s0i, s1r, s1i;
+      fetch_s(cid, lb, s0r, s0i, s1r, s1i);
+      tmem_st4d(tm_s + 8 * lb, s0r, s1r, s0i, s1i);
+    }
+    flat_start(lb);
+  }
+  tmem_wait_st();
   prefetch_case(next_ids[(pair * 8 + slot) * 2 + 1]);
   bool want_prefetch = false;
 
   for (;;) {
     // ---------- elementwise: guard, keep old iterate, U = S*/conj(V) ----------
+    {
+      D4 sv[NBH];
 #pragma unroll
-    for (int lb = 0; lb < NBH; ++lb) {
-      if (lb < nbw) {
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_s + 8 * lb, sv[lb]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double xr = vr[lb][e], xi = vi[lb][e];
-          double m2 = __fma_rn(xr, xr, xi * xi);
-          if (m2 < kZeroGuard2) {  // fpi.py:39-41 / dense.py:170-172
-            xr = kZeroGuard;
-            xi = 0.0;
-            m2 = kZeroGuard * kZeroGuard;
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          double xr2[2], xi2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double xr = vr[lb][e], xi = vi[lb][e];
+            double m2 = __fma_rn(xr, xr, xi * xi);
+            if (m2 < kZeroGuard2) {  // fpi.py:39-41 / dense.py:170-172
+              xr = kZeroGuard;
+              xi = 0.0;
+              m2 = kZeroGuard * kZeroGuard;
+            }
+            xr2[e] = xr;
+            xi2[e] = xi;
+            // S*/conj(v) = S* v / |v|^2
+            const double srr = sv[lb].get(e), sii = sv[lb].get(2 + e);
+            const double r = 1.0 / m2;
+            const double ur = __fma_rn(srr, xr, -(sii * xi)) * r;
+            const double ui = __fma_rn(srr, xi, sii * xr) * r;
+            const int node = 8 * (nb0 + lb) + 2 * q + e;
+            const int ks = node >> 2;
+            if (ks < KS) u_sm[ks * 32 + slot * 4 + (node & 3)] = make_double2(ur, ui);
           }
-          orr[lb][e] = xr;
-          oi[lb][e] = xi;
-          // S*/conj(v) = S* v / |v|^2
-          const double r = 1.0 / m2;
-          const double ur = __fma_rn(sr[lb][e], xr, -(si[lb][e] * xi)) * r;
-          const double ui = __fma_rn(sr[lb][e], xi, si[lb][e] * xr) * r;
-          const int node = 8 * (nb0 + lb) + 2 * q + e;
-          const int ks = node >> 2;
-          if (ks < KS) u_sm[ks * 32 + slot * 4 + (node & 3)] = make_double2(ur, ui);
+          tmem_st4d(tm_o + 8 * lb, xr2[0], xr2[1], xi2[0], xi2[1]);
         }
       }
     }
+    tmem_wait_st();
     named_bar(bar_id, 64);  // U complete for both halves
     if (want_prefetch) {  // the ring entry written after the last refill is visible now
       prefetch_case(next_ids[(pair * 8 + slot) * 2 + (refills & 1)]);
@@ -206,44 +291,44 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
 #pragma unroll
     for (int lb = 0; lb < NBH; ++lb) {
       if (lb < nbw) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double2 w = w_sm[8 * (nb0 + lb) + 2 * q + e];
-          vr[lb][e] = w.x;
-          vi[lb][e] = w.y;
-        }
+        // (node 2q, 2q+1) pairs of each plane land directly in the DMMA register pairs
+        const double2 wr = w_sm[(8 * (nb0 + lb) + 2 * q) / 2];
+        const double2 wi = w_sm[(NB * 8 + 8 * (nb0 + lb) + 2 * q) / 2];
+        vr[lb][0] = wr.x;
+        vr[lb][1] = wr.y;
+        vi[lb][0] = wi.x;
+        vi[lb][1] = wi.y;
       }
     }
-    const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
-#pragma unroll 1
-    for (int ks = 0; ks < KS; ++ks) {
-      const double2 u = u_sm[ks * 32 + lane];
-      const double nui = neg_int(u.y);
-#pragma unroll
-      for (int lb = 0; lb < NBH; ++lb) {
-        if (lb < nbw) {
-          const double2 k = kb[(size_t(lb) * KS + ks) * 32];
-          dmma884(vr[lb][0], vr[lb][1], u.x, k.x);
-          dmma884(vi[lb][0], vi[lb][1], u.x, k.y);
-          dmma884(vr[lb][0], vr[lb][1], nui, k.y);
-          dmma884(vi[lb][0], vi[lb][1], u.y, k.x);
-        }
+    {
+      const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
+      if (nbw == NBH) {
+        gemm_warp<NBH, NBH>(vr, vi, kb, u_sm + lane, KS);
+      } else {
+        if constexpr (NB - NBH > 0) gemm_warp<NBH, NB - NBH>(vr, vi, kb, u_sm + lane, KS);
       }
     }
 
     // ---------- epilogue: per-case step test (dense.py:125-126, 189-193) ----------
     bool small = true;
+    {
+      D4 ov[NBH];
 #pragma unroll
-    for (int lb = 0; lb < NBH; ++lb) {
-      if (lb < nbw) {
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_o + 8 * lb, ov[lb]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int node = 8 * (nb0 + lb) + 2 * q + e;
-          const double dr = vr[lb][e] - orr[lb][e];
-          const double di = vi[lb][e] - oi[lb][e];
-          const double d2 = __fma_rn(dr, dr, di * di);
-          // NaN/inf never compare small: they hold the case open to the cap
-          if (node < b && !(d2 < a.tol2)) small = false;
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int node = 8 * (nb0 + lb) + 2 * q + e;
+            const double dr = vr[lb][e] - ov[lb].get(e);
+            const double di = vi[lb][e] - ov[lb].get(2 + e);
+            const double d2 = __fma_rn(dr, dr, di * di);
+            // NaN/inf never compare small: they hold the case open to the cap
+            if (node < b && !(d2 < a.tol2)) small = false;
+          }
         }
       }
     }
@@ -266,26 +351,51 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int node = 8 * (nb0 + lb) + 2 * q + e;
-            if (node < b) stg_c128(a.V, node * a.v_node + int64_t(cid) * a.v_case, make_double2(vr[lb][e], vi[lb][e]));
+            if (node < b) {  // two 8-byte stores: (re, im) are not a register pair
+              double* p = a.V + 2 * (node * a.v_node + int64_t(cid) * a.v_case);
+              p[0] = vr[lb][e];
+              p[1] = vi[lb][e];
+            }
           }
         }
       }
       if (half == 0 && q == 0) a.iters[cid] = n_it;
       // refill from the prefetch ring; warp 0 of the pair tops the ring up
       const int ring = (pair * 8 + slot) * 2;
-      int nc = next_ids[ring + (refills & 1)];
-      if (half == 0 && q == 0) {
-        next_ids[ring + ((refills + 1) & 1)] =
-            claim_case(a.counter);
-      }
+      const int nc = next_ids[ring + (refills & 1)];
+      if (half == 0 && q == 0) next_ids[ring + ((refills + 1) & 1)] = claim_case(a.counter);
       ++refills;
       cid = (nc < tau) ? nc : INT_MAX;
       n_it = 0;
-      load_case(cid);
       want_prefetch = cid != INT_MAX;
     }
+    // TMEM access is warp-collective (.sync.aligned): the whole warp rewrites
+    // S*, retiring lanes with their new case, the others with what they hold.
+    if (__any_sync(0xffffffffu, done)) {
+      D4 cur[NBH];
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_s + 8 * lb, cur[lb]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          double s0r = cur[lb].get(0), s1r = cur[lb].get(1), s0i = cur[lb].get(2), s1i = cur[lb].get(3);
+          if (done) {
+            fetch_s(cid, lb, s0r, s0i, s1r, s1i);
+            flat_start(lb);
+          }
+          tmem_st4d(tm_s + 8 * lb, s0r, s1r, s0i, s1i);
+        }
+      }
+    }
+    tmem_wait_st();
     if (__all_sync(0xffffffffu, cid == INT_MAX)) break;
   }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(*tmem_base_sm, kTmemCols);
 }
 
 template <int NB>
@@ -297,6 +407,7 @@ static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
   err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_fpi_kernel<NB>, kThreads, smem);
   if (err != cudaSuccess) return set_cuda_error("occupancy(dense)", err);
   if (per_sm < 1) return set_error(TPF_ERR_UNSUPPORTED, "dense kernel does not fit on an SM");
+  if (per_sm > 2) per_sm = 2;  // each CTA holds 256 of the SM's 512 TMEM columns
   // slots in flight = 8 per pair; never launch more CTAs than needed
   const int64_t slots_per_cta = 8 * kPairs;
   int64_t grid = int64_t(per_sm) * sm_count;
