@@ -345,7 +345,7 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world):
     pinned = torch.from_numpy(loads.values).pin_memory()
     host = LoadMatrix(pinned.numpy())
     solver = bsd if method == "dense" else bss
-    for _ in range(1):
+    for _ in range(3):  # populate torch's pinned-host cache for the result arrays
         solver(model, host, device=dev)
     torch.cuda.synchronize(dev)
     if world > 1:
