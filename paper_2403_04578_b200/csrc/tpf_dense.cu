@@ -36,7 +36,6 @@ namespace tpf {
 constexpr int kPairs = 4;          // warp pairs per CTA
 constexpr int kWarps = 2 * kPairs;  // 8 warps
 constexpr int kThreads = 32 * kWarps;
-constexpr int kChunk = 4;  // node blocks per TMEM round trip in the elementwise phases
 
 struct DenseArgs {
   int64_t tau;
@@ -99,57 +98,27 @@ __device__ __forceinline__ void load_frags(double2& u, double2 (&kf)[NBW], const
   for (int lb = 0; lb < NBW; ++lb) kf[lb] = kb[(size_t(lb) * KS + ks) * 32];
 }
 
-// Staging of the NEXT case's S* of a slot into TMEM, one node block per two
-// k-steps of the GEMM, so a refilled slot never waits on global memory.
-struct NextCasePrefetch {
-  const double* S;
-  int64_t s_node, s_case, tau;
-  int b, nb0, q, next;  // next = the case this lane's slot takes after the current one
-  uint32_t tm_n;        // TMEM columns of the staged S*
-  double r[4];
-  __device__ __forceinline__ void load(int lb) {
-    r[0] = r[1] = r[2] = r[3] = 0.0;
-    const int node = 8 * (nb0 + lb) + 2 * q;
-    if (next < tau) {
-      if (node < b) {
-        const double2 s = ldg_c128(S, node * s_node + int64_t(next) * s_case);
-        r[0] = s.x;
-        r[2] = -s.y;  // S* (dense.py:154)
-      }
-      if (node + 1 < b) {
-        const double2 s = ldg_c128(S, (node + 1) * s_node + int64_t(next) * s_case);
-        r[1] = s.x;
-        r[3] = -s.y;
-      }
-    }
-  }
-  __device__ __forceinline__ void store(int lb) { tmem_st4d(tm_n + 8 * lb, r[0], r[1], r[2], r[3]); }
-};
-
 // V' += U K^T for this warp's NBW node blocks; fragments ping-pong between two
 // register sets so the next k-step's shared-memory loads overlap the DMMAs.
 template <int NBH, int NBW>
 __device__ __forceinline__ void gemm_warp(double (&vr)[NBH][2], double (&vi)[NBH][2], const double2* kb,
-                                          const double2* ub, int KS, NextCasePrefetch& pf) {
+                                          const double2* ub, int KS) {
   double2 u0, u1, k0[NBW], k1[NBW];
   load_frags<NBW>(u0, k0, kb, ub, 0, KS);
 #pragma unroll 1
   for (int ks = 0; ks < KS; ks += 2) {
-    const int blk = ks >> 1;  // warp-uniform
-    if (blk < NBW) pf.load(blk);
     const bool odd = ks + 1 < KS;
     if (odd) load_frags<NBW>(u1, k1, kb, ub, ks + 1, KS);
     kstep<NBH, NBW>(vr, vi, u0, k0);
     if (ks + 2 < KS) load_frags<NBW>(u0, k0, kb, ub, ks + 2, KS);
     if (odd) kstep<NBH, NBW>(vr, vi, u1, k1);
-    if (blk < NBW) pf.store(blk);
   }
 }
 
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs a) {
   constexpr int NBH = (NB + 1) / 2;  // max node blocks per warp
-  constexpr uint32_t kTmemCols = 512;  // 2 warps per lane quadrant x 256 columns
+  constexpr uint32_t kTmemCols = 256;  // 2 warps per lane quadrant x 128 columns
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int KS = a.ks_count;
   double2* k_sm = reinterpret_cast<double2*>(smem_raw);
@@ -197,11 +166,10 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
   __syncthreads();
   tmem_fence_after();
 
-  // TMEM holds, per thread, S* (columns [0,8*NBH)), the old iterate
-  // ([8*NBH,16*NBH)) and the next case's S* ([16*NBH,24*NBH)) of its
-  // C-fragment entries: 4 doubles (re0, re1, im0, im1) per node block.
-  const uint32_t tm = *tmem_base_sm + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 256);
-  const uint32_t tm_s = tm, tm_o = tm + 8 * NBH, tm_n = tm + 16 * NBH;  // S*, old iterate, next S*
+  // TMEM holds, per thread, S* (columns [0,8*NBH)) and the old iterate
+  // (columns [8*NBH, 16*NBH)) of its C-fragment entries: 4 doubles per block.
+  const uint32_t tm = *tmem_base_sm + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 128);
+  const uint32_t tm_s = tm, tm_o = tm + 8 * NBH;
 
   // this warp's node blocks (alternate the larger half between pairs)
   const int n_big = NBH, n_small = NB - NBH;
@@ -242,6 +210,23 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     }
   };
 
+  // Warm L2 with this thread's entries of the case its slot will take next, so
+  // the refill load after a freeze hits L2 instead of HBM.
+  auto prefetch_case = [&](int c) {
+    if (c >= tau) return;
+#pragma unroll
+    for (int lb = 0; lb < NBH; ++lb) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int node = 8 * (nb0 + lb) + 2 * q + e;
+        if (lb < nbw && node < b) {
+          const double* p = a.S + 2 * (node * a.s_node + int64_t(c) * a.s_case);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
+  };
+
   // initial fill (refill #0)
   cid = next_ids[(pair * 8 + slot) * 2 + 0];
   refills = 1;
@@ -256,51 +241,51 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     flat_start(lb);
   }
   tmem_wait_st();
-  NextCasePrefetch pf{a.S, a.s_node, a.s_case, tau, b, nb0, q, INT_MAX, tm_n, {0.0, 0.0, 0.0, 0.0}};
+  prefetch_case(next_ids[(pair * 8 + slot) * 2 + 1]);
+  bool want_prefetch = false;
 
   for (;;) {
     // ---------- elementwise: guard, keep old iterate, U = S*/conj(V) ----------
     {
+      D4 sv[NBH];
 #pragma unroll
-      for (int c0 = 0; c0 < NBH; c0 += kChunk) {  // TMEM round trips in chunks of blocks
-        D4 sv[kChunk];
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_s + 8 * lb, sv[lb]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j)
-          if (c0 + j < NBH && c0 + j < nbw) tmem_ld4d(tm_s + 8 * (c0 + j), sv[j]);
-        tmem_wait_ld();
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          double xr2[2], xi2[2];
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int lb = c0 + j;
-          if (lb < NBH && lb < nbw) {
-            double xr2[2], xi2[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              double xr = vr[lb][e], xi = vi[lb][e];
-              double m2 = __fma_rn(xr, xr, xi * xi);
-              if (m2 < kZeroGuard2) {  // fpi.py:39-41 / dense.py:170-172
-                xr = kZeroGuard;
-                xi = 0.0;
-                m2 = kZeroGuard * kZeroGuard;
-              }
-              xr2[e] = xr;
-              xi2[e] = xi;
-              // S*/conj(v) = S* v / |v|^2
-              const double srr = sv[j].get(e), sii = sv[j].get(2 + e);
-              const double r = 1.0 / m2;
-              const double ur = __fma_rn(srr, xr, -(sii * xi)) * r;
-              const double ui = __fma_rn(srr, xi, sii * xr) * r;
-              const int node = 8 * (nb0 + lb) + 2 * q + e;
-              const int ks = node >> 2;
-              if (ks < KS) u_sm[ks * 32 + slot * 4 + (node & 3)] = make_double2(ur, ui);
+          for (int e = 0; e < 2; ++e) {
+            double xr = vr[lb][e], xi = vi[lb][e];
+            double m2 = __fma_rn(xr, xr, xi * xi);
+            if (m2 < kZeroGuard2) {  // fpi.py:39-41 / dense.py:170-172
+              xr = kZeroGuard;
+              xi = 0.0;
+              m2 = kZeroGuard * kZeroGuard;
             }
-            tmem_st4d(tm_o + 8 * lb, xr2[0], xr2[1], xi2[0], xi2[1]);
+            xr2[e] = xr;
+            xi2[e] = xi;
+            // S*/conj(v) = S* v / |v|^2
+            const double srr = sv[lb].get(e), sii = sv[lb].get(2 + e);
+            const double r = 1.0 / m2;
+            const double ur = __fma_rn(srr, xr, -(sii * xi)) * r;
+            const double ui = __fma_rn(srr, xi, sii * xr) * r;
+            const int node = 8 * (nb0 + lb) + 2 * q + e;
+            const int ks = node >> 2;
+            if (ks < KS) u_sm[ks * 32 + slot * 4 + (node & 3)] = make_double2(ur, ui);
           }
+          tmem_st4d(tm_o + 8 * lb, xr2[0], xr2[1], xi2[0], xi2[1]);
         }
       }
     }
     tmem_wait_st();
     named_bar(bar_id, 64);  // U complete for both halves
-    pf.next = next_ids[(pair * 8 + slot) * 2 + (refills & 1)];  // visible after the barrier
+    if (want_prefetch) {  // the ring entry written after the last refill is visible now
+      prefetch_case(next_ids[(pair * 8 + slot) * 2 + (refills & 1)]);
+      want_prefetch = false;
+    }
 
     // ---------- GEMM: V' = W + U K^T on FP64 tensor cores ----------
 #pragma unroll
@@ -318,35 +303,31 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     {
       const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
       if (nbw == NBH) {
-        gemm_warp<NBH, NBH>(vr, vi, kb, u_sm + lane, KS, pf);
+        gemm_warp<NBH, NBH>(vr, vi, kb, u_sm + lane, KS);
       } else {
-        if constexpr (NB - NBH > 0) gemm_warp<NBH, NB - NBH>(vr, vi, kb, u_sm + lane, KS, pf);
+        if constexpr (NB - NBH > 0) gemm_warp<NBH, NB - NBH>(vr, vi, kb, u_sm + lane, KS);
       }
     }
 
     // ---------- epilogue: per-case step test (dense.py:125-126, 189-193) ----------
     bool small = true;
     {
+      D4 ov[NBH];
 #pragma unroll
-      for (int c0 = 0; c0 < NBH; c0 += kChunk) {
-        D4 ov[kChunk];
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_o + 8 * lb, ov[lb]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j)
-          if (c0 + j < NBH && c0 + j < nbw) tmem_ld4d(tm_o + 8 * (c0 + j), ov[j]);
-        tmem_wait_ld();
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int lb = c0 + j;
-          if (lb < NBH && lb < nbw) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int node = 8 * (nb0 + lb) + 2 * q + e;
-              const double dr = vr[lb][e] - ov[j].get(e);
-              const double di = vi[lb][e] - ov[j].get(2 + e);
-              const double d2 = __fma_rn(dr, dr, di * di);
-              // NaN/inf never compare small: they hold the case open to the cap
-              if (node < b && !(d2 < a.tol2)) small = false;
-            }
+          for (int e = 0; e < 2; ++e) {
+            const int node = 8 * (nb0 + lb) + 2 * q + e;
+            const double dr = vr[lb][e] - ov[lb].get(e);
+            const double di = vi[lb][e] - ov[lb].get(2 + e);
+            const double d2 = __fma_rn(dr, dr, di * di);
+            // NaN/inf never compare small: they hold the case open to the cap
+            if (node < b && !(d2 < a.tol2)) small = false;
           }
         }
       }
@@ -386,30 +367,25 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       ++refills;
       cid = (nc < tau) ? nc : INT_MAX;
       n_it = 0;
+      want_prefetch = cid != INT_MAX;
     }
     // TMEM access is warp-collective (.sync.aligned): the whole warp rewrites
-    // S*, retiring lanes with the next case's S* staged during the GEMM, the
-    // others with what they hold.
+    // S*, retiring lanes with their new case, the others with what they hold.
     if (__any_sync(0xffffffffu, done)) {
+      D4 cur[NBH];
 #pragma unroll
-      for (int c0 = 0; c0 < NBH; c0 += kChunk) {
-        D4 cur[kChunk], nxt[kChunk];
+      for (int lb = 0; lb < NBH; ++lb)
+        if (lb < nbw) tmem_ld4d(tm_s + 8 * lb, cur[lb]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          if (c0 + j < NBH && c0 + j < nbw) {
-            tmem_ld4d(tm_s + 8 * (c0 + j), cur[j]);
-            tmem_ld4d(tm_n + 8 * (c0 + j), nxt[j]);
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          double s0r = cur[lb].get(0), s1r = cur[lb].get(1), s0i = cur[lb].get(2), s1i = cur[lb].get(3);
+          if (done) {
+            fetch_s(cid, lb, s0r, s0i, s1r, s1i);
+            flat_start(lb);
           }
-        }
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int lb = c0 + j;
-          if (lb < NBH && lb < nbw) {
-            const D4& src = done ? nxt[j] : cur[j];
-            tmem_st4d(tm_s + 8 * lb, src.get(0), src.get(1), src.get(2), src.get(3));
-            if (done) flat_start(lb);
-          }
+          tmem_st4d(tm_s + 8 * lb, s0r, s1r, s0i, s1i);
         }
       }
     }
@@ -431,7 +407,7 @@ static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
   err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_fpi_kernel<NB>, kThreads, smem);
   if (err != cudaSuccess) return set_cuda_error("occupancy(dense)", err);
   if (per_sm < 1) return set_error(TPF_ERR_UNSUPPORTED, "dense kernel does not fit on an SM");
-  if (per_sm > 1) per_sm = 1;  // each CTA holds all 512 TMEM columns of its SM
+  if (per_sm > 2) per_sm = 2;  // each CTA holds 256 of the SM's 512 TMEM columns
   // slots in flight = 8 per pair; never launch more CTAs than needed
   const int64_t slots_per_cta = 8 * kPairs;
   int64_t grid = int64_t(per_sm) * sm_count;
