@@ -114,6 +114,28 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
                         int32_t* iters, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* Radial-feeder fast path of the sparse solver: one case per SM with the
+ * whole case on chip (sweep vector in shared memory, iterate and loads in
+ * Tensor Memory), level-synchronous up/down sweeps over the depth levels of
+ * the zero-fill tree LU.  Inputs come from the host-built schedule
+ * (paper_2403_04578_b200.sparse.tree_schedule):
+ *   level_info  int32[2*(levels+1)]: node offsets per depth level (root level
+ *               first), then the first TMEM slot of each level
+ *   node_info   int32[4*b]: per level-ordered node {original node, parent,
+ *               first child, child count} (parent -1 at the roots)
+ *   node_coef   complex[4*b]: {L[parent,m], U[m,parent], 1/U[m,m], src}
+ * Limits: b <= 12,800 and sum over levels of ceil(n_level/512) <=
+ * tpf_sparse_tree_max_slots() (16); otherwise use tpf_sparse_fpi_c128.
+ *   workspace >= 256 device bytes                                          */
+int tpf_sparse_tree_max_slots(void);
+int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels,
+                             const int32_t* level_info, const int32_t* node_info, const double* node_coef,
+                             const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                             double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                             double* V, int64_t v_node_stride, int64_t v_case_stride,
+                             int32_t* iters, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* -------------------------------------------------------------- residual --
  * residual_per_case (fpi.py:221-240, constant-power branch) as used by
  * _safe_residuals (dense.py:208-211):
@@ -146,6 +168,16 @@ int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
  * workspace: device scratch of >= tpf_*_solve_host_workspace_bytes(...)
  * bytes, or NULL to let the call cudaMalloc/cudaFree its own.
  * Synchronous: returns when every output is on the host.                  */
+size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz);
+int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t levels,
+                                    const int32_t* level_info, const int32_t* node_info, const double* node_coef,
+                                    const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                                    const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                                    const double* src, double v_flat_re, double v_flat_im,
+                                    double tol, int32_t max_iter, double residual_tol,
+                                    double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                    int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
+                                    int64_t chunk_cases, int32_t device, void* workspace, size_t workspace_bytes);
 size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz);
 size_t tpf_sparse_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz,
                                              int64_t l_nnz, int64_t u_nnz);

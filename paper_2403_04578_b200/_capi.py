@@ -56,6 +56,15 @@ SIGNATURES = {
         _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
     "tpf_dense_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64]),
     "tpf_sparse_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64, _c_i64, _c_i64]),
+    "tpf_sparse_tree_max_slots": (ctypes.c_int, []),
+    "tpf_sparse_tree_fpi_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl,
+        _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_sparse_tree_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64]),
+    "tpf_sparse_tree_solve_host_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),
 }
 

@@ -85,3 +85,24 @@ __device__ __forceinline__ void tmem_ld4d(uint32_t taddr, D4& o) {
                : "memory");
 }
 }  // namespace tpf
+
+namespace tpf {
+// 1 double2 (re, im) <-> 4 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)), "r"(__double2hiint(v.y))
+               : "memory");
+}
+struct D2 {
+  uint32_t r[4];
+  __device__ __forceinline__ double2 get() const {
+    return make_double2(__hiloint2double(int(r[1]), int(r[0])), __hiloint2double(int(r[3]), int(r[2])));
+  }
+};
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, D2& o) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(o.r[0]), "=r"(o.r[1]), "=r"(o.r[2]), "=r"(o.r[3])
+               : "r"(taddr)
+               : "memory");
+}
+}  // namespace tpf

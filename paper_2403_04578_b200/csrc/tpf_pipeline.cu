@@ -317,10 +317,77 @@ struct SparseChunk : ChunkSolver {
   }
 };
 
+struct TreeChunk : ChunkSolver {
+  int b, levels;
+  const int32_t *lvl, *info;
+  const double* coef;
+  double vre, vim, tol;
+  int max_iter;
+  void* ws;
+  size_t ws_bytes;
+  int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+            cudaStream_t st) override {
+    return tpf_sparse_tree_fpi_c128(n, b, levels, lvl, info, coef, S, sn, sc, vre, vim, tol, max_iter, V, vn, vc, it,
+                                    ws, ws_bytes, st);
+  }
+};
+
 }  // namespace
 }  // namespace tpf
 
 using namespace tpf;
+
+extern "C" size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
+                                                             int64_t ydd_nnz) {
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const size_t model = size_t(b) * 160 + size_t(ydd_nnz) * 20 + 24 * 512 + 64 * 8;
+  return pipeline_bytes(tau, b, chunk, model, 256);
+}
+
+extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
+                                               const int32_t* node_info, const double* node_coef, const double* S,
+                                               int64_t s_node_stride, int64_t s_case_stride,
+                                               const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                               const double* ydd_val, const double* src, double v_flat_re,
+                                               double v_flat_im, double tol, int32_t max_iter, double residual_tol,
+                                               double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                               int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
+                                               int64_t chunk_cases, int32_t device, void* workspace,
+                                               size_t workspace_bytes) {
+  if (tau < 0 || b < 1 || levels < 1)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_solve_host_c128: bad shape");
+  if (!S || !level_info || !node_info || !node_coef || !ydd_row_ptr || !src || !V)
+    return set_error(TPF_ERR_INVALID, "null pointer");
+  TPF_CK(cudaSetDevice(device), "cudaSetDevice");
+  if (summary) summary[0] = summary[1] = 0;
+  if (tau == 0) return TPF_OK;
+  if (workspace && workspace_bytes < tpf_sparse_tree_solve_host_workspace_bytes(tau, b, chunk_cases, ydd_row_ptr[b]))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_solve_host_c128: workspace too small");
+  ArenaScope arena(workspace, workspace_bytes);
+  Streams ss;
+  TPF_CK(ss.init(), "cudaStreamCreate");
+  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  cudaStream_t st = ss.s[1];
+  DevBuf dl, di, dc, dws;
+  TPF_CK(upload(dl, level_info, size_t(levels + 1) * 2, st), "upload(levels)");
+  TPF_CK(upload(di, node_info, size_t(b) * 4, st), "upload(node_info)");
+  TPF_CK(upload(dc, node_coef, size_t(b) * 8, st), "upload(node_coef)");
+  TPF_CK(dws.alloc(256), "cudaMalloc(workspace)");
+  TreeChunk sv;
+  sv.b = b;
+  sv.levels = levels;
+  sv.lvl = dl.as<int32_t>();
+  sv.info = di.as<int32_t>();
+  sv.coef = dc.as<double>();
+  sv.vre = v_flat_re;
+  sv.vim = v_flat_im;
+  sv.tol = tol;
+  sv.max_iter = max_iter;
+  sv.ws = dws.p;
+  sv.ws_bytes = 256;
+  return run_pipeline(sv, tau, b, S, s_node_stride, s_case_stride, ydd_row_ptr, ydd_col, ydd_val, src, residual_tol,
+                      V, v_node_stride, v_case_stride, iters, resid, mask, summary, chunk, ss, st);
+}
 
 extern "C" size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                        int64_t ydd_nnz) {

@@ -38,7 +38,7 @@ from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOpti
 from .dense import finish
 
 __all__ = ["batch_solve_sparse", "factorization_count", "factorize_ydd", "TreeLU",
-           "DEFAULT_MAX_BLOCK_NNZ"]
+           "TreeSchedule", "tree_schedule", "SparseOperator", "DEFAULT_MAX_BLOCK_NNZ"]
 
 # sparse.py:44
 DEFAULT_MAX_BLOCK_NNZ = 50_000_000
@@ -160,6 +160,132 @@ def factorize_ydd(y_dd) -> TreeLU:
         ordering=kind)
 
 
+TREE_THREADS = 512      # CTA size of tpf_sparse_tree_fpi_c128
+TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
+TREE_MAX_NODES = 12800  # shared-memory sweep vector: 16 B per node, <= 200 KB
+
+
+@dataclass
+class TreeSchedule:
+    """Depth-level layout of a zero-fill tree LU for the on-chip tree kernel.
+
+    Nodes are renumbered level by level (root level first); within a level,
+    children of the same parent are contiguous.  ``level_info`` = level
+    offsets (levels+1) followed by per-level first TMEM slot (levels+1);
+    ``node_info`` = int32[4 per node] {original node, parent, first child,
+    child count}; ``node_coef`` = complex[4 per node] {L[parent, m],
+    U[m, parent], 1/U[m, m], src[original node]}.
+    """
+
+    b: int
+    levels: int
+    level_info: np.ndarray
+    node_info: np.ndarray
+    node_coef: np.ndarray
+    slots: int
+
+
+def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
+    """Build the level schedule if the LU is a zero-fill tree elimination, else None."""
+    b = f.b
+    if f.ordering != "leaf-first" or b > TREE_MAX_NODES:
+        return None
+    row_src = f.perm[:b].astype(np.int64)
+    col_dst = f.perm[b:].astype(np.int64)
+    if not np.array_equal(col_dst[row_src], np.arange(b)):
+        return None  # not a symmetric permutation
+    ucount = np.diff(f.u_ptr)
+    if ucount.max(initial=0) > 1:
+        return None
+    parent = np.full(b, -1, dtype=np.int64)
+    upar = np.zeros(b, dtype=complex)
+    has = ucount == 1
+    parent[has] = f.u_col[f.u_ptr[:-1][has]]
+    upar[has] = f.u_val[f.u_ptr[:-1][has]]
+    if np.any(parent[has] <= np.nonzero(has)[0]):
+        return None  # parents must be eliminated after their children
+    # L[parent, k]: the entry of row parent(k), column k
+    lval = np.zeros(b, dtype=complex)
+    nchild = np.diff(f.l_ptr)
+    rows = np.repeat(np.arange(b), nchild)
+    if np.any(parent[f.l_col] != rows):
+        return None  # L holds something other than child edges
+    lval[f.l_col] = f.l_val
+    depth = np.zeros(b, dtype=np.int64)
+    for k in range(b - 1, -1, -1):
+        if parent[k] >= 0:
+            depth[k] = depth[parent[k]] + 1
+    levels = int(depth.max(initial=0)) + 1
+    order = []
+    pos_in_level = np.zeros(b, dtype=np.int64)
+    level_nodes = [np.nonzero(depth == 0)[0]]
+    for d in range(1, levels):
+        cand = np.nonzero(depth == d)[0]
+        key = pos_in_level[parent[cand]]
+        level_nodes.append(cand[np.lexsort((cand, key))])
+        pos_in_level[level_nodes[-1]] = np.arange(level_nodes[-1].size)
+    pos_in_level[level_nodes[0]] = np.arange(level_nodes[0].size)
+    # recompute positions level by level (level 0 first) so children sort by parent position
+    for d in range(1, levels):
+        cand = level_nodes[d]
+        key = pos_in_level[parent[cand]]
+        level_nodes[d] = cand[np.lexsort((cand, key))]
+        pos_in_level[level_nodes[d]] = np.arange(cand.size)
+    order = np.concatenate(level_nodes)
+    m_of_k = np.empty(b, dtype=np.int64)
+    m_of_k[order] = np.arange(b)
+    sizes = np.array([x.size for x in level_nodes])
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    slots_per = -(-sizes // TREE_THREADS)
+    j0 = np.concatenate([[0], np.cumsum(slots_per)])
+    if j0[-1] > TREE_MAX_SLOTS:
+        return None
+    pm = np.where(parent[order] >= 0, m_of_k[np.maximum(parent[order], 0)], -1)
+    first = np.zeros(b, dtype=np.int64)
+    cnt = np.zeros(b, dtype=np.int64)
+    kids = pm >= 0
+    np.add.at(cnt, pm[kids], 1)
+    first_seen = np.full(b, b, dtype=np.int64)
+    np.minimum.at(first_seen, pm[kids], np.nonzero(kids)[0])
+    first = np.where(cnt > 0, first_seen, 0)
+    # contiguity of children
+    if np.any(cnt > 0):
+        ok = np.all(pm[first[cnt > 0] + cnt[cnt > 0] - 1] == np.nonzero(cnt > 0)[0])
+        if not ok:
+            return None
+    info = np.stack([row_src[order], pm, first, cnt], axis=1).astype(np.int32)
+    coef = np.stack([lval[order], upar[order], f.u_diag_inv[order], np.asarray(src)[row_src[order]]],
+                    axis=1).astype(complex)
+    return TreeSchedule(b=b, levels=levels,
+                        level_info=np.concatenate([offs, j0]).astype(np.int32),
+                        node_info=np.ascontiguousarray(info.ravel()),
+                        node_coef=np.ascontiguousarray(coef.ravel()), slots=int(j0[-1]))
+
+
+def tree_solve_host(t: TreeSchedule, rhs: np.ndarray) -> np.ndarray:
+    """Numpy emulation of the tree kernel's two sweeps (host-logic tests only)."""
+    b = t.b
+    info = t.node_info.reshape(b, 4)
+    coef = t.node_coef.reshape(b, 4)
+    offs = t.level_info[:t.levels + 1]
+    T = np.zeros(b, dtype=complex)
+    for d in range(t.levels - 1, -1, -1):
+        for m in range(offs[d], offs[d + 1]):
+            z = rhs[info[m, 0]]
+            for c in range(info[m, 2], info[m, 2] + info[m, 3]):
+                z -= coef[c, 0] * T[c]
+            T[m] = z
+    for d in range(t.levels):
+        for m in range(offs[d], offs[d + 1]):
+            z = T[m]
+            if info[m, 1] >= 0:
+                z -= coef[m, 1] * T[info[m, 1]]
+            T[m] = z * coef[m, 2]
+    x = np.empty(b, dtype=complex)
+    x[info[:, 0]] = T
+    return x
+
+
 def lu_solve_host(f: TreeLU, rhs: np.ndarray) -> np.ndarray:
     """Numpy emulation of the kernel's sweep order (host-logic tests only)."""
     b = f.b
@@ -180,7 +306,7 @@ def lu_solve_host(f: TreeLU, rhs: np.ndarray) -> np.ndarray:
 class SparseOperator:
     """One factorization of Y_dd resident on a device; ``solve`` iterates."""
 
-    def __init__(self, model, device=None):
+    def __init__(self, model, device=None, use_tree: bool = True):
         self.device = require_cuda(device)
         self.contract = ModelContract.of(model)
         self.lu = factorize_ydd(self.contract.y_dd)
@@ -196,10 +322,18 @@ class SparseOperator:
                         perm=t(f.perm), src=t(self.contract.src))
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
+        self.tree = tree_schedule(f, self.contract.src) if use_tree else None
+        if self.tree is not None:
+            self.tree_dev = dict(level_info=t(self.tree.level_info), node_info=t(self.tree.node_info),
+                                 node_coef=t(self.tree.node_coef))
 
     @property
     def b(self) -> int:
         return self.contract.b
+
+    @property
+    def kernel(self) -> str:
+        return "sparse_tree_kernel" if self.tree is not None else "sparse_fpi_kernel"
 
     def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V=None, iters=None):
         b, tau = S.shape
@@ -209,6 +343,18 @@ class SparseOperator:
             V = torch.empty((b, tau), dtype=torch.complex128, device=self.device)
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
+        if self.tree is not None:
+            if self._ws is None:
+                self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+            sn, sc = complex_strides(S)
+            vn, vc = complex_strides(V)
+            g = self.tree_dev
+            _capi.call("tpf_sparse_tree_fpi_c128", tau, b, self.tree.levels, g["level_info"].data_ptr(),
+                       g["node_info"].data_ptr(), g["node_coef"].data_ptr(), S.data_ptr(), sn, sc,
+                       self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                       V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                       stream_ptr(self.device))
+            return V, iters
         need = int(_capi.load().tpf_sparse_workspace_bytes(tau, b))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
@@ -227,7 +373,8 @@ class SparseOperator:
 
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
                        max_nnz: int | None = None, *, device=None,
-                       return_on_device: bool = False, chunk_cases: int = 0) -> VoltageBatch:
+                       return_on_device: bool = False, chunk_cases: int = 0,
+                       use_tree: bool = True) -> VoltageBatch:
     """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring."""
     if not isinstance(loads, LoadMatrix):
         loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
@@ -242,8 +389,8 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
                 f"block system would hold {total} nonzeros (> {max_nnz}); "
                 "chunk the batch over cases and solve the chunks separately")
     if not return_on_device:
-        return _solve_host_pipeline(model, loads, opts, device, chunk_cases)
-    op = SparseOperator(model, device)
+        return _solve_host_pipeline(model, loads, opts, device, chunk_cases, use_tree)
+    op = SparseOperator(model, device, use_tree=use_tree)
     S = loads_to_device(loads.values, op.device)
     V, iters = op.solve(S, opts)
     resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
@@ -255,10 +402,12 @@ def _nonempty(a):
     return a if a.size else np.zeros(1, dtype=a.dtype)
 
 
-def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int):
+def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int,
+                         use_tree: bool = True):
     dev = require_cuda(device)
     c = ModelContract.of(model)
     f = factorize_ydd(c.y_dd)
+    tree = tree_schedule(f, c.src) if use_tree else None
     rp, ci, yv = host_csr(c)
     S, sn, sc = host_loads(loads.values)
     b, tau = S.shape
@@ -271,6 +420,16 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, c
     arrs = [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val, f.u_diag_inv,
                                     f.perm)]
     lib = _capi.load()
+    if tree is not None:
+        ws = device_workspace(dev, lib.tpf_sparse_tree_solve_host_workspace_bytes(tau, b, int(chunk_cases), yv.size))
+        torch.cuda.current_stream(dev).synchronize()
+        _capi.call("tpf_sparse_tree_solve_host_c128", tau, b, tree.levels, ptr(tree.level_info),
+                   ptr(tree.node_info), ptr(tree.node_coef), ptr(S), sn, sc, ptr(rp), ptr(ci), ptr(yv),
+                   ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                   float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters), ptr(resid), ptr(mask),
+                   ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
+        return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
+                            residuals=resid, iterations_per_case=iters)
     ws = device_workspace(dev, lib.tpf_sparse_solve_host_workspace_bytes(
         tau, b, int(chunk_cases), yv.size, f.l_col.size, f.u_col.size))
     torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams

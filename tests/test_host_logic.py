@@ -113,3 +113,39 @@ class TestTreeLU:
     def test_leaf_first_detects_cycles(self):
         y = sparse.csr_matrix(np.ones((3, 3)) + 2 * np.eye(3))
         assert leaf_first_order(y) is None
+
+
+class TestTreeSchedule:
+    @pytest.mark.parametrize("n_buses", [2, 9, 101, 1001])
+    def test_schedule_sweeps_solve_ydd(self, n_buses):
+        from paper_2403_04578_b200.sparse import tree_schedule, tree_solve_host
+        m = build_network(GenSpec(n_buses=n_buses, seed=5))
+        t = tree_schedule(factorize_ydd(m.admittance.y_dd), m.source_injection())
+        assert t is not None
+        b = m.n_demand
+        rng = np.random.default_rng(n_buses)
+        r = rng.standard_normal(b) + 1j * rng.standard_normal(b)
+        x = tree_solve_host(t, r)
+        assert np.abs(m.admittance.y_dd @ x - r).max() / np.abs(r).max() < 1e-12
+        # children contiguous, parents one level up, slots within the TMEM budget
+        info = t.node_info.reshape(b, 4)
+        offs = t.level_info[:t.levels + 1]
+        for d in range(1, t.levels):
+            for mm in range(offs[d], offs[d + 1]):
+                p = info[mm, 1]
+                assert offs[d - 1] <= p < offs[d]
+                assert info[p, 2] <= mm < info[p, 2] + info[p, 3]
+        assert t.slots <= 16
+
+    def test_c3_feeder_fits_the_tmem_budget(self):
+        from paper_2403_04578_b200.sparse import tree_schedule
+        m = build_network(GenSpec(n_buses=5001, seed=0))
+        t = tree_schedule(factorize_ydd(m.admittance.y_dd), m.source_injection())
+        assert t is not None and t.levels == 7 and t.slots == 16
+
+    def test_general_matrix_has_no_tree_schedule(self):
+        from paper_2403_04578_b200.sparse import tree_schedule
+        rng = np.random.default_rng(18)
+        y = rng.normal(0, 1, (6, 6)) + 1j * rng.normal(0, 1, (6, 6))
+        np.fill_diagonal(y, np.abs(y).sum(axis=1) + 20.0)
+        assert tree_schedule(factorize_ydd(sparse.csc_matrix(y)), np.zeros(6, complex)) is None
