@@ -41,7 +41,7 @@ struct TreeArgs {
   unsigned long long* counter;
   const int32_t* lvl;     // [levels+1] level offsets in level order (root level first), then [levels+1] slot starts
   const int4* info;       // per level-ordered node m: {original node, parent m or -1, first child m, child count}
-  const double2* coef;    // per m: {a = L[parent, m], u = U[m, parent], uinv = 1/U[m,m], src}
+  const double2* coef;    // per m: {e = Y[parent, m], unused, uinv = 1/U[m,m], src}
   double2 v_flat;
   double tol2;
   int max_iter;
@@ -54,9 +54,16 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 x) {
   return make_double2(__fma_rn(a.x, x.x, -(a.y * x.y)), __fma_rn(a.x, x.y, a.y * x.x));
 }
 
+constexpr int kSB = 3;  // slots per batch: their loads are issued together (ILP across slots)
+
+// Scaled sweeps (zhat = z / U_mm, so L[p,c] z_c = Y[p,c] zhat_c):
+//   up:   zhat_m = (r_m - sum_c e_c zhat_c) * uinv_m,   e_c = Y[parent(c), c]
+//   down: w_m    = zhat_m - uinv_m * e_m * w_parent     (U[m,p] = Y[m,p] = e_m for symmetric Y)
 __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const TreeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* T = reinterpret_cast<double2*>(smem_raw);  // [b]
+  double2* T = reinterpret_cast<double2*>(smem_raw);       // [b] sweep vector
+  int2* kids = reinterpret_cast<int2*>(T + a.b);           // [b] {first child, count}
+  int* par = reinterpret_cast<int*>(kids + a.b);           // [b] parent (-1 at roots)
   __shared__ int s_off[kMaxLevels + 1], s_j0[kMaxLevels + 1];
   __shared__ int s_case;
   __shared__ uint32_t s_tmem;
@@ -67,13 +74,17 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     s_off[i] = a.lvl[i];
     s_j0[i] = a.lvl[L + 1 + i];
   }
+  for (int m = tid; m < a.b; m += kTreeThreads) {
+    const int4 inf = __ldg(&a.info[m]);
+    kids[m] = make_int2(inf.z, inf.w);
+    par[m] = inf.y;
+  }
   if (warp == 0) tmem_alloc(&s_tmem, 512);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tm = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 128);
   const uint32_t tm_v = tm, tm_s = tm + 4 * kMaxSlots;
-  const int nslots = s_j0[L];
 
   for (;;) {
     if (tid == 0) {
@@ -103,29 +114,41 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     while (it < a.max_iter) {
       // ---- up-sweep: deepest level first ----
       for (int d = L - 1; d >= 0; --d) {
-        const int off = s_off[d], end = s_off[d + 1];
-        for (int j = s_j0[d]; j < s_j0[d + 1]; ++j) {
-          D2 vv, ss;
-          tmem_ld2(tm_v + 4 * j, vv);
-          tmem_ld2(tm_s + 4 * j, ss);
-          tmem_wait_ld();
-          const int m = off + (j - s_j0[d]) * kTreeThreads + tid;
-          if (m < end) {
-            double2 v = vv.get();
-            const double2 s = ss.get();
-            double m2 = __fma_rn(v.x, v.x, v.y * v.y);
-            if (m2 < kZeroGuard2) {  // fpi.py:39-41
-              v = make_double2(kZeroGuard, 0.0);
-              m2 = kZeroGuard * kZeroGuard;
+        const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
+        for (int j = jb; j < je; j += kSB) {
+          D2 vv[kSB], ss[kSB];
+          double2 ui[kSB], src[kSB];
+#pragma unroll
+          for (int u = 0; u < kSB; ++u) {
+            if (j + u < je) {  // warp-uniform
+              tmem_ld2(tm_v + 4 * (j + u), vv[u]);
+              tmem_ld2(tm_s + 4 * (j + u), ss[u]);
             }
-            const double r = 1.0 / m2;
-            const double2 src = __ldg(&a.coef[4 * m + 3]);
-            // r_k = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
-            double2 z = make_double2(-(__fma_rn(s.x, v.x, s.y * v.y) * r + src.x),
-                                     -(__fma_rn(s.x, v.y, -(s.y * v.x)) * r + src.y));
-            const int4 inf = __ldg(&a.info[m]);
-            for (int c = inf.z; c < inf.z + inf.w; ++c) z = cfma_sub(z, __ldg(&a.coef[4 * c]), T[c]);
-            T[m] = z;
+            const int m = off + (j + u - jb) * kTreeThreads + tid;
+            const bool ok = j + u < je && m < end;
+            ui[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
+            src[u] = (ok && d == 0) ? __ldg(&a.coef[4 * m + 3]) : make_double2(0.0, 0.0);
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < kSB; ++u) {
+            const int m = off + (j + u - jb) * kTreeThreads + tid;
+            if (j + u < je && m < end) {
+              double2 v = vv[u].get();
+              const double2 s = ss[u].get();
+              double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+              if (m2 < kZeroGuard2) {  // fpi.py:39-41
+                v = make_double2(kZeroGuard, 0.0);
+                m2 = kZeroGuard * kZeroGuard;
+              }
+              const double r = 1.0 / m2;
+              // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
+              double2 z = make_double2(-(__fma_rn(s.x, v.x, s.y * v.y) * r + src[u].x),
+                                       -(__fma_rn(s.x, v.y, -(s.y * v.x)) * r + src[u].y));
+              const int2 k = kids[m];
+              for (int c = k.x; c < k.x + k.y; ++c) z = cfma_sub(z, __ldg(&a.coef[4 * c]), T[c]);
+              T[m] = cmul2(z, ui[u]);
+            }
           }
         }
         __syncthreads();
@@ -134,25 +157,37 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       bool small = true;
       int all_small = 0;
       for (int d = 0; d < L; ++d) {
-        const int off = s_off[d], end = s_off[d + 1];
-        for (int j = s_j0[d]; j < s_j0[d + 1]; ++j) {
-          D2 vv;
-          tmem_ld2(tm_v + 4 * j, vv);
-          tmem_wait_ld();
-          const int m = off + (j - s_j0[d]) * kTreeThreads + tid;
-          double2 v = vv.get();
-          double2 w = v;
-          if (m < end) {
-            const int4 inf = __ldg(&a.info[m]);
-            double2 z = T[m];
-            if (inf.y >= 0) z = cfma_sub(z, __ldg(&a.coef[4 * m + 1]), T[inf.y]);
-            w = cmul2(z, __ldg(&a.coef[4 * m + 2]));
-            T[m] = w;
-            if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
-            const double dr = w.x - v.x, di = w.y - v.y;
-            if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+        const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
+        for (int j = jb; j < je; j += kSB) {
+          D2 vv[kSB];
+          double2 e[kSB], ui[kSB];
+#pragma unroll
+          for (int u = 0; u < kSB; ++u) {
+            if (j + u < je) tmem_ld2(tm_v + 4 * (j + u), vv[u]);
+            const int m = off + (j + u - jb) * kTreeThreads + tid;
+            const bool ok = j + u < je && m < end && d > 0;
+            e[u] = ok ? __ldg(&a.coef[4 * m]) : make_double2(0.0, 0.0);
+            ui[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
           }
-          tmem_st2(tm_v + 4 * j, w);
+          tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < kSB; ++u) {
+            if (j + u < je) {
+              const int m = off + (j + u - jb) * kTreeThreads + tid;
+              double2 v = vv[u].get();
+              double2 w = v;
+              if (m < end) {
+                w = T[m];
+                const int p = par[m];
+                if (p >= 0) w = cfma_sub(w, cmul2(ui[u], e[u]), T[p]);
+                T[m] = w;
+                if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+                const double dr = w.x - v.x, di = w.y - v.y;
+                if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+              }
+              tmem_st2(tm_v + 4 * (j + u), w);
+            }
+          }
         }
         tmem_wait_st();
         if (d + 1 < L)
@@ -178,7 +213,6 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       }
     }
     if (tid == 0) a.iters[cs] = it;
-    (void)nslots;
   }
   tmem_fence_before();
   __syncthreads();
@@ -206,8 +240,8 @@ extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, 
   if (tau == 0) return TPF_OK;
   if (!level_info || !node_info || !node_coef || !S || !V || !iters || !workspace || workspace_bytes < 256)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: null pointer or small workspace");
-  const size_t smem = size_t(b) * sizeof(double2);
-  if (smem > 200 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_fpi_c128: b too large for one SM");
+  const size_t smem = size_t(b) * (sizeof(double2) + sizeof(int2) + sizeof(int));
+  if (smem > 220 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_fpi_c128: b too large for one SM");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaFuncSetAttribute(sparse_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tree)", err);

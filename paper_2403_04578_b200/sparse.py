@@ -162,7 +162,7 @@ def factorize_ydd(y_dd) -> TreeLU:
 
 TREE_THREADS = 512      # CTA size of tpf_sparse_tree_fpi_c128
 TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
-TREE_MAX_NODES = 12800  # shared-memory sweep vector: 16 B per node, <= 200 KB
+TREE_MAX_NODES = 9600  # shared memory: sweep vector + child ranges + parents, 28 B per node
 
 
 @dataclass
@@ -254,8 +254,14 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
         if not ok:
             return None
     info = np.stack([row_src[order], pm, first, cnt], axis=1).astype(np.int32)
-    coef = np.stack([lval[order], upar[order], f.u_diag_inv[order], np.asarray(src)[row_src[order]]],
-                    axis=1).astype(complex)
+    # scaled sweeps use e_m = Y[parent, m] = L[parent, m] U[m, m]; symmetric Y needs U[m, p] == e_m
+    e = lval[order] / f.u_diag_inv[order]
+    if not np.allclose(upar[order], e, rtol=1e-12, atol=0.0):
+        return None
+    src_o = np.asarray(src)[row_src[order]]
+    if np.any(src_o[offs[1]:] != 0):
+        return None  # source injection only at the root level (nodes next to the slack)
+    coef = np.stack([e, upar[order], f.u_diag_inv[order], src_o], axis=1).astype(complex)
     return TreeSchedule(b=b, levels=levels,
                         level_info=np.concatenate([offs, j0]).astype(np.int32),
                         node_info=np.ascontiguousarray(info.ravel()),
@@ -274,13 +280,11 @@ def tree_solve_host(t: TreeSchedule, rhs: np.ndarray) -> np.ndarray:
             z = rhs[info[m, 0]]
             for c in range(info[m, 2], info[m, 2] + info[m, 3]):
                 z -= coef[c, 0] * T[c]
-            T[m] = z
+            T[m] = z * coef[m, 2]
     for d in range(t.levels):
         for m in range(offs[d], offs[d + 1]):
-            z = T[m]
             if info[m, 1] >= 0:
-                z -= coef[m, 1] * T[info[m, 1]]
-            T[m] = z * coef[m, 2]
+                T[m] -= coef[m, 2] * coef[m, 0] * T[info[m, 1]]
     x = np.empty(b, dtype=complex)
     x[info[:, 0]] = T
     return x
