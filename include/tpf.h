@@ -126,7 +126,7 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
  *   node_coef   complex[4*b]: {e = Y[parent,m], U[m,parent], 1/U[m,m], src}
  *               (symmetric Y_dd: U[m,parent] = e; src nonzero only at the
  *               root level)
- * Limits: b <= 9,600 and sum over levels of ceil(n_level/512) <=
+ * Limits: b <= 7,800 and sum over levels of ceil(n_level/512) <=
  * tpf_sparse_tree_max_slots() (16); otherwise use tpf_sparse_fpi_c128.
  *   workspace >= 256 device bytes                                          */
 int tpf_sparse_tree_max_slots(void);

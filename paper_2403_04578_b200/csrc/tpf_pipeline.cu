@@ -340,7 +340,7 @@ using namespace tpf;
 extern "C" size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                              int64_t ydd_nnz) {
   const int64_t chunk = pick_chunk(tau, chunk_cases);
-  const size_t model = size_t(b) * 160 + size_t(ydd_nnz) * 20 + 24 * 512 + 64 * 8;
+  const size_t model = size_t(b) * 256 + size_t(ydd_nnz) * 24 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, 256);
 }
 
@@ -394,14 +394,14 @@ extern "C" size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, i
   const int64_t chunk = pick_chunk(tau, chunk_cases);
   const bool large = b > tpf_dense_max_nodes();
   const size_t solver = large ? tpf_dense_large_workspace_bytes(chunk, b) : tpf_dense_workspace_bytes(b);
-  const size_t model = size_t(b) * b * 16 + size_t(b) * 48 + size_t(ydd_nnz) * 20 + 16 * 512;
+  const size_t model = size_t(b) * b * 16 + size_t(b) * 128 + size_t(ydd_nnz) * 24 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, solver);
 }
 
 extern "C" size_t tpf_sparse_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                         int64_t ydd_nnz, int64_t l_nnz, int64_t u_nnz) {
   const int64_t chunk = pick_chunk(tau, chunk_cases);
-  const size_t model = size_t(b) * 64 + size_t(ydd_nnz + l_nnz + u_nnz) * 20 + 24 * 512;
+  const size_t model = size_t(b) * 128 + size_t(ydd_nnz + l_nnz + u_nnz) * 24 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, tpf_sparse_workspace_bytes(chunk, b));
 }
 

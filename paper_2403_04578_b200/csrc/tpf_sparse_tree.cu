@@ -61,8 +61,9 @@ constexpr int kSB = 3;  // slots per batch: their loads are issued together (ILP
 //   down: w_m    = zhat_m - uinv_m * e_m * w_parent     (U[m,p] = Y[m,p] = e_m for symmetric Y)
 __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const TreeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* T = reinterpret_cast<double2*>(smem_raw);       // [b] sweep vector
-  int2* kids = reinterpret_cast<int2*>(T + a.b);           // [b] {first child, count}
+  double2* T = reinterpret_cast<double2*>(smem_raw);       // [b] sweep vector (zhat, then w)
+  double2* P = T + a.b;                                    // [b] e_m * zhat_m, pulled by the parent
+  int2* kids = reinterpret_cast<int2*>(P + a.b);           // [b] {first child, count}
   int* par = reinterpret_cast<int*>(kids + a.b);           // [b] parent (-1 at roots)
   __shared__ int s_off[kMaxLevels + 1], s_j0[kMaxLevels + 1];
   __shared__ int s_case;
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
         for (int j = jb; j < je; j += kSB) {
           D2 vv[kSB], ss[kSB];
-          double2 ui[kSB], src[kSB];
+          double2 ui[kSB], src[kSB], e[kSB];
 #pragma unroll
           for (int u = 0; u < kSB; ++u) {
             if (j + u < je) {  // warp-uniform
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
             const int m = off + (j + u - jb) * kTreeThreads + tid;
             const bool ok = j + u < je && m < end;
             ui[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
+            e[u] = (ok && d > 0) ? __ldg(&a.coef[4 * m]) : make_double2(0.0, 0.0);
             src[u] = (ok && d == 0) ? __ldg(&a.coef[4 * m + 3]) : make_double2(0.0, 0.0);
           }
           tmem_wait_ld();
@@ -146,8 +148,14 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
               double2 z = make_double2(-(__fma_rn(s.x, v.x, s.y * v.y) * r + src[u].x),
                                        -(__fma_rn(s.x, v.y, -(s.y * v.x)) * r + src[u].y));
               const int2 k = kids[m];
-              for (int c = k.x; c < k.x + k.y; ++c) z = cfma_sub(z, __ldg(&a.coef[4 * c]), T[c]);
-              T[m] = cmul2(z, ui[u]);
+              for (int c = k.x; c < k.x + k.y; ++c) {
+                const double2 pc = P[c];
+                z.x -= pc.x;
+                z.y -= pc.y;
+              }
+              const double2 zh = cmul2(z, ui[u]);
+              T[m] = zh;
+              P[m] = cmul2(e[u], zh);
             }
           }
         }
@@ -240,7 +248,7 @@ extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, 
   if (tau == 0) return TPF_OK;
   if (!level_info || !node_info || !node_coef || !S || !V || !iters || !workspace || workspace_bytes < 256)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: null pointer or small workspace");
-  const size_t smem = size_t(b) * (sizeof(double2) + sizeof(int2) + sizeof(int));
+  const size_t smem = size_t(b) * (2 * sizeof(double2) + sizeof(int2) + sizeof(int));
   if (smem > 220 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_fpi_c128: b too large for one SM");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t err = cudaFuncSetAttribute(sparse_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -162,7 +162,7 @@ def factorize_ydd(y_dd) -> TreeLU:
 
 TREE_THREADS = 512      # CTA size of tpf_sparse_tree_fpi_c128
 TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
-TREE_MAX_NODES = 9600  # shared memory: sweep vector + child ranges + parents, 28 B per node
+TREE_MAX_NODES = 7800  # shared memory: sweep vector, child products, child ranges, parents: 44 B per node
 
 
 @dataclass
