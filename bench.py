@@ -73,7 +73,11 @@ def dist_env():
     return world, rank, local
 
 
-def workload(cfg, rank):
+HOST_GEN_LIMIT = 8 << 30  # bytes of S above which the value leg generates loads on the device
+
+
+def workload(cfg, rank, host_tau=None):
+    """(model, host LoadMatrix of host_tau cases or the full tau, method, description, tau, lspec)."""
     from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios
     n_buses, seed, tau, scale, method, desc = CONFIGS[cfg]
     if ARGS.tau:
@@ -81,8 +85,9 @@ def workload(cfg, rank):
     spec = GenSpec(n_buses=n_buses, seed=0, load_scale=scale)
     model = build_network(spec)
     lseed = seed if rank == 0 else 1000 + rank
-    loads = gen_scenarios(model, tau, GenSpec(n_buses=n_buses, seed=lseed, load_scale=scale))
-    return model, loads, method, desc
+    lspec = GenSpec(n_buses=n_buses, seed=lseed, load_scale=scale)
+    loads = gen_scenarios(model, min(tau, host_tau) if host_tau else tau, lspec)
+    return model, loads, method, desc, tau, lspec
 
 
 def cpu_sample(model, loads, seconds, cores):
@@ -122,7 +127,7 @@ def run_reference():
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    model, loads, method, desc = workload(ARGS.config, 0)
+    model, loads, method, desc, _, _ = workload(ARGS.config, 0, host_tau=1 << 16)
     cores = os.cpu_count() or 1
     from threadpoolctl import threadpool_limits
     from oracle import tpf_oracle as orc
@@ -206,14 +211,17 @@ class Clocks:
                     reasons=sorted(reasons))
 
 
-def traffic_from_profiles(kernel):
+def traffic_from_profiles(kernel, tau):
+    """DRAM bytes per launch from the committed ncu capture, scaled to this tau."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+            d = json.load(fh).get(kernel, {})
     except (OSError, ValueError):
         return None
+    if "dram_bytes_per_launch" not in d:
+        return None
+    return d["dram_bytes_per_launch"] * (tau / d["tau"]) if d.get("tau") else d["dram_bytes_per_launch"]
 
 
 def run_ours():
@@ -229,12 +237,19 @@ def run_ours():
     from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse
     from paper_2403_04578_b200._device import residual_and_summary
 
-    model, loads, method, desc = workload(ARGS.config, rank)
-    b, tau = loads.values.shape
+    n_buses = CONFIGS[ARGS.config][0]
+    full_tau = ARGS.tau or CONFIGS[ARGS.config][2]
+    device_gen = (n_buses - 1) * full_tau * 16 > HOST_GEN_LIMIT
+    model, loads, method, desc, tau, lspec = workload(ARGS.config, rank, host_tau=(1 << 16) if device_gen else None)
+    b = model.n_demand
     lib = _capi.load()
     peak_tf = ctypes_probe(lib)
     op = DenseOperator(model, dev) if method == "dense" else SparseOperator(model, dev)
-    S = torch.from_numpy(loads.values).to(dev)
+    if device_gen:
+        from paper_2403_04578_b200.synth import gen_scenarios_device
+        S = gen_scenarios_device(model, tau, lspec, device=dev)
+    else:
+        S = torch.from_numpy(loads.values).to(dev)
     V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
     iters = torch.empty(tau, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -282,9 +297,9 @@ def run_ours():
     if method == "dense":
         alg = 8.0 * b * b * sum_n  # FLOP_alg = 8 b^2 sum_j n_j
         achieved = alg / (kms * 1e-3) / 1e12
-        roofline = dict(bound="fp64-tensor", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
+        roofline = dict(bound="tensor", pipe="FP64 DMMA (mma.sync m8n8k4)", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
                         frac=achieved / peak_tf if peak_tf else None,
-                        traffic=traffic_from_profiles("dense_fpi_kernel"),
+                        traffic=traffic_from_profiles("dense_fpi_kernel", tau),
                         kernel="dense_fpi_kernel", kernel_ms=kms,
                         peak_source="measured in-run: DMMA-only probe (tpf_probe_fp64_tflops); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
@@ -294,9 +309,12 @@ def run_ours():
         achieved = alg / (kms * 1e-3) / 1e9
         peak = measured_hbm()
         roofline = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                        traffic=traffic_from_profiles("sparse_fpi_kernel"), kernel="sparse_fpi_kernel",
+                        traffic=traffic_from_profiles(op.kernel, tau), kernel=op.kernel,
                         kernel_ms=kms, peak_source="MEASURED_PEAKS.json hbm_gbs",
-                        algorithmic=f"48*b*sum(n_j) = {alg:.4e} bytes per launch")
+                        algorithmic=f"48*b*sum(n_j) = {alg:.4e} bytes per launch",
+                        compulsory=dict(bytes=32.0 * b * tau, gbs=32.0 * b * tau / (kms * 1e-3) / 1e9,
+                                        frac=32.0 * b * tau / (kms * 1e-3) / 1e9 / peak,
+                                        what="S read once + V written once"))
 
     e2e = None
     if not ARGS.no_e2e:
@@ -311,6 +329,8 @@ def run_ours():
                     warmup=ARGS.warmup, ms_per_step=ms / ARGS.steps, higher_is_better=True,
                     scaling="weak", vs_baseline=None, dtype="c128", data="synthetic",
                     config=dict(workload=desc, b=b, tau_per_gpu=tau, method=method,
+                                loads="device generator (synth.gen_scenarios_device)" if device_gen
+                                else "host generator, bit-identical to tpflow.gen_scenarios",
                                 sum_iterations=sum_n, batch_iterations=int(summ[0]),
                                 converged=int(summ[1]),
                                 l2="inputs (S, V: %.0f MB each) larger than the 126 MB L2" % (b * tau * 16 / 1e6),
@@ -363,7 +383,7 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
     b, tau = loads.values.shape
-    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * 16),
+    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * 16), cases_per_step=tau,
                 d2h_bytes_per_step=int(b * tau * 16 + tau * (4 + 8 + 1)),
                 ms_per_step=t * 1e3, api=f"paper_2403_04578_b200.batch_solve_{method}(model, LoadMatrix)",
                 iterations=int(out.iterations))
