@@ -31,6 +31,22 @@
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
 
+#ifdef TPF_PHASE_TIMING
+// per warp: [0] elementwise, [1] barrier U, [2] GEMM, [3] epilogue math, [4] barrier flags,
+// [5] retire/refill, [6] iterations, [7] total
+__device__ long long g_phase[148 * 2 * 8][8];
+#define PHASE_MARK(i)                         \
+  do {                                        \
+    const long long _t = clock64();           \
+    ph[i] += _t - ph_t;                       \
+    ph_t = _t;                                \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
 namespace tpf {
 
 constexpr int kPairs = 4;          // warp pairs per CTA
@@ -244,6 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
   prefetch_case(next_ids[(pair * 8 + slot) * 2 + 1]);
   bool want_prefetch = false;
 
+#ifdef TPF_PHASE_TIMING
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long ph_t = clock64();
+  const long long ph_start = ph_t;
+#endif
   for (;;) {
     // ---------- elementwise: guard, keep old iterate, U = S*/conj(V) ----------
     {
@@ -281,7 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       }
     }
     tmem_wait_st();
+    PHASE_MARK(0);
     named_bar(bar_id, 64);  // U complete for both halves
+    PHASE_MARK(1);
     if (want_prefetch) {  // the ring entry written after the last refill is visible now
       prefetch_case(next_ids[(pair * 8 + slot) * 2 + (refills & 1)]);
       want_prefetch = false;
@@ -309,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       }
     }
 
+    PHASE_MARK(2);
     // ---------- epilogue: per-case step test (dense.py:125-126, 189-193) ----------
     bool small = true;
     {
@@ -334,7 +358,9 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     }
     const uint32_t ball = __ballot_sync(0xffffffffu, small);
     if (lane == 0) flags[pair * 2 + half] = ball;
+    PHASE_MARK(3);
     named_bar(bar_id, 64);  // flags of both halves visible; U reads finished
+    PHASE_MARK(4);
     const uint32_t both = flags[pair * 2] & flags[pair * 2 + 1];
     const bool my_small = ((both >> (slot * 4)) & 0xFu) == 0xFu;
 
@@ -390,8 +416,17 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
       }
     }
     tmem_wait_st();
+    PHASE_MARK(5);
+#ifdef TPF_PHASE_TIMING
+    ph[6] += 1;
+#endif
     if (__all_sync(0xffffffffu, cid == INT_MAX)) break;
   }
+#ifdef TPF_PHASE_TIMING
+  ph[7] = clock64() - ph_start;
+  if (lane == 0 && blockIdx.x < 148 * 2)
+    for (int i = 0; i < 8; ++i) g_phase[blockIdx.x * 8 + warp][i] = ph[i];
+#endif
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -428,6 +463,13 @@ size_t dense_smem_bytes(int b) {
 }  // namespace tpf
 
 using namespace tpf;
+
+#ifdef TPF_PHASE_TIMING
+extern "C" int tpf_debug_phase_cycles(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * 8 * (n < 148 * 16 ? n : 148 * 16)) == cudaSuccess
+             ? 0 : 2;
+}
+#endif
 
 extern "C" int tpf_dense_max_nodes(void) { return 104; }
 
