@@ -75,6 +75,22 @@ int tpf_dense_fpi_c128(int64_t tau, int32_t b,
                        int32_t* iters, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* The two b <= 104 kernels behind tpf_dense_fpi_c128 (same arguments; the
+ * environment variable TPF_DENSE_KERNEL=pairs selects the second):
+ *   _ws_    warp-specialised: per SM sub-partition one DMMA warp alternating
+ *           between two slot groups and two elementwise warps (default);
+ *   _pairs_ pairs of warps sharing 8 slots, each doing GEMM and elementwise. */
+int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b,
+                          const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                          const double* K, const double* W, double v_flat_re, double v_flat_im,
+                          double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
+                          int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
+int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b,
+                             const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                             const double* K, const double* W, double v_flat_re, double v_flat_im,
+                             double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
+                             int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Dense TPF for b > 104 (K streamed from L2; config C5, b = 1,000): an
  * iteration-synchronous loop over a compacted active set of unconverged cases,
  * tiled FP64-DMMA GEMM per iteration.  Same arguments and semantics as

@@ -31,6 +31,12 @@ SIGNATURES = {
     "tpf_dense_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
         _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_dense_ws_fpi_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
+        _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_dense_pairs_fpi_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
+        _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
     "tpf_dense_large_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
     "tpf_dense_fpi_large_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,

@@ -27,6 +27,8 @@
 // runs in, so results are bitwise invariant to permutation and sharding.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -478,12 +480,49 @@ extern "C" size_t tpf_dense_workspace_bytes(int32_t b) {
   return 256;
 }
 
+extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                     int64_t s_case_stride, const double* K, const double* W, double v_flat_re,
+                                     double v_flat_im, double tol, int32_t max_iter, double* V, int64_t v_node_stride,
+                                     int64_t v_case_stride, int32_t* iters, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
+// Kernel selection for tpf_dense_fpi_c128: the warp-specialised kernel
+// (tpf_dense_ws.cu) unless TPF_DENSE_KERNEL=pairs selects the pair kernel below.
+static bool use_pairs_kernel() {
+  static const bool pairs = [] {
+    const char* e = getenv("TPF_DENSE_KERNEL");
+    return e && strcmp(e, "pairs") == 0;
+  }();
+  return pairs;
+}
+
+extern "C" int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                        int64_t s_case_stride, const double* K, const double* W,
+                                        double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                        double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                        int32_t* iters, void* workspace, size_t workspace_bytes,
+                                        void* stream);
+
 extern "C" int tpf_dense_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
                                   int64_t s_case_stride, const double* K, const double* W,
                                   double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
                                   double* V, int64_t v_node_stride, int64_t v_case_stride,
                                   int32_t* iters, void* workspace, size_t workspace_bytes,
                                   void* stream) {
+  if (use_pairs_kernel())
+    return tpf_dense_pairs_fpi_c128(tau, b, S, s_node_stride, s_case_stride, K, W, v_flat_re, v_flat_im, tol,
+                                    max_iter, V, v_node_stride, v_case_stride, iters, workspace, workspace_bytes,
+                                    stream);
+  return tpf_dense_ws_fpi_c128(tau, b, S, s_node_stride, s_case_stride, K, W, v_flat_re, v_flat_im, tol, max_iter,
+                               V, v_node_stride, v_case_stride, iters, workspace, workspace_bytes, stream);
+}
+
+extern "C" int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                        int64_t s_case_stride, const double* K, const double* W,
+                                        double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                        double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                        int32_t* iters, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
   if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: need tau >= 0 and b >= 1");
   if (b > 104)
     return set_error(TPF_ERR_UNSUPPORTED,
@@ -492,7 +531,7 @@ extern "C" int tpf_dense_fpi_c128(int64_t tau, int32_t b, const double* S, int64
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
   if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
   if (tau == 0) return TPF_OK;
-  if (!S || !K || !W || !V || !iters) return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: null pointer");
+  if (!S || !K || !W || !V || !iters) return set_error(TPF_ERR_INVALID, "tpf_dense_pairs_fpi_c128: null pointer");
   if (!workspace || workspace_bytes < tpf_dense_workspace_bytes(b))
     return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_c128: workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -64,7 +64,7 @@ class DenseOperator:
         return self._ws
 
     def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V: torch.Tensor | None = None,
-              iters: torch.Tensor | None = None):
+              iters: torch.Tensor | None = None, kernel: str | None = None):
         """Run the iteration on a device b x tau complex128 tensor (any strides).
 
         Returns ``(V, iters)``; V is b x tau C-contiguous unless given.
@@ -80,6 +80,8 @@ class DenseOperator:
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
         fn = "tpf_dense_fpi_large_c128" if self.large else "tpf_dense_fpi_c128"
+        if kernel is not None and not self.large:
+            fn = {"ws": "tpf_dense_ws_fpi_c128", "pairs": "tpf_dense_pairs_fpi_c128"}[kernel]
         _capi.call(fn, tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
                    self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                    V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),

@@ -186,3 +186,32 @@ def test_large_b_permutation_invariance_bitwise(golden):
     a = solve(g)
     b = solve(g, S=np.ascontiguousarray(g.S[:, perm]))
     assert np.array_equal(b.values, a.values[:, perm])
+
+
+@pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
+                                  "nine_zero_batch"])
+def test_ws_and_pair_kernels_bitwise_equal(golden, name):
+    """Warp-specialised and pair kernels: same DMMA order per element -> same bits."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator
+    g = golden(name)
+    op = DenseOperator(g.model)
+    S = torch.from_numpy(g.S).cuda()
+    o = g.opts()
+    V1, it1 = op.solve(S, o, kernel="ws")
+    V2, it2 = op.solve(S, o, kernel="pairs")
+    assert torch.equal(it1, it2)
+    assert torch.equal(V1, V2)
+
+
+def test_ws_kernel_full_c2_counts():
+    import torch
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, DenseOperator
+    spec = GenSpec(n_buses=101, seed=0)
+    model = build_network(spec)
+    S = torch.from_numpy(gen_scenarios(model, 525600, spec).values).cuda()
+    op = DenseOperator(model)
+    V1, it1 = op.solve(S, kernel="ws")
+    assert int(it1.sum()) == 2615281
+    V2, it2 = op.solve(S, kernel="pairs")
+    assert torch.equal(V1, V2)
