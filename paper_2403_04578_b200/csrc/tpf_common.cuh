@@ -22,6 +22,21 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
       : "d"(a), "d"(b));
 }
 
+// Same, but volatile: keeps program order among DMMAs (the scheduler would
+// otherwise pull dependent DMMAs together to save registers).
+__device__ __forceinline__ void dmma884_v(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 16-byte shared load that the compiler may not merge with an earlier identical load.
+__device__ __forceinline__ double2 lds128_v(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
 // Sign flip on the integer pipe (keeps the FP64 pipe free for DMMA).
 __device__ __forceinline__ double neg_int(double x) {
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));

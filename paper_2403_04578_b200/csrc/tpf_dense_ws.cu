@@ -61,27 +61,26 @@ struct Shared {
   uint32_t tmem;
 };
 
-// Two k-steps (kp, kp+1) of the complex GEMM for all NB node blocks; the 2*NB
-// DMMAs of the first pass do not depend on each other.
-template <int NB>
-__device__ __forceinline__ void kpair(double (&vr)[NB][2], double (&vi)[NB][2], const D4& af, const double2* k_sm,
-                                      int kp, int KS, int lane) {
+// Two k-steps (kp, kp+1) of the complex GEMM for all NB node blocks.  Per
+// block the four real DMMAs run back to back (the two that accumulate onto
+// the same fragment are two instructions = 32 pipe cycles apart, more than the
+// ~27-cycle DMMA latency), so each K fragment is loaded once; KS is a
+// template parameter so every fragment address is an immediate offset.
+template <int NB, int KS>
+__device__ __forceinline__ void kpair(double (&vr)[NB][2], double (&vi)[NB][2], const D4& af, const double2* kb,
+                                      int kp) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int ks = kp + h;
     if (ks < KS) {
       const double ur = af.get(2 * h), ui = af.get(2 * h + 1);
       const double nui = neg_int(ui);
-      const double2* kb = k_sm + size_t(ks) * 32 + lane;
+      const double2* k0 = kb + size_t(ks) * 32;
 #pragma unroll
       for (int lb = 0; lb < NB; ++lb) {
-        const double2 k = kb[size_t(lb) * KS * 32];
+        const double2 k = k0[size_t(lb) * KS * 32];
         dmma884(vr[lb][0], vr[lb][1], ur, k.x);
         dmma884(vi[lb][0], vi[lb][1], ur, k.y);
-      }
-#pragma unroll
-      for (int lb = 0; lb < NB; ++lb) {
-        const double2 k = kb[size_t(lb) * KS * 32];
         dmma884(vr[lb][0], vr[lb][1], nui, k.y);
         dmma884(vi[lb][0], vi[lb][1], ui, k.x);
       }
@@ -89,10 +88,9 @@ __device__ __forceinline__ void kpair(double (&vr)[NB][2], double (&vi)[NB][2], 
   }
 }
 
-template <int NB>
+template <int NB, int KS>
 __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double2* k_sm, const double* w_re,
                                          const double* w_im, int q, int lane, uint32_t tm) {
-  const int KS = a.ks_count;
   uint32_t par[2] = {0u, 0u};
   bool alive[2] = {true, true};
   const int qq = lane & 3;
@@ -121,13 +119,14 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
     D4 a0, a1;
     tmem_ld4d(uv, a0);
     tmem_wait_ld();
+    const double2* kb = k_sm + lane;
 #pragma unroll 1
     for (int kp = 0; kp < KS; kp += 4) {
       if (kp + 2 < KS) tmem_ld4d(uv + 4 * (kp + 2), a1);
-      kpair<NB>(vr, vi, a0, k_sm, kp, KS, lane);
+      kpair<NB, KS>(vr, vi, a0, kb, kp);
       tmem_wait_ld();
       if (kp + 4 < KS) tmem_ld4d(uv + 4 * (kp + 4), a0);
-      if (kp + 2 < KS) kpair<NB>(vr, vi, a1, k_sm, kp + 2, KS, lane);
+      if (kp + 2 < KS) kpair<NB, KS>(vr, vi, a1, kb, kp + 2);
       tmem_wait_ld();
     }
     // V' in C-fragment order over the consumed U
@@ -139,11 +138,11 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
   }
 }
 
-template <int NB>
+template <int NB, int KS>
 __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stage, int q, int g, int lane,
                                         uint32_t tm) {
   const int slot = lane >> 2, qq = lane & 3;
-  const int b = a.b, KS = a.ks_count;
+  const int b = a.b;
   const int64_t tau = a.tau;
   const uint32_t uv = tm + g * kGroupCols, vc = uv + 104;
   int cid = INT_MAX, nxt = INT_MAX, n_it = 0;
@@ -285,10 +284,10 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
   }
 }
 
-template <int NB>
+template <int NB, int KS>
 __global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int KS = a.ks_count, b = a.b;
+  const int b = a.b;
   double2* k_sm = reinterpret_cast<double2*>(smem_raw);                 // [NB][KS][32]
   double* w_re = reinterpret_cast<double*>(k_sm + size_t(NB) * KS * 32);  // [NB*8]
   double* w_im = w_re + NB * 8;
@@ -321,25 +320,25 @@ __global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
   const int q = warp & 3;
   const uint32_t tm = sh.tmem + (uint32_t(32 * q) << 16);
   if (warp < 4)
-    mma_warp<NB>(a, sh, k_sm, w_re, w_im, q, lane, tm);
+    mma_warp<NB, KS>(a, sh, k_sm, w_re, w_im, q, lane, tm);
   else
-    ew_warp<NB>(a, sh, stage + (warp - 4) * 64, q, (warp >> 2) - 1, lane, tm);
+    ew_warp<NB, KS>(a, sh, stage + (warp - 4) * 64, q, (warp >> 2) - 1, lane, tm);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   if (warp == 0) tmem_dealloc(sh.tmem, kTmemCols);
 }
 
-template <int NB>
+template <int NB, int KS>
 int launch(const Args& a, cudaStream_t st, int sms) {
   const size_t smem = size_t(NB) * a.ks_count * 32 * 16 + size_t(NB) * 8 * 16 + 8 * 64 * 16 + sizeof(Shared) + 64;
-  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
   const int64_t need = (a.tau + 63) / 64;  // 64 slots per CTA
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  dense_ws_kernel<NB><<<unsigned(grid), kThreads, smem, st>>>(a);
+  dense_ws_kernel<NB, KS><<<unsigned(grid), kThreads, smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense_ws_kernel)", err);
   return TPF_OK;
@@ -388,19 +387,19 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
   a.iters = iters;
   a.counter = static_cast<unsigned long long*>(workspace);
   switch ((b + 7) / 8) {
-    case 1: return ws::launch<1>(a, st, sms);
-    case 2: return ws::launch<2>(a, st, sms);
-    case 3: return ws::launch<3>(a, st, sms);
-    case 4: return ws::launch<4>(a, st, sms);
-    case 5: return ws::launch<5>(a, st, sms);
-    case 6: return ws::launch<6>(a, st, sms);
-    case 7: return ws::launch<7>(a, st, sms);
-    case 8: return ws::launch<8>(a, st, sms);
-    case 9: return ws::launch<9>(a, st, sms);
-    case 10: return ws::launch<10>(a, st, sms);
-    case 11: return ws::launch<11>(a, st, sms);
-    case 12: return ws::launch<12>(a, st, sms);
-    case 13: return ws::launch<13>(a, st, sms);
+    case 1: return a.ks_count == 2 ? ws::launch<1, 2>(a, st, sms) : ws::launch<1, 1>(a, st, sms);
+    case 2: return a.ks_count == 4 ? ws::launch<2, 4>(a, st, sms) : ws::launch<2, 3>(a, st, sms);
+    case 3: return a.ks_count == 6 ? ws::launch<3, 6>(a, st, sms) : ws::launch<3, 5>(a, st, sms);
+    case 4: return a.ks_count == 8 ? ws::launch<4, 8>(a, st, sms) : ws::launch<4, 7>(a, st, sms);
+    case 5: return a.ks_count == 10 ? ws::launch<5, 10>(a, st, sms) : ws::launch<5, 9>(a, st, sms);
+    case 6: return a.ks_count == 12 ? ws::launch<6, 12>(a, st, sms) : ws::launch<6, 11>(a, st, sms);
+    case 7: return a.ks_count == 14 ? ws::launch<7, 14>(a, st, sms) : ws::launch<7, 13>(a, st, sms);
+    case 8: return a.ks_count == 16 ? ws::launch<8, 16>(a, st, sms) : ws::launch<8, 15>(a, st, sms);
+    case 9: return a.ks_count == 18 ? ws::launch<9, 18>(a, st, sms) : ws::launch<9, 17>(a, st, sms);
+    case 10: return a.ks_count == 20 ? ws::launch<10, 20>(a, st, sms) : ws::launch<10, 19>(a, st, sms);
+    case 11: return a.ks_count == 22 ? ws::launch<11, 22>(a, st, sms) : ws::launch<11, 21>(a, st, sms);
+    case 12: return a.ks_count == 24 ? ws::launch<12, 24>(a, st, sms) : ws::launch<12, 23>(a, st, sms);
+    case 13: return a.ks_count == 26 ? ws::launch<13, 26>(a, st, sms) : ws::launch<13, 25>(a, st, sms);
     default: break;
   }
   return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");
