@@ -299,8 +299,8 @@ def run_ours():
         achieved = alg / (kms * 1e-3) / 1e12
         roofline = dict(bound="tensor", pipe="FP64 DMMA (mma.sync m8n8k4)", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
                         frac=achieved / peak_tf if peak_tf else None,
-                        traffic=traffic_from_profiles("dense_fpi_kernel", tau),
-                        kernel="dense_fpi_kernel", kernel_ms=kms,
+                        traffic=traffic_from_profiles("dense_ws_kernel", tau),
+                        kernel="dense_ws_kernel", kernel_ms=kms,
                         peak_source="measured in-run: DMMA-only probe (tpf_probe_fp64_tflops); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                         algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch")

@@ -22,10 +22,10 @@ run(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); run(); e1.record(); torch.cuda.synchronize()
 print("kernel ms (timing build)", e0.elapsed_time(e1), "sum_n", int(it.sum()))
-buf = np.zeros((148 * 16, 8), dtype=np.int64)
+buf = np.zeros((148 * 12, 8), dtype=np.int64)
 lib.tpf_debug_ws_phase_cycles(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)))
-b = buf.reshape(148, 16, 8)
-mma = b[:, 0:8].reshape(-1, 8); ew = b[:, 8:16].reshape(-1, 8)
+b = buf.reshape(148, 12, 8)
+mma = b[:, 0:4].reshape(-1, 8); ew = b[:, 4:12].reshape(-1, 8)
 print("MMA: rounds %.0f, wait-U %.1f%%, gemm %.1f%%, per-round gemm %.0f clk wait %.0f clk" % (
     mma[:, 6].mean(), 100 * mma[:, 0].mean() / mma[:, 7].mean(), 100 * mma[:, 1].mean() / mma[:, 7].mean(),
     mma[:, 1].mean() / mma[:, 6].mean(), mma[:, 0].mean() / mma[:, 6].mean()))
