@@ -215,3 +215,56 @@ def test_ws_kernel_full_c2_counts():
     assert int(it1.sum()) == 2615281
     V2, it2 = op.solve(S, kernel="pairs")
     assert torch.equal(V1, V2)
+
+
+@pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 64, 96, 100, 101, 104, 105, 128])
+def test_feeder_sizes_across_kernel_boundaries(b):
+    """Every node-block count of the shared-memory kernels (b <= 104) and the
+    switch to the large-b kernel (b = 105): counts exact vs the oracle."""
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, batch_solve_dense
+    spec = GenSpec(n_buses=b + 1, seed=b)
+    model = build_network(spec)
+    loads = gen_scenarios(model, 300, spec)
+    out = batch_solve_dense(model, loads)
+    V, n, mask, _ = orc.dense_per_case(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                       loads.values)
+    assert np.array_equal(out.iterations_per_case, n)
+    assert np.array_equal(out.converged_mask, mask)
+    assert np.abs(out.values - V).max() < 1e-12
+
+
+def test_nonfinite_and_zero_loads_are_data():
+    """NaN / inf loads never pass the step test: those cases run to the cap and are
+    flagged, the rest of the batch is unaffected (dense.py:189-193, 198-199)."""
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, batch_solve_dense, LoadMatrix
+    spec = GenSpec(n_buses=35, seed=1)
+    model = build_network(spec)
+    S = gen_scenarios(model, 64, spec).values.copy()
+    clean = batch_solve_dense(model, LoadMatrix(S))
+    S[3, 5] = np.nan
+    S[7, 9] = np.inf
+    S[:, 11] = 0.0
+    out = batch_solve_dense(model, LoadMatrix(S))
+    assert out.iterations_per_case[5] == 100 and out.iterations_per_case[9] == 100
+    assert not out.converged_mask[5] and not out.converged_mask[9]
+    assert out.converged_mask[11] and out.iterations_per_case[11] <= 1
+    keep = np.ones(64, bool)
+    keep[[5, 9, 11]] = False
+    assert np.array_equal(out.values[:, keep], clean.values[:, keep])
+
+
+def test_empty_batch():
+    from paper_2403_04578_b200 import GenSpec, build_network, batch_solve_dense, LoadMatrix
+    model = build_network(GenSpec(n_buses=9, seed=42))
+    out = batch_solve_dense(model, LoadMatrix(np.zeros((8, 0), complex)))
+    assert out.values.shape == (8, 0) and out.iterations == 0
+
+
+def test_max_iterations_cap_and_tolerance_options(golden):
+    """SolveOptions are honoured: a 2-iteration cap stops every case at 2."""
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_dense, SolveOptions
+    g = golden("c2_slice192")
+    out = batch_solve_dense(g.model, LoadMatrix(g.S), SolveOptions(max_iterations=2))
+    assert (out.iterations_per_case == 2).all() and out.iterations == 2
+    loose = batch_solve_dense(g.model, LoadMatrix(g.S), SolveOptions(tolerance=1e-4))
+    assert loose.iterations < 7

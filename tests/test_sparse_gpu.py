@@ -95,3 +95,33 @@ def test_tree_kernel_device_path_matches_pipeline(golden):
     host = solve(g, chunk_cases=100)
     dev = solve(g, return_on_device=True)
     assert np.array_equal(host.values, dev.values.cpu().numpy())
+
+
+def test_sparse_nonfinite_loads_flagged():
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, batch_solve_sparse, LoadMatrix
+    spec = GenSpec(n_buses=101, seed=3)
+    model = build_network(spec)
+    S = gen_scenarios(model, 40, spec).values.copy()
+    S[10, 4] = np.nan
+    for use_tree in (True, False):
+        out = batch_solve_sparse(model, LoadMatrix(S), use_tree=use_tree)
+        assert out.iterations_per_case[4] == 100 and not out.converged_mask[4]
+        assert out.converged_mask[np.arange(40) != 4].all()
+
+
+def test_sparse_fortran_order_same_bits(golden):
+    g = golden("acc3_b100_t100")
+    a = solve(g)
+    b = solve(g, S=np.asfortranarray(g.S))
+    assert np.array_equal(a.values, b.values)
+
+
+def test_sparse_matches_dense_on_c1_feeder():
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, batch_solve_sparse, batch_solve_dense
+    spec = GenSpec(n_buses=35, seed=0)
+    model = build_network(spec)
+    loads = gen_scenarios(model, 2000, spec)
+    d = batch_solve_dense(model, loads)
+    s = batch_solve_sparse(model, loads)
+    assert np.array_equal(d.iterations_per_case, s.iterations_per_case)
+    assert np.abs(d.values - s.values).max() < 1e-12
