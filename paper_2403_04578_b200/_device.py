@@ -72,13 +72,21 @@ def loads_to_device(values: np.ndarray, device: torch.device) -> torch.Tensor:
 
 
 def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tensor,
-                         iters: torch.Tensor, residual_tol: float, device: torch.device):
-    """Residual post-check and converged mask on the device (dense.py:198-199)."""
+                         iters: torch.Tensor, residual_tol: float, device: torch.device,
+                         csr=None, out=None):
+    """Residual post-check and converged mask on the device (dense.py:198-199).
+
+    ``csr`` (from ``contract.csr_on``) and ``out`` = (resid, mask, summ) may be
+    passed in to reuse device buffers: then the call only enqueues kernels.
+    """
     tau = V.shape[1]
-    rp, ci, val, src = contract.csr_on(device)
-    resid = torch.empty(tau, dtype=torch.float64, device=device)
-    mask = torch.empty(tau, dtype=torch.uint8, device=device)
-    summ = torch.zeros(2, dtype=torch.int32, device=device)
+    rp, ci, val, src = csr if csr is not None else contract.csr_on(device)
+    if out is None:
+        resid = torch.empty(tau, dtype=torch.float64, device=device)
+        mask = torch.empty(tau, dtype=torch.uint8, device=device)
+        summ = torch.empty(2, dtype=torch.int32, device=device)
+    else:
+        resid, mask, summ = out
     st = stream_ptr(device)
     sn, sc = complex_strides(S)
     vn, vc = complex_strides(V)
