@@ -97,29 +97,43 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
 
+// CTA tile TMV cases x TN nodes, 8 warps as WM x (8/WM).  Two instantiations:
+// TMV = 64 for the bulk of the solve and TMV = 8 for the heavy tail, when at
+// most kTailM cases are still active (near voltage collapse a few cases need
+// many more iterations; 64-row tiles would then be mostly empty rows).  Each
+// launch exits at once when the active count is outside its range.  Both
+// issue the same DMMAs in the same order for every output element, so a
+// case's bits do not depend on which one ran an iteration.
+constexpr int kTailM = 64;
+
+template <int TMV, int WM>
 __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
+  constexpr int WN = 8 / WM;
+  constexpr int MFR = TMV / WM / 8, NFR = TN / WN / 8;  // fragments per warp tile
+  constexpr int MFT = TMV / 8;                         // m-fragments per CTA tile
   const int n_act = a.count[cur];
-  const int m0 = blockIdx.x * TM;
+  if (TMV == 8 ? n_act > kTailM : n_act <= kTailM) return;
+  const int m0 = blockIdx.x * TMV;
   if (m0 >= n_act) return;
   const int n0 = blockIdx.y * TN;
   const int b = a.b;
   // fragment-ordered slabs: A[ks][mf][lane], B[ks][nf][lane]
   extern __shared__ __align__(16) double2 dyn_smem[];
-  double2 (*As)[KSTEPS * MF * 32] = reinterpret_cast<double2 (*)[KSTEPS * MF * 32]>(dyn_smem);
-  double2 (*Bs)[KSTEPS * NF * 32] = reinterpret_cast<double2 (*)[KSTEPS * NF * 32]>(dyn_smem + 2 * KSTEPS * MF * 32);
+  double2 (*As)[KSTEPS * MFT * 32] = reinterpret_cast<double2 (*)[KSTEPS * MFT * 32]>(dyn_smem);
+  double2 (*Bs)[KSTEPS * NF * 32] = reinterpret_cast<double2 (*)[KSTEPS * NF * 32]>(dyn_smem + 2 * KSTEPS * MFT * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2;  // 0..1 -> 32 cases
-  const int wn = warp & 3;   // 0..3 -> 16 nodes
+  const int wm = warp / WN;
+  const int wn = warp % WN;
 
   auto load_slab = [&](int stage, int k0) {
-    // A: TM x TK elements, element e: m = e % TM (fast, coalesced over cases), kk = e / TM
-    for (int e = tid; e < TM * TK; e += LTHREADS) {
-      const int m = e % TM, kk = e / TM;
+    // A: TMV x TK elements, element e: m = e % TMV (fast, coalesced over cases), kk = e / TMV
+    for (int e = tid; e < TMV * TK; e += LTHREADS) {
+      const int m = e % TMV, kk = e / TMV;
       const int gm = m0 + m, gk = k0 + kk;
       const bool ok = gm < n_act && gk < b;
       const double2* src = ok ? a.U + int64_t(gk) * a.tau + gm : a.U;
       const int ks = kk >> 2, mf = m >> 3;
-      cp_async16(&As[stage][(ks * MF + mf) * 32 + (m & 7) * 4 + (kk & 3)], src, ok);
+      cp_async16(&As[stage][(ks * MFT + mf) * 32 + (m & 7) * 4 + (kk & 3)], src, ok);
     }
     // B: K[n][k], element e: kk = e % TK (fast, contiguous in a K row), n = e / TK
     for (int e = tid; e < TN * TK; e += LTHREADS) {
@@ -133,11 +147,11 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  double cr[4][2][2], ci[4][2][2];
+  double cr[MFR][NFR][2], ci[MFR][NFR][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MFR; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < NFR; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
   const int nslabs = (b + TK - 1) / TK;
   load_slab(0, 0);
@@ -152,16 +166,16 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
     __syncthreads();
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
-      double2 af[4], bf[2];
+      double2 af[MFR], bf[NFR];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[stage][(ks * MF + wm * 4 + i) * 32 + lane];
+      for (int i = 0; i < MFR; ++i) af[i] = As[stage][(ks * MFT + wm * MFR + i) * 32 + lane];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[stage][(ks * NF + wn * 2 + j) * 32 + lane];
+      for (int j = 0; j < NFR; ++j) bf[j] = Bs[stage][(ks * NF + wn * NFR + j) * 32 + lane];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < MFR; ++i) {
         const double nui = neg_int(af[i].y);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NFR; ++j) {
           dmma884(cr[i][j][0], cr[i][j][1], af[i].x, bf[j].x);
           dmma884(ci[i][j][0], ci[i][j][1], af[i].x, bf[j].y);
           dmma884(cr[i][j][0], cr[i][j][1], nui, bf[j].y);
@@ -175,16 +189,16 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
   // epilogue: V' = acc + W, step test against the (guarded) old iterate, in-place update
   const int* act = a.act[cur];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+  for (int i = 0; i < MFR; ++i) {
+    const int m = m0 + wm * (MFR * 8) + i * 8 + (lane >> 2);
     bool row_bad = false;
     const bool mvalid = m < n_act;
     const int c = mvalid ? act[m] : 0;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < NFR; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int n = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + e;
+        const int n = n0 + wn * (NFR * 8) + j * 8 + 2 * (lane & 3) + e;
         if (mvalid && n < b) {
           double2* vp = a.V + n * a.v_node + int64_t(c) * a.v_case;
           double2 old = *vp;
@@ -278,12 +292,15 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   const dim3 ggrid(unsigned((tau + TM - 1) / TM), unsigned((b + TN - 1) / TN));
   const unsigned pgrid = unsigned(sms) * 8;
   const int gsmem = int(2 * KSTEPS * (MF + NF) * 32 * sizeof(double2));
-  cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
+  const int gsmem_tail = int(2 * KSTEPS * (1 + NF) * 32 * sizeof(double2));
+  cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel<TM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
   if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(gemm_kernel)", aerr);
+  const dim3 tgrid(unsigned(kTailM / 8), unsigned((b + TN - 1) / TN));
   for (int it = 0; it < max_iter; ++it) {
     const int cur = it & 1;
     prep_kernel<<<pgrid, 256, 0, st>>>(a, cur);
-    gemm_kernel<<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
+    gemm_kernel<TM, 2><<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
+    gemm_kernel<8, 1><<<tgrid, LTHREADS, gsmem_tail, st>>>(a, cur);
     compact_kernel<<<tb, 256, 0, st>>>(a, cur);
   }
   cudaError_t err = cudaGetLastError();
