@@ -79,12 +79,18 @@ int tpf_dense_fpi_c128(int64_t tau, int32_t b,
  * environment variable TPF_DENSE_KERNEL=pairs selects the second):
  *   _ws_    warp-specialised: per SM sub-partition one DMMA warp alternating
  *           between two slot groups and two elementwise warps (default);
+ *   _solo_  8 independent warps, each owning 8 slots and all node blocks;
  *   _pairs_ pairs of warps sharing 8 slots, each doing GEMM and elementwise. */
 int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b,
                           const double* S, int64_t s_node_stride, int64_t s_case_stride,
                           const double* K, const double* W, double v_flat_re, double v_flat_im,
                           double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
                           int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
+int tpf_dense_solo_fpi_c128(int64_t tau, int32_t b,
+                            const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                            const double* K, const double* W, double v_flat_re, double v_flat_im,
+                            double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
+                            int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
 int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b,
                              const double* S, int64_t s_node_stride, int64_t s_case_stride,
                              const double* K, const double* W, double v_flat_re, double v_flat_im,

@@ -34,6 +34,9 @@ SIGNATURES = {
     "tpf_dense_ws_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
         _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_dense_solo_fpi_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
+        _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
     "tpf_dense_pairs_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
         _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),

@@ -345,6 +345,221 @@ int launch(const Args& a, cudaStream_t st, int sms) {
 }
 
 }  // namespace ws
+
+// ---------------------------------------------------------------------------
+// "Solo" variant: 8 independent warps per SM, each owning 8 case slots and all
+// node blocks, each doing its own GEMM and elementwise work.  Two DMMA
+// streams per SM sub-partition (one warp issuing DMMAs cannot fill the FP64
+// tensor pipe: ~20 cycles per DMMA instead of 16 with one LDS per 4 DMMAs);
+// while one warp is in its elementwise phase the other keeps the pipe busy.
+// Per warp in its TMEM lane quadrant: U in A-fragment order (100 columns) and
+// the guarded iterate (104 columns); S is re-read from L2 each round.  No
+// inter-warp synchronisation at all after the prologue.
+namespace solo {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
+
+template <int NB, int KS>
+__global__ void __launch_bounds__(kThreads, 1) dense_solo_kernel(const ws::Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = a.b;
+  const int64_t tau = a.tau;
+  double2* k_sm = reinterpret_cast<double2*>(smem_raw);                 // [NB][KS][32]
+  double* w_re = reinterpret_cast<double*>(k_sm + size_t(NB) * KS * 32);  // [NB*8]
+  double* w_im = w_re + NB * 8;
+  double2* stage_all = reinterpret_cast<double2*>(w_im + NB * 8);       // [8 warps][64]
+  uint32_t* tmem_sm = reinterpret_cast<uint32_t*>(stage_all + kWarps * 64);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = lane >> 2, qq = lane & 3;
+
+  for (int idx = tid; idx < NB * KS * 32; idx += kThreads) {
+    const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
+    const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
+    k_sm[idx] = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
+  }
+  for (int i = tid; i < NB * 8; i += kThreads) {
+    const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
+    w_re[i] = w.x;
+    w_im[i] = w.y;
+  }
+  if (warp == 0) tmem_alloc(tmem_sm, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tm = *tmem_sm + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 256);
+  const uint32_t uv = tm, vc = tm + 104;  // U (A order, 100 cols) | guarded iterate (C order, 104 cols)
+  double2* stage = stage_all + warp * 64;
+  const double2* kb = k_sm + lane;
+
+  auto claim_slot = [&](bool want) {
+    int c = INT_MAX;
+    if (qq == 0 && want) c = ws::claim(a.counter);
+    return __shfl_sync(0xffffffffu, c, lane & ~3);
+  };
+  auto prefetch = [&](int c) {
+    if (c >= tau) return;
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int node = 8 * lb + 2 * qq + e;
+        if (node < b) {
+          const double* p = a.S + 2 * (node * a.s_node + int64_t(c) * a.s_case);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+  };
+
+  int cid = claim_slot(true);
+  int nxt = claim_slot(true);
+  if (cid >= tau) cid = INT_MAX;
+  prefetch(cid);
+  prefetch(nxt);
+  int n_it = 0;
+
+  double vr[NB][2], vi[NB][2];  // the iterate entering the next U (flat start)
+#pragma unroll
+  for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      vr[lb][e] = a.v_flat_re;
+      vi[lb][e] = a.v_flat_im;
+    }
+
+  for (;;) {
+    // ---- guard, keep the iterate (TMEM), U = S*/conj(v) in A-fragment order (TMEM) ----
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb) {
+      double xr[2], xi[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int node = 8 * lb + 2 * qq + e;
+        const double2 sv = (cid < tau && node < b) ? ldg_c128(a.S, node * a.s_node + int64_t(cid) * a.s_case)
+                                                   : make_double2(0.0, 0.0);
+        xr[e] = vr[lb][e];
+        xi[e] = vi[lb][e];
+        double m2 = __fma_rn(xr[e], xr[e], xi[e] * xi[e]);
+        if (m2 < kZeroGuard2) {  // fpi.py:39-41
+          xr[e] = kZeroGuard;
+          xi[e] = 0.0;
+          m2 = kZeroGuard * kZeroGuard;
+        }
+        const double r = 1.0 / m2;
+        const double sr = sv.x, si = -sv.y;  // S* (dense.py:154)
+        stage[slot * 8 + 2 * qq + e] =
+            make_double2(__fma_rn(sr, xr[e], -(si * xi[e])) * r, __fma_rn(sr, xi[e], si * xr[e]) * r);
+      }
+      tmem_st4d(vc + 8 * lb, xr[0], xr[1], xi[0], xi[1]);
+      __syncwarp();
+      const double2 u0 = stage[slot * 8 + qq];
+      const double2 u1 = stage[slot * 8 + 4 + qq];
+      __syncwarp();
+      if (2 * lb < KS) tmem_st4d(uv + 8 * lb, u0.x, u0.y, u1.x, u1.y);
+    }
+    tmem_wait_st();
+
+    // ---- GEMM: V' = W + U K^T ----
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb) {
+      const double2 wr = reinterpret_cast<const double2*>(w_re)[(8 * lb + 2 * qq) / 2];
+      const double2 wi = reinterpret_cast<const double2*>(w_im)[(8 * lb + 2 * qq) / 2];
+      vr[lb][0] = wr.x;
+      vr[lb][1] = wr.y;
+      vi[lb][0] = wi.x;
+      vi[lb][1] = wi.y;
+    }
+    {
+      D4 a0, a1;
+      tmem_ld4d(uv, a0);
+      tmem_wait_ld();
+#pragma unroll 1
+      for (int kp = 0; kp < KS; kp += 4) {
+        if (kp + 2 < KS) tmem_ld4d(uv + 4 * (kp + 2), a1);
+        ws::kpair<NB, KS>(vr, vi, a0, kb, kp);
+        tmem_wait_ld();
+        if (kp + 4 < KS) tmem_ld4d(uv + 4 * (kp + 4), a0);
+        if (kp + 2 < KS) ws::kpair<NB, KS>(vr, vi, a1, kb, kp + 2);
+        tmem_wait_ld();
+      }
+    }
+
+    // ---- per-case step test (dense.py:125-126, 189-193) ----
+    bool small = true;
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb) {
+      D4 ov;
+      tmem_ld4d(vc + 8 * lb, ov);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double dr = vr[lb][e] - ov.get(e), di = vi[lb][e] - ov.get(2 + e);
+        const int node = 8 * lb + 2 * qq + e;
+        if (node < b && !(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+      }
+    }
+    const uint32_t ball = __ballot_sync(0xffffffffu, small);
+    const bool my_small = ((ball >> (slot * 4)) & 0xFu) == 0xFu;
+    bool done = false;
+    if (cid != INT_MAX) {
+      ++n_it;
+      done = my_small || n_it >= a.max_iter;
+    }
+    if (__any_sync(0xffffffffu, done)) {
+      if (done) {
+#pragma unroll
+        for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int node = 8 * lb + 2 * qq + e;
+            if (node < b) {
+              double* p = a.V + 2 * (node * a.v_node + int64_t(cid) * a.v_case);
+              p[0] = vr[lb][e];
+              p[1] = vi[lb][e];
+            }
+          }
+        if (qq == 0) a.iters[cid] = n_it;
+      }
+      const int fresh_id = claim_slot(done);
+      if (done) {
+        cid = nxt < tau ? nxt : INT_MAX;
+        nxt = fresh_id;
+        n_it = 0;
+        prefetch(nxt);
+#pragma unroll
+        for (int lb = 0; lb < NB; ++lb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            vr[lb][e] = a.v_flat_re;
+            vi[lb][e] = a.v_flat_im;
+          }
+      }
+    }
+    if (__all_sync(0xffffffffu, cid == INT_MAX)) break;
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(*tmem_sm, 512);
+}
+
+template <int NB, int KS>
+int launch(const ws::Args& a, cudaStream_t st, int sms) {
+  const size_t smem = size_t(NB) * KS * 32 * 16 + size_t(NB) * 8 * 16 + kWarps * 64 * 16 + 64;
+  cudaError_t err = cudaFuncSetAttribute(dense_solo_kernel<NB, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+  if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_solo)", err);
+  int64_t grid = sms;
+  const int64_t need = (a.tau + 63) / 64;
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  dense_solo_kernel<NB, KS><<<unsigned(grid), kThreads, smem, st>>>(a);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(dense_solo_kernel)", err);
+  return TPF_OK;
+}
+
+}  // namespace solo
 }  // namespace tpf
 
 using namespace tpf;
@@ -400,6 +615,62 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
     case 11: return a.ks_count == 22 ? ws::launch<11, 22>(a, st, sms) : ws::launch<11, 21>(a, st, sms);
     case 12: return a.ks_count == 24 ? ws::launch<12, 24>(a, st, sms) : ws::launch<12, 23>(a, st, sms);
     case 13: return a.ks_count == 26 ? ws::launch<13, 26>(a, st, sms) : ws::launch<13, 25>(a, st, sms);
+    default: break;
+  }
+  return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");
+}
+
+extern "C" int tpf_dense_solo_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                       int64_t s_case_stride, const double* K, const double* W, double v_flat_re,
+                                       double v_flat_im, double tol, int32_t max_iter, double* V,
+                                       int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_dense_solo_fpi_c128: need tau >= 0 and b >= 1");
+  if (b > 104) return set_error(TPF_ERR_UNSUPPORTED, "tpf_dense_solo_fpi_c128: b > 104");
+  if (tau > INT_MAX - 4096) return set_error(TPF_ERR_INVALID, "tau too large for one launch; shard it");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!S || !K || !W || !V || !iters || !workspace || workspace_bytes < 256)
+    return set_error(TPF_ERR_INVALID, "tpf_dense_solo_fpi_c128: null pointer or small workspace");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+  if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
+  ws::Args a;
+  a.tau = tau;
+  a.b = b;
+  a.ks_count = (b + 3) / 4;
+  a.S = S;
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.K = K;
+  a.W = W;
+  a.v_flat_re = v_flat_re;
+  a.v_flat_im = v_flat_im;
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = V;
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  a.counter = static_cast<unsigned long long*>(workspace);
+  switch ((b + 7) / 8) {
+    case 1: return a.ks_count == 2 ? solo::launch<1, 2>(a, st, sms) : solo::launch<1, 1>(a, st, sms);
+    case 2: return a.ks_count == 4 ? solo::launch<2, 4>(a, st, sms) : solo::launch<2, 3>(a, st, sms);
+    case 3: return a.ks_count == 6 ? solo::launch<3, 6>(a, st, sms) : solo::launch<3, 5>(a, st, sms);
+    case 4: return a.ks_count == 8 ? solo::launch<4, 8>(a, st, sms) : solo::launch<4, 7>(a, st, sms);
+    case 5: return a.ks_count == 10 ? solo::launch<5, 10>(a, st, sms) : solo::launch<5, 9>(a, st, sms);
+    case 6: return a.ks_count == 12 ? solo::launch<6, 12>(a, st, sms) : solo::launch<6, 11>(a, st, sms);
+    case 7: return a.ks_count == 14 ? solo::launch<7, 14>(a, st, sms) : solo::launch<7, 13>(a, st, sms);
+    case 8: return a.ks_count == 16 ? solo::launch<8, 16>(a, st, sms) : solo::launch<8, 15>(a, st, sms);
+    case 9: return a.ks_count == 18 ? solo::launch<9, 18>(a, st, sms) : solo::launch<9, 17>(a, st, sms);
+    case 10: return a.ks_count == 20 ? solo::launch<10, 20>(a, st, sms) : solo::launch<10, 19>(a, st, sms);
+    case 11: return a.ks_count == 22 ? solo::launch<11, 22>(a, st, sms) : solo::launch<11, 21>(a, st, sms);
+    case 12: return a.ks_count == 24 ? solo::launch<12, 24>(a, st, sms) : solo::launch<12, 23>(a, st, sms);
+    case 13: return a.ks_count == 26 ? solo::launch<13, 26>(a, st, sms) : solo::launch<13, 25>(a, st, sms);
     default: break;
   }
   return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");

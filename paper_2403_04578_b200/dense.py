@@ -81,7 +81,8 @@ class DenseOperator:
         vn, vc = complex_strides(V)
         fn = "tpf_dense_fpi_large_c128" if self.large else "tpf_dense_fpi_c128"
         if kernel is not None and not self.large:
-            fn = {"ws": "tpf_dense_ws_fpi_c128", "pairs": "tpf_dense_pairs_fpi_c128"}[kernel]
+            fn = {"ws": "tpf_dense_ws_fpi_c128", "pairs": "tpf_dense_pairs_fpi_c128",
+                  "solo": "tpf_dense_solo_fpi_c128"}[kernel]
         _capi.call(fn, tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
                    self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                    V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),

@@ -188,10 +188,11 @@ def test_large_b_permutation_invariance_bitwise(golden):
     assert np.array_equal(b.values, a.values[:, perm])
 
 
+@pytest.mark.parametrize("kernel", ["pairs", "solo"])
 @pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
                                   "nine_zero_batch"])
-def test_ws_and_pair_kernels_bitwise_equal(golden, name):
-    """Warp-specialised and pair kernels: same DMMA order per element -> same bits."""
+def test_ws_and_pair_kernels_bitwise_equal(golden, name, kernel):
+    """Warp-specialised, pair and solo kernels: same DMMA order per element -> same bits."""
     import torch
     from paper_2403_04578_b200 import DenseOperator
     g = golden(name)
@@ -199,7 +200,7 @@ def test_ws_and_pair_kernels_bitwise_equal(golden, name):
     S = torch.from_numpy(g.S).cuda()
     o = g.opts()
     V1, it1 = op.solve(S, o, kernel="ws")
-    V2, it2 = op.solve(S, o, kernel="pairs")
+    V2, it2 = op.solve(S, o, kernel=kernel)
     assert torch.equal(it1, it2)
     assert torch.equal(V1, V2)
 
