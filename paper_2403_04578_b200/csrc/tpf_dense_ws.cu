@@ -177,17 +177,24 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
 
   for (;;) {
     // ---- guard, keep the iterate (TMEM), U = S*/conj(v) in A-fragment order ----
-    // S of the slot's case is re-read every round: the 64 slots x 148 SMs x 1.6 KB
-    // working set stays in L2, and the EW warps have a whole GEMM of slack.
-#pragma unroll
-    for (int lb = 0; lb < NB; ++lb) {
-      double2 sv[2];
+    // S of the slot's case is re-read every round (the 64 slots x 148 SMs x 1.6 KB
+    // working set stays in L2), two node blocks ahead of its use so the L2
+    // latency overlaps the previous blocks' arithmetic.
+    auto load_s = [&](double2 (&dst)[2], int lb) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int node = 8 * lb + 2 * qq + e;
-        sv[e] = (cid < tau && node < b) ? ldg_c128(a.S, node * a.s_node + int64_t(cid) * a.s_case)
-                                        : make_double2(0.0, 0.0);
+        dst[e] = (lb < NB && cid < tau && node < b) ? ldg_c128(a.S, node * a.s_node + int64_t(cid) * a.s_case)
+                                                    : make_double2(0.0, 0.0);
       }
+    };
+    double2 sq[3][2];
+    load_s(sq[0], 0);
+    load_s(sq[1], 1);
+#pragma unroll
+    for (int lb = 0; lb < NB; ++lb) {
+      load_s(sq[(lb + 2) % 3], lb + 2);
+      const double2* sv = sq[lb % 3];
       D4 nv;
       tmem_ld4d(uv + 8 * lb, nv);  // V' of the last GEMM (ignored by fresh slots)
       tmem_wait_ld();
