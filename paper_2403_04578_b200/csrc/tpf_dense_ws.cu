@@ -22,6 +22,7 @@
 //     fragment); the GEMM issues, per k-step, the 26 DMMAs that do not depend
 //     on each other before the 26 that accumulate onto them.
 #include <climits>
+#include <cstdlib>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -88,9 +89,11 @@ __device__ __forceinline__ void kpair(double (&vr)[NB][2], double (&vi)[NB][2], 
   }
 }
 
-template <int NB, int KS>
+// DMMA warp over node blocks [NB0, NB0 + NBW) of both slot groups of its SMSP.
+template <int KS, int NB0, int NBW, int SPLIT>
 __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double2* k_sm, const double* w_re,
                                          const double* w_im, int q, int lane, uint32_t tm) {
+  constexpr int NB = NBW;
   uint32_t par[2] = {0u, 0u};
   bool alive[2] = {true, true};
   const int qq = lane & 3;
@@ -107,8 +110,8 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
     double vr[NB][2], vi[NB][2];
 #pragma unroll
     for (int lb = 0; lb < NB; ++lb) {
-      const double2 wr = reinterpret_cast<const double2*>(w_re)[(8 * lb + 2 * qq) / 2];
-      const double2 wi = reinterpret_cast<const double2*>(w_im)[(8 * lb + 2 * qq) / 2];
+      const double2 wr = reinterpret_cast<const double2*>(w_re)[(8 * (NB0 + lb) + 2 * qq) / 2];
+      const double2 wi = reinterpret_cast<const double2*>(w_im)[(8 * (NB0 + lb) + 2 * qq) / 2];
       vr[lb][0] = wr.x;
       vr[lb][1] = wr.y;
       vi[lb][0] = wi.x;
@@ -119,7 +122,7 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
     D4 a0, a1;
     tmem_ld4d(uv, a0);
     tmem_wait_ld();
-    const double2* kb = k_sm + lane;
+    const double2* kb = k_sm + size_t(NB0) * KS * 32 + lane;
 #pragma unroll 1
     for (int kp = 0; kp < KS; kp += 4) {
       if (kp + 2 < KS) tmem_ld4d(uv + 4 * (kp + 2), a1);
@@ -129,9 +132,11 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
       if (kp + 2 < KS) kpair<NB, KS>(vr, vi, a1, kb, kp + 2);
       tmem_wait_ld();
     }
-    // V' in C-fragment order over the consumed U
+    // V' in C-fragment order over the consumed U -- with two DMMA warps, only
+    // once both have finished reading U (named barrier of the SMSP's pair)
+    if constexpr (SPLIT == 2) named_bar(1 + q, 64);
 #pragma unroll
-    for (int lb = 0; lb < NB; ++lb) tmem_st4d(uv + 8 * lb, vr[lb][0], vr[lb][1], vi[lb][0], vi[lb][1]);
+    for (int lb = 0; lb < NB; ++lb) tmem_st4d(uv + 8 * (NB0 + lb), vr[lb][0], vr[lb][1], vi[lb][0], vi[lb][1]);
     tmem_wait_st();
     tmem_fence_before();
     mbar_arrive(&sh.full_v[q][g]);
@@ -291,8 +296,12 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
   }
 }
 
-template <int NB, int KS>
-__global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
+// SPLIT DMMA warps per SMSP share each GEMM (node blocks split NBA / NB - NBA):
+// SPLIT = 1: 12 warps (4 DMMA + 8 EW); SPLIT = 2: 16 warps (8 DMMA + 8 EW), so
+// two DMMA streams feed every FP64 tensor pipe.
+template <int NB, int KS, int SPLIT>
+__global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const Args a) {
+  constexpr int NBA = SPLIT == 1 ? NB : (NB + 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = a.b;
   double2* k_sm = reinterpret_cast<double2*>(smem_raw);                 // [NB][KS][32]
@@ -302,12 +311,13 @@ __global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
   Shared& sh = *reinterpret_cast<Shared*>(stage + 8 * 64);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  for (int idx = tid; idx < NB * KS * 32; idx += kThreads) {
+  constexpr int kT = 32 * (8 + 4 * SPLIT);
+  for (int idx = tid; idx < NB * KS * 32; idx += kT) {
     const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
     const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
     k_sm[idx] = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
   }
-  for (int i = tid; i < NB * 8; i += kThreads) {
+  for (int i = tid; i < NB * 8; i += kT) {
     const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
     w_re[i] = w.x;
     w_im[i] = w.y;
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
     for (int q = 0; q < 4; ++q)
       for (int g = 0; g < 2; ++g) {
         mbar_init(&sh.full_u[q][g], 32);
-        mbar_init(&sh.full_v[q][g], 32);
+        mbar_init(&sh.full_v[q][g], 32 * SPLIT);
         sh.done[q][g] = 0;
       }
   }
@@ -326,26 +336,31 @@ __global__ void __launch_bounds__(kThreads, 1) dense_ws_kernel(const Args a) {
   tmem_fence_after();
   const int q = warp & 3;
   const uint32_t tm = sh.tmem + (uint32_t(32 * q) << 16);
-  if (warp < 4)
-    mma_warp<NB, KS>(a, sh, k_sm, w_re, w_im, q, lane, tm);
-  else
-    ew_warp<NB, KS>(a, sh, stage + (warp - 4) * 64, q, (warp >> 2) - 1, lane, tm);
+  const int wg = warp >> 2;
+  if (wg == 0) {
+    mma_warp<KS, 0, NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
+  } else if (SPLIT == 2 && wg == 1) {
+    if constexpr (SPLIT == 2) mma_warp<KS, NBA, NB - NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
+  } else {
+    const int e = warp - 4 * SPLIT;  // 0..7
+    ew_warp<NB, KS>(a, sh, stage + e * 64, q, e >> 2, lane, tm);
+  }
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   if (warp == 0) tmem_dealloc(sh.tmem, kTmemCols);
 }
 
-template <int NB, int KS>
+template <int NB, int KS, int SPLIT>
 int launch(const Args& a, cudaStream_t st, int sms) {
   const size_t smem = size_t(NB) * a.ks_count * 32 * 16 + size_t(NB) * 8 * 16 + 8 * 64 * 16 + sizeof(Shared) + 64;
-  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
   const int64_t need = (a.tau + 63) / 64;  // 64 slots per CTA
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  dense_ws_kernel<NB, KS><<<unsigned(grid), kThreads, smem, st>>>(a);
+  dense_ws_kernel<NB, KS, SPLIT><<<unsigned(grid), 32 * (8 + 4 * SPLIT), smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense_ws_kernel)", err);
   return TPF_OK;
@@ -571,6 +586,21 @@ int launch(const ws::Args& a, cudaStream_t st, int sms) {
 
 using namespace tpf;
 
+// Default: one DMMA warp per SMSP (12 warps).  TPF_WS_SPLIT=2 selects two DMMA
+// warps per SMSP sharing each GEMM (16 warps); measured slower on C2 (8.17 vs
+// 7.38 ms): the elementwise warps then cannot refill U fast enough.
+template <int NB, int KS>
+static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
+  static const int split = [] {
+    const char* e = getenv("TPF_WS_SPLIT");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
+  if constexpr (NB >= 2) {
+    if (split == 2) return ws::launch<NB, KS, 2>(a, st, sms);
+  }
+  return ws::launch<NB, KS, 1>(a, st, sms);
+}
+
 extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
                                      int64_t s_case_stride, const double* K, const double* W, double v_flat_re,
                                      double v_flat_im, double tol, int32_t max_iter, double* V, int64_t v_node_stride,
@@ -609,19 +639,19 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
   a.iters = iters;
   a.counter = static_cast<unsigned long long*>(workspace);
   switch ((b + 7) / 8) {
-    case 1: return a.ks_count == 2 ? ws::launch<1, 2>(a, st, sms) : ws::launch<1, 1>(a, st, sms);
-    case 2: return a.ks_count == 4 ? ws::launch<2, 4>(a, st, sms) : ws::launch<2, 3>(a, st, sms);
-    case 3: return a.ks_count == 6 ? ws::launch<3, 6>(a, st, sms) : ws::launch<3, 5>(a, st, sms);
-    case 4: return a.ks_count == 8 ? ws::launch<4, 8>(a, st, sms) : ws::launch<4, 7>(a, st, sms);
-    case 5: return a.ks_count == 10 ? ws::launch<5, 10>(a, st, sms) : ws::launch<5, 9>(a, st, sms);
-    case 6: return a.ks_count == 12 ? ws::launch<6, 12>(a, st, sms) : ws::launch<6, 11>(a, st, sms);
-    case 7: return a.ks_count == 14 ? ws::launch<7, 14>(a, st, sms) : ws::launch<7, 13>(a, st, sms);
-    case 8: return a.ks_count == 16 ? ws::launch<8, 16>(a, st, sms) : ws::launch<8, 15>(a, st, sms);
-    case 9: return a.ks_count == 18 ? ws::launch<9, 18>(a, st, sms) : ws::launch<9, 17>(a, st, sms);
-    case 10: return a.ks_count == 20 ? ws::launch<10, 20>(a, st, sms) : ws::launch<10, 19>(a, st, sms);
-    case 11: return a.ks_count == 22 ? ws::launch<11, 22>(a, st, sms) : ws::launch<11, 21>(a, st, sms);
-    case 12: return a.ks_count == 24 ? ws::launch<12, 24>(a, st, sms) : ws::launch<12, 23>(a, st, sms);
-    case 13: return a.ks_count == 26 ? ws::launch<13, 26>(a, st, sms) : ws::launch<13, 25>(a, st, sms);
+    case 1: return a.ks_count == 2 ? ws_launch<1, 2>(a, st, sms) : ws_launch<1, 1>(a, st, sms);
+    case 2: return a.ks_count == 4 ? ws_launch<2, 4>(a, st, sms) : ws_launch<2, 3>(a, st, sms);
+    case 3: return a.ks_count == 6 ? ws_launch<3, 6>(a, st, sms) : ws_launch<3, 5>(a, st, sms);
+    case 4: return a.ks_count == 8 ? ws_launch<4, 8>(a, st, sms) : ws_launch<4, 7>(a, st, sms);
+    case 5: return a.ks_count == 10 ? ws_launch<5, 10>(a, st, sms) : ws_launch<5, 9>(a, st, sms);
+    case 6: return a.ks_count == 12 ? ws_launch<6, 12>(a, st, sms) : ws_launch<6, 11>(a, st, sms);
+    case 7: return a.ks_count == 14 ? ws_launch<7, 14>(a, st, sms) : ws_launch<7, 13>(a, st, sms);
+    case 8: return a.ks_count == 16 ? ws_launch<8, 16>(a, st, sms) : ws_launch<8, 15>(a, st, sms);
+    case 9: return a.ks_count == 18 ? ws_launch<9, 18>(a, st, sms) : ws_launch<9, 17>(a, st, sms);
+    case 10: return a.ks_count == 20 ? ws_launch<10, 20>(a, st, sms) : ws_launch<10, 19>(a, st, sms);
+    case 11: return a.ks_count == 22 ? ws_launch<11, 22>(a, st, sms) : ws_launch<11, 21>(a, st, sms);
+    case 12: return a.ks_count == 24 ? ws_launch<12, 24>(a, st, sms) : ws_launch<12, 23>(a, st, sms);
+    case 13: return a.ks_count == 26 ? ws_launch<13, 26>(a, st, sms) : ws_launch<13, 25>(a, st, sms);
     default: break;
   }
   return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");

@@ -269,3 +269,28 @@ def test_max_iterations_cap_and_tolerance_options(golden):
     assert (out.iterations_per_case == 2).all() and out.iterations == 2
     loose = batch_solve_dense(g.model, LoadMatrix(g.S), SolveOptions(tolerance=1e-4))
     assert loose.iterations < 7
+
+
+def test_ws_two_dmma_warps_variant_bitwise_equal(golden):
+    """TPF_WS_SPLIT=2 (two DMMA warps per SMSP) gives the same bits (run in a subprocess:
+    the variant is chosen once per process)."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.');"
+            "from tests.conftest import Golden;"
+            "from paper_2403_04578_b200 import DenseOperator;"
+            "g = Golden('c2_slice192'); op = DenseOperator(g.model);"
+            "V, it = op.solve(torch.from_numpy(g.S).cuda(), g.opts(), kernel='ws');"
+            "np.save(sys.argv[1], V.cpu().numpy())")
+    import os
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for split in ("1", "2"):
+            f = os.path.join(d, f"v{split}.npy")
+            env = dict(os.environ, TPF_WS_SPLIT=split)
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(f))
+        assert np.array_equal(outs[0], outs[1])
