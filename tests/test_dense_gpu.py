@@ -276,8 +276,8 @@ def test_ws_two_dmma_warps_variant_bitwise_equal(golden):
     the variant is chosen once per process)."""
     import subprocess
     import sys
-    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.');"
-            "from tests.conftest import Golden;"
+    code = ("import numpy as np, torch, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "from conftest import Golden;"
             "from paper_2403_04578_b200 import DenseOperator;"
             "g = Golden('c2_slice192'); op = DenseOperator(g.model);"
             "V, it = op.solve(torch.from_numpy(g.S).cuda(), g.opts(), kernel='ws');"
