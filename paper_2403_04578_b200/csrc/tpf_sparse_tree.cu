@@ -41,7 +41,7 @@ struct TreeArgs {
   unsigned long long* counter;
   const int32_t* lvl;     // [levels+1] level offsets in level order (root level first), then [levels+1] slot starts
   const int4* info;       // per level-ordered node m: {original node, parent m or -1, first child m, child count}
-  const double2* coef;    // per m: {e = Y[parent, m], unused, uinv = 1/U[m,m], src}
+  const double2* coef;    // per m: {e = Y[parent, m], g = U[m,parent]/U[m,m], uinv = 1/U[m,m], src}
   double2 v_flat;
   double tol2;
   int max_iter;
@@ -54,11 +54,12 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 x) {
   return make_double2(__fma_rn(a.x, x.x, -(a.y * x.y)), __fma_rn(a.x, x.y, a.y * x.x));
 }
 
-constexpr int kSB = 3;  // slots per batch: their loads are issued together (ILP across slots)
+constexpr int kLS = 6;  // max TMEM slots of one level (the host schedule guarantees it)
+constexpr int kMaxRoots = 512;
 
-// Scaled sweeps (zhat = z / U_mm, so L[p,c] z_c = Y[p,c] zhat_c):
-//   up:   zhat_m = (r_m - sum_c e_c zhat_c) * uinv_m,   e_c = Y[parent(c), c]
-//   down: w_m    = zhat_m - uinv_m * e_m * w_parent     (U[m,p] = Y[m,p] = e_m for symmetric Y)
+// Sweeps with g_m = U[m,parent] / U[m,m] (so L[p,m] z_m = g_m z_m for symmetric Y):
+//   up:   z_m = r_m - sum_c g_c z_c
+//   down: w_m = z_m / U[m,m] - g_m w_parent
 __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const TreeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* T = reinterpret_cast<double2*>(smem_raw);       // [b] sweep vector (zhat, then w)
@@ -66,6 +67,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
   int2* kids = reinterpret_cast<int2*>(P + a.b);           // [b] {first child, count}
   int* par = reinterpret_cast<int*>(kids + a.b);           // [b] parent (-1 at roots)
   __shared__ int s_off[kMaxLevels + 1], s_j0[kMaxLevels + 1];
+  __shared__ double2 s_src[kMaxRoots];  // source injection of the root level (zero elsewhere)
+  __shared__ int s_slot_lvl[kMaxSlots];
   __shared__ int s_case;
   __shared__ uint32_t s_tmem;
 
@@ -80,12 +83,28 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     kids[m] = make_int2(inf.z, inf.w);
     par[m] = inf.y;
   }
+  __syncthreads();
+  for (int m = tid; m < s_off[1] && m < kMaxRoots; m += kTreeThreads) s_src[m] = __ldg(&a.coef[4 * m + 3]);
+  if (tid < kMaxSlots) {
+    int lv = 0;
+    for (int d = 0; d < L; ++d)
+      if (s_j0[d] <= tid && tid < s_j0[d + 1]) lv = d;
+    s_slot_lvl[tid] = lv;
+  }
   if (warp == 0) tmem_alloc(&s_tmem, 512);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tm = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 128);
   const uint32_t tm_v = tm, tm_s = tm + 4 * kMaxSlots;
+  const int nslots = s_j0[L];
+  // node of TMEM slot j of this thread (-1 if none): slot j belongs to level s_slot_lvl[j]
+  auto slot_node = [&](int j) {
+    if (j >= nslots) return -1;
+    const int d = s_slot_lvl[j];
+    const int m = s_off[d] + (j - s_j0[d]) * kTreeThreads + tid;
+    return m < s_off[d + 1] ? m : -1;
+  };
 
   for (;;) {
     if (tid == 0) {
@@ -97,68 +116,96 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     if (cs < 0) break;
 
     // ---- load the case: S into TMEM, flat start V (dense.py:155) ----
-    for (int d = 0; d < L; ++d) {
-      for (int j = s_j0[d]; j < s_j0[d + 1]; ++j) {
-        const int pos = (j - s_j0[d]) * kTreeThreads + tid;
-        double2 s = make_double2(0.0, 0.0);
-        if (s_off[d] + pos < s_off[d + 1]) {
-          const int node = __ldg(&a.info[s_off[d] + pos].x);
-          s = __ldg(a.S + node * a.s_node + int64_t(cs) * a.s_case);
+    // all of this thread's slots at once: the S loads are independent HBM/L2
+    // round trips, so they are issued together before any TMEM store
+#pragma unroll
+    for (int j0 = 0; j0 < kMaxSlots; j0 += 4) {
+      double2 sv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = slot_node(j0 + j);
+        sv[j] = make_double2(0.0, 0.0);
+        if (m >= 0) sv[j] = __ldg(a.S + __ldg(&a.info[m].x) * a.s_node + int64_t(cs) * a.s_case);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j0 + j < nslots) {  // warp-uniform
+          tmem_st2(tm_s + 4 * (j0 + j), sv[j]);
+          tmem_st2(tm_v + 4 * (j0 + j), a.v_flat);
         }
-        tmem_st2(tm_s + 4 * j, s);
-        tmem_st2(tm_v + 4 * j, a.v_flat);
       }
     }
     tmem_wait_st();
 
+    // Per level, every thread holds the data of its (at most kLS) slots of that
+    // level in registers: the TMEM iterate/load and the node coefficients.  A
+    // level's loads are issued right after the previous level's arithmetic,
+    // BEFORE the barrier, so their latency overlaps the barrier wait.
+    //   up:   z_m = r_m - sum_c P_c,  P_m = g_m z_m            (g = U[m,p] / U[m,m])
+    //   down: w_m = z_m / U_mm - g_m w_p
+    D2 vv[1], ss[1];
+    double2 cg[kLS], cu[kLS];
+    // global coefficient loads of a level, issued before the barrier that precedes it
+    auto issue_up = [&](int d) {
+      const int jb = s_j0[d], je = s_j0[d + 1], off = s_off[d], end = s_off[d + 1];
+#pragma unroll
+      for (int u = 0; u < kLS; ++u) {
+        const int m = off + u * kTreeThreads + tid;
+        cg[u] = (jb + u < je && m < end) ? __ldg(&a.coef[4 * m + 1]) : make_double2(0.0, 0.0);
+      }
+    };
+    auto issue_down = [&](int d) {
+      const int jb = s_j0[d], je = s_j0[d + 1], off = s_off[d], end = s_off[d + 1];
+#pragma unroll
+      for (int u = 0; u < kLS; ++u) {
+        const int m = off + u * kTreeThreads + tid;
+        const bool ok = jb + u < je && m < end;
+        cu[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
+        cg[u] = (ok && d > 0) ? __ldg(&a.coef[4 * m + 1]) : make_double2(0.0, 0.0);
+      }
+    };
+
     int it = 0;
+    issue_up(L - 1);
     while (it < a.max_iter) {
       // ---- up-sweep: deepest level first ----
       for (int d = L - 1; d >= 0; --d) {
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
-        for (int j = jb; j < je; j += kSB) {
-          D2 vv[kSB], ss[kSB];
-          double2 ui[kSB], src[kSB], e[kSB];
 #pragma unroll
-          for (int u = 0; u < kSB; ++u) {
-            if (j + u < je) {  // warp-uniform
-              tmem_ld2(tm_v + 4 * (j + u), vv[u]);
-              tmem_ld2(tm_s + 4 * (j + u), ss[u]);
-            }
-            const int m = off + (j + u - jb) * kTreeThreads + tid;
-            const bool ok = j + u < je && m < end;
-            ui[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
-            e[u] = (ok && d > 0) ? __ldg(&a.coef[4 * m]) : make_double2(0.0, 0.0);
-            src[u] = (ok && d == 0) ? __ldg(&a.coef[4 * m + 3]) : make_double2(0.0, 0.0);
+        for (int u = 0; u < kLS; ++u) {
+          const int m = off + u * kTreeThreads + tid;
+          if (jb + u < je) {  // warp-uniform
+            tmem_ld2(tm_v + 4 * (jb + u), vv[0]);
+            tmem_ld2(tm_s + 4 * (jb + u), ss[0]);
+            tmem_wait_ld();
           }
-          tmem_wait_ld();
-#pragma unroll
-          for (int u = 0; u < kSB; ++u) {
-            const int m = off + (j + u - jb) * kTreeThreads + tid;
-            if (j + u < je && m < end) {
-              double2 v = vv[u].get();
-              const double2 s = ss[u].get();
-              double m2 = __fma_rn(v.x, v.x, v.y * v.y);
-              if (m2 < kZeroGuard2) {  // fpi.py:39-41
-                v = make_double2(kZeroGuard, 0.0);
-                m2 = kZeroGuard * kZeroGuard;
-              }
-              const double r = 1.0 / m2;
-              // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
-              double2 z = make_double2(-(__fma_rn(s.x, v.x, s.y * v.y) * r + src[u].x),
-                                       -(__fma_rn(s.x, v.y, -(s.y * v.x)) * r + src[u].y));
-              const int2 k = kids[m];
-              for (int c = k.x; c < k.x + k.y; ++c) {
-                const double2 pc = P[c];
-                z.x -= pc.x;
-                z.y -= pc.y;
-              }
-              const double2 zh = cmul2(z, ui[u]);
-              T[m] = zh;
-              P[m] = cmul2(e[u], zh);
+          if (jb + u < je && m < end) {
+            double2 v = vv[0].get();
+            const double2 sl = ss[0].get();
+            double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+            if (m2 < kZeroGuard2) {  // fpi.py:39-41
+              v = make_double2(kZeroGuard, 0.0);
+              m2 = kZeroGuard * kZeroGuard;
             }
+            const double r = 1.0 / m2;
+            const double2 src = d == 0 ? s_src[m] : make_double2(0.0, 0.0);
+            // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
+            double2 z = make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
+                                     -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
+            const int2 k = kids[m];
+            for (int c = k.x; c < k.x + k.y; ++c) {
+              const double2 pc = P[c];
+              z.x -= pc.x;
+              z.y -= pc.y;
+            }
+            T[m] = z;
+            P[m] = cmul2(cg[u], z);
           }
         }
+        if (d > 0)
+          issue_up(d - 1);
+        else
+          issue_down(0);
         __syncthreads();
       }
       // ---- down-sweep: root level first, step test, iterate update ----
@@ -166,58 +213,51 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       int all_small = 0;
       for (int d = 0; d < L; ++d) {
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
-        for (int j = jb; j < je; j += kSB) {
-          D2 vv[kSB];
-          double2 e[kSB], ui[kSB];
 #pragma unroll
-          for (int u = 0; u < kSB; ++u) {
-            if (j + u < je) tmem_ld2(tm_v + 4 * (j + u), vv[u]);
-            const int m = off + (j + u - jb) * kTreeThreads + tid;
-            const bool ok = j + u < je && m < end && d > 0;
-            e[u] = ok ? __ldg(&a.coef[4 * m]) : make_double2(0.0, 0.0);
-            ui[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
-          }
-          tmem_wait_ld();
-#pragma unroll
-          for (int u = 0; u < kSB; ++u) {
-            if (j + u < je) {
-              const int m = off + (j + u - jb) * kTreeThreads + tid;
-              double2 v = vv[u].get();
-              double2 w = v;
-              if (m < end) {
-                w = T[m];
-                const int p = par[m];
-                if (p >= 0) w = cfma_sub(w, cmul2(ui[u], e[u]), T[p]);
-                T[m] = w;
-                if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
-                const double dr = w.x - v.x, di = w.y - v.y;
-                if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
-              }
-              tmem_st2(tm_v + 4 * (j + u), w);
+        for (int u = 0; u < kLS; ++u) {
+          if (jb + u < je) {
+            const int m = off + u * kTreeThreads + tid;
+            tmem_ld2(tm_v + 4 * (jb + u), vv[0]);
+            tmem_wait_ld();
+            double2 v = vv[0].get();
+            double2 w = v;
+            if (m < end) {
+              w = cmul2(T[m], cu[u]);
+              const int p = par[m];
+              if (p >= 0) w = cfma_sub(w, cg[u], T[p]);
+              T[m] = w;
+              if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+              const double dr = w.x - v.x, di = w.y - v.y;
+              if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
             }
+            tmem_st2(tm_v + 4 * (jb + u), w);
           }
         }
         tmem_wait_st();
-        if (d + 1 < L)
+        if (d + 1 < L) {
+          issue_down(d + 1);
           __syncthreads();
-        else
+        } else {
           all_small = __syncthreads_and(small);
+        }
       }
       ++it;
       if (all_small) break;
+      issue_up(L - 1);
     }
 
     // ---- retire: V out, per-case count ----
-    for (int d = 0; d < L; ++d) {
-      for (int j = s_j0[d]; j < s_j0[d + 1]; ++j) {
-        D2 vv;
-        tmem_ld2(tm_v + 4 * j, vv);
-        tmem_wait_ld();
-        const int m = s_off[d] + (j - s_j0[d]) * kTreeThreads + tid;
-        if (m < s_off[d + 1]) {
-          const int node = __ldg(&a.info[m].x);
-          a.V[node * a.v_node + int64_t(cs) * a.v_case] = vv.get();
-        }
+#pragma unroll
+    for (int j0 = 0; j0 < kMaxSlots; j0 += 4) {
+      D2 vo[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j0 + j < nslots) tmem_ld2(tm_v + 4 * (j0 + j), vo[j]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int m = slot_node(j0 + j);
+        if (m >= 0) a.V[__ldg(&a.info[m].x) * a.v_node + int64_t(cs) * a.v_case] = vo[j].get();
       }
     }
     if (tid == 0) a.iters[cs] = it;

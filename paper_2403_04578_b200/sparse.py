@@ -162,6 +162,8 @@ def factorize_ydd(y_dd) -> TreeLU:
 
 TREE_THREADS = 512      # CTA size of tpf_sparse_tree_fpi_c128
 TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
+TREE_LEVEL_SLOTS = 6    # slots of one depth level held in registers at a time
+TREE_MAX_ROOTS = 512    # root-level nodes (source injections kept in shared memory)
 TREE_MAX_NODES = 7800  # shared memory: sweep vector, child products, child ranges, parents: 44 B per node
 
 
@@ -261,7 +263,10 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
     src_o = np.asarray(src)[row_src[order]]
     if np.any(src_o[offs[1]:] != 0):
         return None  # source injection only at the root level (nodes next to the slack)
-    coef = np.stack([e, upar[order], f.u_diag_inv[order], src_o], axis=1).astype(complex)
+    g = upar[order] * f.u_diag_inv[order]  # U[m, parent] / U[m, m] = L[parent, m] for symmetric Y
+    if np.any(-(-sizes // TREE_THREADS) > TREE_LEVEL_SLOTS) or sizes[0] > TREE_MAX_ROOTS:
+        return None
+    coef = np.stack([e, g, f.u_diag_inv[order], src_o], axis=1).astype(complex)
     return TreeSchedule(b=b, levels=levels,
                         level_info=np.concatenate([offs, j0]).astype(np.int32),
                         node_info=np.ascontiguousarray(info.ravel()),
@@ -279,12 +284,14 @@ def tree_solve_host(t: TreeSchedule, rhs: np.ndarray) -> np.ndarray:
         for m in range(offs[d], offs[d + 1]):
             z = rhs[info[m, 0]]
             for c in range(info[m, 2], info[m, 2] + info[m, 3]):
-                z -= coef[c, 0] * T[c]
-            T[m] = z * coef[m, 2]
+                z -= coef[c, 1] * T[c]
+            T[m] = z
     for d in range(t.levels):
         for m in range(offs[d], offs[d + 1]):
+            w = T[m] * coef[m, 2]
             if info[m, 1] >= 0:
-                T[m] -= coef[m, 2] * coef[m, 0] * T[info[m, 1]]
+                w -= coef[m, 1] * T[info[m, 1]]
+            T[m] = w
     x = np.empty(b, dtype=complex)
     x[info[:, 0]] = T
     return x
