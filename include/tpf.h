@@ -160,6 +160,28 @@ int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels,
                              double* V, int64_t v_node_stride, int64_t v_case_stride,
                              int32_t* iters, void* workspace, size_t workspace_bytes,
                              void* stream);
+/* Same solve with the residual post-check (tpf_residual_c128, below) fused
+ * into the kernel's retire step: resid[j] is bit-identical to what
+ * tpf_residual_c128 computes from this call's V, and no second pass over
+ * S and V is made.  Y_dd is passed as level-ordered ELL rows built on the
+ * host by tpf_sparse_tree_build_ell (width <= tpf_sparse_tree_max_ell_width()):
+ *   ell_col int32[width*b], ell_val complex[width*b], entry r of level-ordered
+ *   row m at [r*b + m], columns level-ordered, -1 = padding.              */
+int tpf_sparse_tree_fpi_resid_c128(int64_t tau, int32_t b, int32_t levels,
+                                   const int32_t* level_info, const int32_t* node_info, const double* node_coef,
+                                   const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                                   double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                   double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                   int32_t* iters, int32_t ell_width, const int32_t* ell_col,
+                                   const double* ell_val, double* resid,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+int tpf_sparse_tree_max_ell_width(void);
+/* Host helpers (no device work): widest CSR row of Y_dd (-1 on bad input),
+ * and the ELL rows above from the ORIGINAL-order CSR and node_info.        */
+int tpf_sparse_tree_ell_width(int32_t b, const int32_t* ydd_row_ptr);
+int tpf_sparse_tree_build_ell(int32_t b, int32_t width, const int32_t* node_info,
+                              const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                              int32_t* ell_col, double* ell_val);
 
 /* -------------------------------------------------------------- residual --
  * residual_per_case (fpi.py:221-240, constant-power branch) as used by

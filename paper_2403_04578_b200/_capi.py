@@ -69,6 +69,12 @@ SIGNATURES = {
     "tpf_sparse_tree_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl,
         _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_sparse_tree_fpi_resid_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl,
+        _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_sparse_tree_max_ell_width": (ctypes.c_int, []),
+    "tpf_sparse_tree_ell_width": (ctypes.c_int, [_c_i32, _c_ptr]),
+    "tpf_sparse_tree_build_ell": (ctypes.c_int, [_c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr]),
     "tpf_sparse_tree_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64]),
     "tpf_sparse_tree_solve_host_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,

@@ -73,14 +73,15 @@ def loads_to_device(values: np.ndarray, device: torch.device) -> torch.Tensor:
 
 def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tensor,
                          iters: torch.Tensor, residual_tol: float, device: torch.device,
-                         csr=None, out=None):
+                         csr=None, out=None, have_resid: bool = False):
     """Residual post-check and converged mask on the device (dense.py:198-199).
 
     ``csr`` (from ``contract.csr_on``) and ``out`` = (resid, mask, summ) may be
     passed in to reuse device buffers: then the call only enqueues kernels.
+    ``have_resid``: ``out[0]`` already holds the residuals (a solver that fuses
+    the post-check, ``SparseOperator.solve(..., resid=)``); only the summary runs.
     """
     tau = V.shape[1]
-    rp, ci, val, src = csr if csr is not None else contract.csr_on(device)
     if out is None:
         resid = torch.empty(tau, dtype=torch.float64, device=device)
         mask = torch.empty(tau, dtype=torch.uint8, device=device)
@@ -90,8 +91,10 @@ def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tens
     st = stream_ptr(device)
     sn, sc = complex_strides(S)
     vn, vc = complex_strides(V)
-    _capi.call("tpf_residual_c128", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
-               rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
+    if not have_resid:
+        rp, ci, val, src = csr if csr is not None else contract.csr_on(device)
+        _capi.call("tpf_residual_c128", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                   rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
     _capi.call("tpf_batch_summary", tau, iters.data_ptr(), resid.data_ptr(), float(residual_tol),
                mask.data_ptr(), summ.data_ptr(), st)
     return resid, mask, summ

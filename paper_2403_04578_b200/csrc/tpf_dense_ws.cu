@@ -30,8 +30,8 @@
 namespace tpf {
 namespace ws {
 
-constexpr int kWarps = 12;  // warps 0-3: MMA (SMSP w), 4-7: EW group 0, 8-11: EW group 1
-constexpr int kThreads = 32 * kWarps;
+// 12 warps: warps 0-3: MMA (SMSP w), 4-7: EW group 0, 8-11: EW group 1
+// (the SPLIT=2 variant launches 16 warps: see ws_launch)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kGroupCols = 208;  // 104 (U / V' hand-off) + 104 (guarded iterate)
 

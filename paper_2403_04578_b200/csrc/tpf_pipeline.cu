@@ -170,6 +170,12 @@ struct ChunkSolver {
   virtual ~ChunkSolver() = default;
   virtual int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc,
                     int32_t* iters, cudaStream_t st) = 0;
+  // solvers whose kernel also computes the residual post-check override this
+  // (returning 1 = done, the separate residual kernel is skipped)
+  virtual int solve_resid(int64_t, const double*, int64_t, int64_t, double*, int64_t, int64_t, int32_t*,
+                          const int32_t*, const int32_t*, const double*, const double*, double*, cudaStream_t) {
+    return -1;
+  }
 };
 
 int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64_t s_node, int64_t s_case,
@@ -224,6 +230,17 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     cudaEventRecord(ss.in_done[k], sin);
     cudaStreamWaitEvent(scomp, ss.in_done[k], 0);
     if (c >= 2) cudaStreamWaitEvent(scomp, ss.out_done[k], 0);
+    rc = solver.solve_resid(n, d_S[k].as<double>(), dsn_S, dsc_S, d_V[k].as<double>(), dsn_V, dsc_V,
+                            d_it.as<int32_t>() + lo, d_rp.as<int32_t>(), d_ci.as<int32_t>(), d_yv.as<double>(),
+                            d_src.as<double>(), d_res.as<double>() + lo, scomp);
+    if (rc == TPF_OK) {
+      cudaEventRecord(ss.comp_done[k], scomp);
+      cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
+      TPF_CK(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
+      cudaEventRecord(ss.out_done[k], sout);
+      continue;
+    }
+    if (rc > 0) break;  // a real error from the fused solver
     rc = solver.solve(n, d_S[k].as<double>(), dsn_S, dsc_S, d_V[k].as<double>(), dsn_V, dsc_V,
                       d_it.as<int32_t>() + lo, scomp);
     if (rc != TPF_OK) break;
@@ -330,6 +347,16 @@ struct TreeChunk : ChunkSolver {
     return tpf_sparse_tree_fpi_c128(n, b, levels, lvl, info, coef, S, sn, sc, vre, vim, tol, max_iter, V, vn, vc, it,
                                     ws, ws_bytes, st);
   }
+  int ell_w = 0;  // 0: Y_dd rows too wide for the fused residual
+  const int32_t* ell_col = nullptr;
+  const double* ell_val = nullptr;
+  int solve_resid(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+                  const int32_t*, const int32_t*, const double*, const double*, double* resid,
+                  cudaStream_t st) override {
+    if (ell_w < 1) return -1;
+    return tpf_sparse_tree_fpi_resid_c128(n, b, levels, lvl, info, coef, S, sn, sc, vre, vim, tol, max_iter, V, vn,
+                                          vc, it, ell_w, ell_col, ell_val, resid, ws, ws_bytes, st);
+  }
 };
 
 }  // namespace
@@ -340,7 +367,7 @@ using namespace tpf;
 extern "C" size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                              int64_t ydd_nnz) {
   const int64_t chunk = pick_chunk(tau, chunk_cases);
-  const size_t model = size_t(b) * 256 + size_t(ydd_nnz) * 24 + 64 * 1024;
+  const size_t model = size_t(b) * 256 + size_t(ydd_nnz) * 24 + size_t(b) * 16 * 20 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, 256);
 }
 
@@ -373,7 +400,26 @@ extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t l
   TPF_CK(upload(di, node_info, size_t(b) * 4, st), "upload(node_info)");
   TPF_CK(upload(dc, node_coef, size_t(b) * 8, st), "upload(node_coef)");
   TPF_CK(dws.alloc(256), "cudaMalloc(workspace)");
+  // level-ordered ELL rows of Y_dd for the residual fused into the tree kernel
+  const int ell_w = tpf_sparse_tree_ell_width(b, ydd_row_ptr);
+  std::vector<int32_t> h_ec;
+  std::vector<double> h_ev;
+  DevBuf dec, dev_;
+  const bool fuse = ydd_col && ydd_val && ell_w >= 1 && ell_w <= tpf_sparse_tree_max_ell_width();
+  if (fuse) {
+    h_ec.resize(size_t(ell_w) * b);
+    h_ev.resize(size_t(ell_w) * b * 2);
+    int rc = tpf_sparse_tree_build_ell(b, ell_w, node_info, ydd_row_ptr, ydd_col, ydd_val, h_ec.data(), h_ev.data());
+    if (rc != TPF_OK) return rc;
+    TPF_CK(upload(dec, h_ec.data(), h_ec.size(), st), "upload(ell_col)");
+    TPF_CK(upload(dev_, h_ev.data(), h_ev.size(), st), "upload(ell_val)");
+  }
   TreeChunk sv;
+  if (fuse) {
+    sv.ell_w = ell_w;
+    sv.ell_col = dec.as<int32_t>();
+    sv.ell_val = dev_.as<double>();
+  }
   sv.b = b;
   sv.levels = levels;
   sv.lvl = dl.as<int32_t>();

@@ -19,6 +19,7 @@
 // CTA = 512 threads (16 warps, 4 per TMEM lane quadrant, 128 columns each =
 // 16 slots), one CTA per SM (all 512 TMEM columns), persistent over cases.
 #include <climits>
+#include <vector>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -45,6 +46,13 @@ struct TreeArgs {
   double2 v_flat;
   double tol2;
   int max_iter;
+  // optional fused residual post-check (same arithmetic as residual_kernel):
+  // Y_dd rows in level order as ELL, entry r of row m at [r * b + m] (coalesced
+  // over m), entries in the original CSR order, padding col = -1
+  int ell_w;
+  const int32_t* ell_col;
+  const double2* ell_val;
+  double* resid;          // or null
 };
 
 __device__ __forceinline__ double2 cfma_sub(double2 acc, double2 a, double2 x) {  // acc - a*x
@@ -56,6 +64,8 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 x) {
 
 constexpr int kLS = 6;  // max TMEM slots of one level (the host schedule guarantees it)
 constexpr int kMaxRoots = 512;
+constexpr int kMaxEllWidth = 16;  // widest Y_dd row the fused residual takes
+constexpr int kEllChunk = 8;      // ELL entries loaded together
 
 // Sweeps with g_m = U[m,parent] / U[m,m] (so L[p,m] z_m = g_m z_m for symmetric Y):
 //   up:   z_m = r_m - sum_c g_c z_c
@@ -70,6 +80,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
   __shared__ double2 s_src[kMaxRoots];  // source injection of the root level (zero elsewhere)
   __shared__ int s_slot_lvl[kMaxSlots];
   __shared__ int s_case;
+  __shared__ double s_red[kTreeThreads / 32];
   __shared__ uint32_t s_tmem;
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -246,7 +257,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       issue_up(L - 1);
     }
 
-    // ---- retire: V out, per-case count ----
+    // ---- retire: V out, per-case count; with the fused residual V also goes
+    // to T (the sweeps are done with it) ----
 #pragma unroll
     for (int j0 = 0; j0 < kMaxSlots; j0 += 4) {
       D2 vo[4];
@@ -257,7 +269,65 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int m = slot_node(j0 + j);
-        if (m >= 0) a.V[__ldg(&a.info[m].x) * a.v_node + int64_t(cs) * a.v_case] = vo[j].get();
+        if (m >= 0) {
+          const double2 v = vo[j].get();
+          a.V[__ldg(&a.info[m].x) * a.v_node + int64_t(cs) * a.v_case] = v;
+          if (a.resid) T[m] = v;
+        }
+      }
+    }
+    if (a.resid) {
+      // residual_per_case (fpi.py:221-240): max_i |s_i + v_i conj(src_i + (Y_dd v)_i)|,
+      // the operations of residual_kernel in the same order (bit-identical)
+      __syncthreads();
+      double worst = 0.0;
+      // per slot: every ELL entry load is issued at once (one L2 round trip),
+      // only the T[col] shared-memory reads depend on them
+#pragma unroll 2
+      for (int j = 0; j < nslots; ++j) {  // warp-uniform bound
+        D2 sd;
+        tmem_ld2(tm_s + 4 * j, sd);
+        const int m = slot_node(j);
+        double ar = 0.0, ai = 0.0;
+        if (m >= 0) {
+          const double2 si = __ldg(&a.coef[4 * m + 3]);
+          ar = si.x;
+          ai = si.y;
+        }
+        for (int r0 = 0; r0 < a.ell_w; r0 += kEllChunk) {
+          int c[kEllChunk];
+          double2 y[kEllChunk];
+#pragma unroll
+          for (int r = 0; r < kEllChunk; ++r) {
+            const bool ok = m >= 0 && r0 + r < a.ell_w;
+            c[r] = ok ? __ldg(a.ell_col + (r0 + r) * a.b + m) : -1;
+            y[r] = ok ? __ldg(a.ell_val + (r0 + r) * a.b + m) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int r = 0; r < kEllChunk; ++r) {
+            if (c[r] >= 0) {
+              const double2 v = T[c[r]];
+              ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
+              ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
+            }
+          }
+        }
+        tmem_wait_ld();
+        if (m >= 0) {
+          const double2 v = T[m];
+          const double2 sl = sd.get();
+          const double mr = sl.x + (v.x * ar + v.y * ai);
+          const double mi = sl.y + (v.y * ar - v.x * ai);
+          worst = nanmax(worst, hypot(mr, mi));
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) worst = nanmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+      if ((tid & 31) == 0) s_red[warp] = worst;
+      __syncthreads();
+      if (tid == 0) {
+        double w = 0.0;
+        for (int k = 0; k < kTreeThreads / 32; ++k) w = nanmax(w, s_red[k]);
+        a.resid[cs] = w;
       }
     }
     if (tid == 0) a.iters[cs] = it;
@@ -275,12 +345,12 @@ using namespace tpf;
 
 extern "C" int tpf_sparse_tree_max_slots(void) { return kMaxSlots; }
 
-extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
-                                        const int32_t* node_info, const double* node_coef, const double* S,
-                                        int64_t s_node_stride, int64_t s_case_stride, double v_flat_re,
-                                        double v_flat_im, double tol, int32_t max_iter, double* V,
-                                        int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
-                                        void* workspace, size_t workspace_bytes, void* stream) {
+static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info, const int32_t* node_info,
+                       const double* node_coef, const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                       double v_flat_re, double v_flat_im, double tol, int32_t max_iter, double* V,
+                       int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, int32_t ell_w,
+                       const int32_t* ell_col, const double* ell_val, double* resid, void* workspace,
+                       size_t workspace_bytes, void* stream) {
   if (tau < 0 || b < 1 || levels < 1 || levels > kMaxLevels)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: bad shape");
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
@@ -288,6 +358,8 @@ extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, 
   if (tau == 0) return TPF_OK;
   if (!level_info || !node_info || !node_coef || !S || !V || !iters || !workspace || workspace_bytes < 256)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: null pointer or small workspace");
+  if (resid && (!ell_col || !ell_val || ell_w < 1 || ell_w > kMaxEllWidth))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_resid_c128: bad ELL rows");
   const size_t smem = size_t(b) * (2 * sizeof(double2) + sizeof(int2) + sizeof(int));
   if (smem > 220 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_fpi_c128: b too large for one SM");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -316,6 +388,10 @@ extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, 
   a.v_flat = make_double2(v_flat_re, v_flat_im);
   a.tol2 = tol * tol;
   a.max_iter = max_iter;
+  a.ell_w = ell_w;
+  a.ell_col = ell_col;
+  a.ell_val = reinterpret_cast<const double2*>(ell_val);
+  a.resid = resid;
   int64_t grid = sms;
   if (tau < grid) grid = tau;
   sparse_tree_kernel<<<unsigned(grid), kTreeThreads, smem, st>>>(a);
@@ -323,3 +399,71 @@ extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, 
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_tree_kernel)", err);
   return TPF_OK;
 }
+
+extern "C" int tpf_sparse_tree_fpi_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
+                                        const int32_t* node_info, const double* node_coef, const double* S,
+                                        int64_t s_node_stride, int64_t s_case_stride, double v_flat_re,
+                                        double v_flat_im, double tol, int32_t max_iter, double* V,
+                                        int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  return tree_launch(tau, b, levels, level_info, node_info, node_coef, S, s_node_stride, s_case_stride, v_flat_re,
+                     v_flat_im, tol, max_iter, V, v_node_stride, v_case_stride, iters, 0, nullptr, nullptr, nullptr,
+                     workspace, workspace_bytes, stream);
+}
+
+extern "C" int tpf_sparse_tree_fpi_resid_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
+                                              const int32_t* node_info, const double* node_coef, const double* S,
+                                              int64_t s_node_stride, int64_t s_case_stride, double v_flat_re,
+                                              double v_flat_im, double tol, int32_t max_iter, double* V,
+                                              int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                              int32_t ell_width, const int32_t* ell_col, const double* ell_val,
+                                              double* resid, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!resid) return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_resid_c128: null resid");
+  return tree_launch(tau, b, levels, level_info, node_info, node_coef, S, s_node_stride, s_case_stride, v_flat_re,
+                     v_flat_im, tol, max_iter, V, v_node_stride, v_case_stride, iters, ell_width, ell_col, ell_val,
+                     resid, workspace, workspace_bytes, stream);
+}
+
+extern "C" int tpf_sparse_tree_ell_width(int32_t b, const int32_t* ydd_row_ptr) {
+  if (b < 1 || !ydd_row_ptr) {
+    set_error(TPF_ERR_INVALID, "tpf_sparse_tree_ell_width: bad argument");
+    return -1;
+  }
+  int w = 0;
+  for (int i = 0; i < b; ++i) w = ydd_row_ptr[i + 1] - ydd_row_ptr[i] > w ? ydd_row_ptr[i + 1] - ydd_row_ptr[i] : w;
+  return w;
+}
+
+extern "C" int tpf_sparse_tree_build_ell(int32_t b, int32_t width, const int32_t* node_info,
+                                         const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                                         int32_t* ell_col, double* ell_val) {
+  if (b < 1 || width < 1 || !node_info || !ydd_row_ptr || !ydd_col || !ydd_val || !ell_col || !ell_val)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_build_ell: bad argument");
+  std::vector<int32_t> m_of(size_t(b), -1);
+  for (int m = 0; m < b; ++m) {
+    const int i = node_info[4 * m];
+    if (i < 0 || i >= b || m_of[i] >= 0) return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_build_ell: bad node_info");
+    m_of[i] = m;
+  }
+  for (int m = 0; m < b; ++m) {
+    const int i = node_info[4 * m];
+    const int lo = ydd_row_ptr[i], n = ydd_row_ptr[i + 1] - lo;
+    if (n > width) return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_build_ell: row wider than width");
+    for (int r = 0; r < width; ++r) {
+      const size_t at = size_t(r) * b + m;
+      if (r < n) {
+        const int c = ydd_col[lo + r];
+        if (c < 0 || c >= b) return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_build_ell: bad column");
+        ell_col[at] = m_of[c];
+        ell_val[2 * at] = ydd_val[2 * (lo + r)];
+        ell_val[2 * at + 1] = ydd_val[2 * (lo + r) + 1];
+      } else {
+        ell_col[at] = -1;
+        ell_val[2 * at] = ell_val[2 * at + 1] = 0.0;
+      }
+    }
+  }
+  return TPF_OK;
+}
+
+extern "C" int tpf_sparse_tree_max_ell_width(void) { return kMaxEllWidth; }

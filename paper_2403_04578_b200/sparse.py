@@ -273,6 +273,19 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
                         node_coef=np.ascontiguousarray(coef.ravel()), slots=int(j0[-1]))
 
 
+def tree_ell(t: TreeSchedule, contract) -> tuple[int, np.ndarray, np.ndarray] | None:
+    """Level-ordered ELL rows of Y_dd for the fused residual (tpf_sparse_tree_build_ell), or None."""
+    lib = _capi.load()
+    rp, ci, yv = host_csr(contract)
+    w = int(lib.tpf_sparse_tree_ell_width(t.b, ptr(rp)))
+    if w < 1 or w > int(lib.tpf_sparse_tree_max_ell_width()):
+        return None
+    col = np.empty(w * t.b, dtype=np.int32)
+    val = np.empty(w * t.b, dtype=np.complex128)
+    _capi.call("tpf_sparse_tree_build_ell", t.b, w, ptr(t.node_info), ptr(rp), ptr(ci), ptr(yv), ptr(col), ptr(val))
+    return w, col, val
+
+
 def tree_solve_host(t: TreeSchedule, rhs: np.ndarray) -> np.ndarray:
     """Numpy emulation of the tree kernel's two sweeps (host-logic tests only)."""
     b = t.b
@@ -333,10 +346,14 @@ class SparseOperator:
                         perm=t(f.perm), src=t(self.contract.src))
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
+        self._csr = None
         self.tree = tree_schedule(f, self.contract.src) if use_tree else None
         if self.tree is not None:
             self.tree_dev = dict(level_info=t(self.tree.level_info), node_info=t(self.tree.node_info),
                                  node_coef=t(self.tree.node_coef))
+            ell = tree_ell(self.tree, self.contract)
+            if ell is not None:  # residual post-check fused into the tree kernel
+                self.tree_dev.update(ell_w=ell[0], ell_col=t(ell[1]), ell_val=t(ell[2]))
 
     @property
     def b(self) -> int:
@@ -346,7 +363,19 @@ class SparseOperator:
     def kernel(self) -> str:
         return "sparse_tree_kernel" if self.tree is not None else "sparse_fpi_kernel"
 
-    def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V=None, iters=None):
+    def csr(self):
+        """Y_dd CSR + source injection on the device (original node order), cached."""
+        if self._csr is None:
+            self._csr = self.contract.csr_on(self.device)
+        return self._csr
+
+    def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V=None, iters=None, resid=None):
+        """Iterate a device b x tau load tensor; returns ``(V, iters)``.
+
+        With ``resid`` (float64[tau] device tensor) the residual post-check
+        (fpi.py:221-240) is also written: fused into the tree kernel's retire
+        step, or by ``tpf_residual_c128`` after the general kernel.
+        """
         b, tau = S.shape
         if b != self.b:
             raise ValueError(f"load matrix has {b} rows, model has {self.b}")
@@ -360,11 +389,17 @@ class SparseOperator:
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
             g = self.tree_dev
-            _capi.call("tpf_sparse_tree_fpi_c128", tau, b, self.tree.levels, g["level_info"].data_ptr(),
-                       g["node_info"].data_ptr(), g["node_coef"].data_ptr(), S.data_ptr(), sn, sc,
-                       self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
-                       V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
-                       stream_ptr(self.device))
+            head = (tau, b, self.tree.levels, g["level_info"].data_ptr(), g["node_info"].data_ptr(),
+                    g["node_coef"].data_ptr(), S.data_ptr(), sn, sc, self.v_flat.real, self.v_flat.imag,
+                    float(opts.tolerance), int(opts.max_iterations), V.data_ptr(), vn, vc, iters.data_ptr())
+            tail = (self._ws.data_ptr(), self._ws.numel(), stream_ptr(self.device))
+            if resid is not None and "ell_w" in g:
+                _capi.call("tpf_sparse_tree_fpi_resid_c128", *head, g["ell_w"], g["ell_col"].data_ptr(),
+                           g["ell_val"].data_ptr(), resid.data_ptr(), *tail)
+                return V, iters
+            _capi.call("tpf_sparse_tree_fpi_c128", *head, *tail)
+            if resid is not None:
+                self._residual(S, V, resid)
             return V, iters
         need = int(_capi.load().tpf_sparse_workspace_bytes(tau, b))
         if self._ws is None or self._ws.numel() < need:
@@ -379,7 +414,17 @@ class SparseOperator:
                    self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                    V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
                    stream_ptr(self.device))
+        if resid is not None:
+            self._residual(S, V, resid)
         return V, iters
+
+    def _residual(self, S, V, resid):
+        rp, ci, val, src = self.csr()
+        sn, sc = complex_strides(S)
+        vn, vc = complex_strides(V)
+        _capi.call("tpf_residual_c128", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                   rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(),
+                   stream_ptr(self.device))
 
 
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
@@ -403,8 +448,12 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
         return _solve_host_pipeline(model, loads, opts, device, chunk_cases, use_tree)
     op = SparseOperator(model, device, use_tree=use_tree)
     S = loads_to_device(loads.values, op.device)
-    V, iters = op.solve(S, opts)
-    resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
+    resid = torch.empty(S.shape[1], dtype=torch.float64, device=op.device)
+    V, iters = op.solve(S, opts, resid=resid)
+    out = (resid, torch.empty(S.shape[1], dtype=torch.uint8, device=op.device),
+           torch.empty(2, dtype=torch.int32, device=op.device))
+    resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device,
+                                             out=out, have_resid=True)
     return finish(V, iters, resid, mask, summ, return_on_device)
 
 

@@ -137,6 +137,28 @@ class TestTreeSchedule:
                 assert info[p, 2] <= mm < info[p, 2] + info[p, 3]
         assert t.slots <= 16
 
+    @pytest.mark.parametrize("n_buses", [2, 9, 1001])
+    def test_ell_rows_reproduce_ydd_in_level_order(self, n_buses):
+        """tpf_sparse_tree_build_ell (host helper of the fused residual) == Y_dd permuted to level order."""
+        from paper_2403_04578_b200.sparse import tree_schedule, tree_ell
+        from paper_2403_04578_b200._device import ModelContract
+        m = build_network(GenSpec(n_buses=n_buses, seed=7))
+        t = tree_schedule(factorize_ydd(m.admittance.y_dd), m.source_injection())
+        w, col, val = tree_ell(t, ModelContract.of(m))
+        b = m.n_demand
+        y = m.admittance.y_dd.toarray()
+        orig = t.node_info.reshape(b, 4)[:, 0]
+        dense = np.zeros((b, b), dtype=complex)
+        col, val = col.reshape(w, b), val.reshape(w, b)
+        for mm in range(b):
+            row = m.admittance.y_dd.getrow(orig[mm])
+            n = row.nnz
+            assert (col[n:, mm] == -1).all() and (val[n:, mm] == 0).all()
+            # same entries in the same (original CSR) order
+            assert np.array_equal(orig[col[:n, mm]], row.indices) and np.array_equal(val[:n, mm], row.data)
+            dense[mm, col[:n, mm]] = val[:n, mm]
+        assert np.array_equal(dense, y[np.ix_(orig, orig)])
+
     def test_c3_feeder_fits_the_tmem_budget(self):
         from paper_2403_04578_b200.sparse import tree_schedule
         m = build_network(GenSpec(n_buses=5001, seed=0))

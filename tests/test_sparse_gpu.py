@@ -125,3 +125,42 @@ def test_sparse_matches_dense_on_c1_feeder():
     s = batch_solve_sparse(model, loads)
     assert np.array_equal(d.iterations_per_case, s.iterations_per_case)
     assert np.abs(d.values - s.values).max() < 1e-12
+
+
+@pytest.mark.parametrize("name", ["c3_slice6", "c1_slice512", "nine_t500", "acc7_mixed_zero"])
+def test_fused_residual_bitwise_equals_residual_kernel(golden, name):
+    """tpf_sparse_tree_fpi_resid_c128's in-kernel post-check == tpf_residual_c128 on the same V."""
+    import torch
+    from paper_2403_04578_b200 import SparseOperator
+    from paper_2403_04578_b200._device import residual_and_summary
+    g = golden(name)
+    op = SparseOperator(g.model, "cuda:0")
+    if op.tree is None:
+        pytest.skip("not a tree schedule")
+    S = torch.from_numpy(np.ascontiguousarray(g.S)).to("cuda:0")
+    tau = S.shape[1]
+    fused = torch.full((tau,), -1.0, dtype=torch.float64, device="cuda:0")
+    V, iters = op.solve(S, g.opts(), resid=fused)
+    ref, _, _ = residual_and_summary(op.contract, S, V, iters, 1e-8, op.device)
+    a, b = fused.cpu().numpy(), ref.cpu().numpy()
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    assert np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+
+
+def test_fused_residual_nonfinite_case():
+    import torch
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, SparseOperator, SolveOptions
+    from paper_2403_04578_b200._device import residual_and_summary
+    spec = GenSpec(n_buses=101, seed=3)
+    model = build_network(spec)
+    S = gen_scenarios(model, 40, spec).values.copy()
+    S[10, 4] = np.nan
+    op = SparseOperator(model, "cuda:0")
+    St = torch.from_numpy(S).to("cuda:0")
+    fused = torch.empty(40, dtype=torch.float64, device="cuda:0")
+    V, iters = op.solve(St, SolveOptions(), resid=fused)
+    ref, _, _ = residual_and_summary(op.contract, St, V, iters, 1e-8, op.device)
+    a, b = fused.cpu().numpy(), ref.cpu().numpy()
+    assert np.isnan(a[4]) and np.isnan(b[4])
+    keep = np.arange(40) != 4
+    assert np.array_equal(a[keep], b[keep])
