@@ -5,6 +5,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import hashlib
+
 import numpy as np
 import torch
 from scipy import sparse
@@ -46,6 +48,15 @@ class ModelContract:
                    src=np.ascontiguousarray(np.asarray(model.source_injection(), dtype=complex)),
                    v_s=complex(model.slack.v_s),
                    constant_power=bool(model.zip.is_constant_power))
+
+    def fingerprint(self) -> bytes:
+        """Digest of everything the solve reads (Y_dd pattern and values, src, v_s)."""
+        h = hashlib.blake2b(digest_size=20)
+        y = self.y_dd
+        for a in (np.asarray(y.shape, dtype=np.int64), y.indptr, y.indices, y.data, self.src,
+                  np.asarray([self.v_s], dtype=complex)):
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.digest()
 
     def csr_on(self, device: torch.device):
         rp = torch.from_numpy(self.y_dd.indptr.astype(np.int32)).to(device)

@@ -298,11 +298,17 @@ size_t pipeline_bytes(int64_t tau, int b, int64_t chunk, size_t model_bytes, siz
          model_bytes + r(solver_ws) + 4096;
 }
 
-int64_t pick_chunk(int64_t tau, int64_t requested) {
+int64_t pick_chunk(int64_t tau, int b, int64_t requested) {
   if (requested > 0) return requested < tau ? requested : (tau > 0 ? tau : 1);
   int64_t c = (tau + 15) / 16;  // ~16 chunks: fill/drain costs ~1/8 of the transfer time
-  if (c < 16384) c = 16384;
+  if (c < 16384) c = 16384;     // enough cases per launch to fill 148 SMs
   c = (c + 4095) / 4096 * 4096;
+  // but at most ~192 MB of S per chunk: the first H2D and the last D2H are
+  // not overlapped, so a chunk's transfer time is the pipeline's fill+drain
+  int64_t cap = (int64_t(192) << 20) / (int64_t(b) * 16);
+  if (cap < 1024) cap = 1024;
+  cap = cap / 256 * 256;
+  if (c > cap) c = cap;
   return c < tau ? c : (tau > 0 ? tau : 1);
 }
 
@@ -366,7 +372,7 @@ using namespace tpf;
 
 extern "C" size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                              int64_t ydd_nnz) {
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   const size_t model = size_t(b) * 256 + size_t(ydd_nnz) * 24 + size_t(b) * 16 * 20 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, 256);
 }
@@ -393,7 +399,7 @@ extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t l
   ArenaScope arena(workspace, workspace_bytes);
   Streams ss;
   TPF_CK(ss.init(), "cudaStreamCreate");
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   cudaStream_t st = ss.s[1];
   DevBuf dl, di, dc, dws;
   TPF_CK(upload(dl, level_info, size_t(levels + 1) * 2, st), "upload(levels)");
@@ -437,7 +443,7 @@ extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t l
 
 extern "C" size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                        int64_t ydd_nnz) {
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   const bool large = b > tpf_dense_max_nodes();
   const size_t solver = large ? tpf_dense_large_workspace_bytes(chunk, b) : tpf_dense_workspace_bytes(b);
   const size_t model = size_t(b) * b * 16 + size_t(b) * 128 + size_t(ydd_nnz) * 24 + 64 * 1024;
@@ -446,7 +452,7 @@ extern "C" size_t tpf_dense_solve_host_workspace_bytes(int64_t tau, int32_t b, i
 
 extern "C" size_t tpf_sparse_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                         int64_t ydd_nnz, int64_t l_nnz, int64_t u_nnz) {
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   const size_t model = size_t(b) * 128 + size_t(ydd_nnz + l_nnz + u_nnz) * 24 + 64 * 1024;
   return pipeline_bytes(tau, b, chunk, model, tpf_sparse_workspace_bytes(chunk, b));
 }
@@ -470,7 +476,7 @@ extern "C" int tpf_dense_solve_host_c128(int64_t tau, int32_t b, const double* S
   Streams ss;
   TPF_CK(ss.init(), "cudaStreamCreate");
   const bool large = b > tpf_dense_max_nodes();
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   DevBuf dK, dW, dws;
   TPF_CK(upload(dK, K, size_t(b) * b * 2, ss.s[1]), "upload(K)");
   TPF_CK(upload(dW, W, size_t(b) * 2, ss.s[1]), "upload(W)");
@@ -520,7 +526,7 @@ extern "C" int tpf_sparse_solve_host_c128(int64_t tau, int32_t b, const double* 
   ArenaScope arena(workspace, workspace_bytes);
   Streams ss;
   TPF_CK(ss.init(), "cudaStreamCreate");
-  const int64_t chunk = pick_chunk(tau, chunk_cases);
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   const int64_t lnnz = l_ptr[b], unnz = u_ptr[b];
   DevBuf dlp, dlc, dlv, dup, duc, duv, dud, dperm, dsrc, dws;
   cudaStream_t st = ss.s[1];

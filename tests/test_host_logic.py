@@ -171,3 +171,28 @@ class TestTreeSchedule:
         y = rng.normal(0, 1, (6, 6)) + 1j * rng.normal(0, 1, (6, 6))
         np.fill_diagonal(y, np.abs(y).sum(axis=1) + 20.0)
         assert tree_schedule(factorize_ydd(sparse.csc_matrix(y)), np.zeros(6, complex)) is None
+
+
+class TestDenseOperatorCache:
+    def test_cache_returns_same_bits_and_tracks_content(self):
+        from paper_2403_04578_b200.dense import dense_kw
+        from paper_2403_04578_b200._device import ModelContract
+        m = build_network(GenSpec(n_buses=30, seed=2))
+        c = ModelContract.of(m)
+        K1, W1 = dense_kw(c)
+        K2, W2 = dense_kw(ModelContract.of(m))
+        assert K1 is K2 and W1 is W2
+        assert np.array_equal(K1, -np.linalg.inv(c.y_dd.toarray()))
+        # a different feeder (or changed impedances) never hits the entry
+        m2 = build_network(GenSpec(n_buses=30, seed=3))
+        K3, _ = dense_kw(ModelContract.of(m2))
+        assert K3 is not K1 and not np.array_equal(K3, K1)
+
+    def test_singular_ydd_still_raises(self):
+        from scipy import sparse as sp
+        from paper_2403_04578_b200.dense import dense_kw
+        from paper_2403_04578_b200._device import ModelContract
+        c = ModelContract(b=2, y_dd=sp.csr_matrix(np.array([[1, 1], [1, 1]], dtype=complex)),
+                          src=np.zeros(2, dtype=complex), v_s=1 + 0j, constant_power=True)
+        with pytest.raises(np.linalg.LinAlgError):
+            dense_kw(c)
