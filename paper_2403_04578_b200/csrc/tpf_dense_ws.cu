@@ -23,6 +23,7 @@
 //     on each other before the 26 that accumulate onto them.
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -34,6 +35,11 @@ namespace ws {
 // (the SPLIT=2 variant launches 16 warps: see ws_launch)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kGroupCols = 208;  // 104 (U / V' hand-off) + 104 (guarded iterate)
+// 3M variant: V' of node blocks [0, kM3Pass0) goes to a per-group scratch area
+// after the two groups (columns 416 + 48 g), so the second pass can still read
+// all of U from the hand-off buffer
+constexpr int kM3Pass0 = 6;
+constexpr uint32_t kScratchCol = 2 * kGroupCols;
 
 struct Args {
   int64_t tau;
@@ -48,11 +54,69 @@ struct Args {
   int64_t v_node, v_case;
   int32_t* iters;
   unsigned long long* counter;
+  // step-test bracket (3M variant): high words of |delta| bounds, see step_small
+  int tol_hi_small, tol_hi_big;
 };
+
+#ifdef TPF_PHASE_TIMING
+// debug build only (tools/build_timing.sh): per-warp cycle accounting,
+// [block][warp][8] = {wait U, gemm | U round, wait V', test, retire, rounds, total}
+__device__ long long g_ws_cyc[148 * 12 * 8];
+struct PhaseClock {
+  long long c[8], t, t_start;
+  __device__ __forceinline__ void start() {
+    for (int i = 0; i < 8; ++i) c[i] = 0;
+    t = t_start = clock64();
+  }
+  __device__ __forceinline__ void mark(int i) {
+    const long long n = clock64();
+    c[i] += n - t;
+    t = n;
+  }
+  __device__ __forceinline__ void round() { ++c[6]; }
+  __device__ __forceinline__ void flush() {
+    c[7] = clock64() - t_start;
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 148 && w < 12)
+      for (int i = 0; i < 8; ++i) g_ws_cyc[(blockIdx.x * 12 + w) * 8 + i] = c[i];
+  }
+};
+#else
+struct PhaseClock {
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void round() {}
+  __device__ __forceinline__ void flush() {}
+};
+#endif
 
 __device__ __forceinline__ int claim(unsigned long long* counter) {
   const unsigned long long c = atomicAdd(counter, 1ull);
   return c < (unsigned long long)INT_MAX ? int(c) : INT_MAX;
+}
+
+// 1/x for the iterate's |v|^2 (in [1e-24, ~1e300]): MUFU seed + two Newton
+// steps, faithfully rounded; 4 FP64 instructions instead of the IEEE divide's
+// ~10 (every FP64 instruction here costs the SMSP's DMMA stream ~9 cycles).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+__device__ __forceinline__ int abs_hi(double x) { return __double2hiint(x) & 0x7fffffff; }
+
+// Step test of the 3M variant: |dr + i di|^2 < tol^2 is decided on the
+// integer pipe when the high words of |dr|, |di| are clearly below 0.7 tol
+// (true) or above tol (false) -- exact either way, see tpf_dense_ws_fpi_c128 --
+// and by the FP64 test only for the rare values in between.  NaN/inf have the
+// largest high words, so they never pass.
+// v (guarded) has |v|^2 >= 1e-24 for sure when |re| or |im| >= 1.01e-12
+__device__ __forceinline__ bool maybe_tiny(double x, double y) {
+  return max(abs_hi(x), abs_hi(y)) <= 0x3d71c4a2;  // high word of 1.01e-12
 }
 
 struct Shared {
@@ -143,13 +207,151 @@ __device__ __forceinline__ void mma_warp(const Args& a, Shared& sh, const double
   }
 }
 
-template <int NB, int KS>
+// 3M complex GEMM (Gauss): per node block three real accumulators
+//   P1 = sum ur kr,  P2 = sum ui ki,  P3 = sum (ur + ui)(kr + ki)
+//   V' = W + (P1 - P2) + i (P3 - P1 - P2)
+// i.e. 3 DMMAs per block and k-step instead of 4 (6 b^2 instead of 8 b^2 real
+// flops per case-iteration); kr + ki and ur + ui are formed in registers.
+// One k-step (compile-time H selects the half of the A fragment D4).
+template <int KS, int B0, int NBP, int NKS, int H>
+__device__ __forceinline__ void kstep3(double (&p1)[NBP][2], double (&p2)[NBP][2], double (&p3)[NBP][2], const D4& af,
+                                       const double2* kb, const double* ksb, int ks) {
+  const double ur = af.get(2 * H), ui = af.get(2 * H + 1);
+  const double us = ur + ui;
+  const double2* k0 = kb + size_t(ks) * 32;
+#pragma unroll
+  for (int lb = 0; lb < NBP; ++lb) {
+    const double2 k = k0[size_t(B0 + lb) * KS * 32];
+    // kr + ki: precomputed in shared memory for the first NKS blocks
+    const double kss = (B0 + lb < NKS) ? ksb[(size_t(B0 + lb) * KS + ks) * 32] : k.x + k.y;
+    dmma884(p1[lb][0], p1[lb][1], ur, k.x);
+    dmma884(p2[lb][0], p2[lb][1], ui, k.y);
+    dmma884(p3[lb][0], p3[lb][1], us, kss);
+  }
+}
+
+// Shared-memory layout of the kernel: K^T fragments (kr, ki) [NB][KS][32],
+// W re / im [NB*8] each, EW staging [8][64], Shared; the 3M variant adds
+// W re + im [NB*8] and, for as many node blocks as fit, kr + ki [NKS][KS][32].
+template <int NB, int KS, bool M3>
+struct Layout {
+  static constexpr size_t k_bytes = size_t(NB) * KS * 32 * 16;
+  static constexpr size_t w_off = k_bytes;
+  static constexpr size_t stage_off = w_off + size_t(NB) * 8 * 16;
+  static constexpr size_t shared_off = stage_off + 8 * 64 * 16;
+  static constexpr size_t wsum_off = shared_off + 256;
+  static constexpr size_t ks_off = wsum_off + (M3 ? size_t(NB) * 8 * 8 : 0);
+  static constexpr size_t cap = 232448;  // 227 KB opt-in maximum per block
+  static constexpr size_t plane = size_t(KS) * 32 * 8;
+  static constexpr int fit = int((cap - ks_off) / plane);
+  static constexpr int NKS = !M3 ? 0 : (fit < NB ? fit : NB);
+  static constexpr size_t bytes = ks_off + size_t(NKS) * plane;
+};
+
+// One pass over all k-steps for node blocks [B0, B0 + NBP); V' written to
+// TMEM at dst + 8 lb (C-fragment order, same layout as the 4M path).  The
+// accumulators start at P1 = Re W, P2 = 0, P3 = Re W + Im W, so
+// V' = (P1 - P2) + i ((P3 - P1) - P2).
+template <int KS, int B0, int NBP, int NKS>
+__device__ __forceinline__ void pass3(uint32_t uv, uint32_t dst, const double2* kb, const double* ksb,
+                                      const double* w_re, const double* w_sum, int qq) {
+  double p1[NBP][2], p2[NBP][2], p3[NBP][2];
+#pragma unroll
+  for (int lb = 0; lb < NBP; ++lb) {
+    const double2 wr = reinterpret_cast<const double2*>(w_re)[(8 * (B0 + lb) + 2 * qq) / 2];
+    const double2 ws = reinterpret_cast<const double2*>(w_sum)[(8 * (B0 + lb) + 2 * qq) / 2];
+    p1[lb][0] = wr.x;
+    p1[lb][1] = wr.y;
+    p2[lb][0] = p2[lb][1] = 0.0;
+    p3[lb][0] = ws.x;
+    p3[lb][1] = ws.y;
+  }
+  // k-steps in groups of 4 (two TMEM A-fragment loads, ping-pong) with no
+  // run-time conditions in the loop; the KS % 4 tail is unrolled at compile time
+  D4 a0, a1;
+  tmem_ld4d(uv, a0);
+  tmem_wait_ld();
+  constexpr int KM = KS / 4 * 4;
+#pragma unroll 1
+  for (int kp = 0; kp < KM; kp += 4) {
+    tmem_ld4d(uv + 4 * (kp + 2), a1);
+    kstep3<KS, B0, NBP, NKS, 0>(p1, p2, p3, a0, kb, ksb, kp);
+    kstep3<KS, B0, NBP, NKS, 1>(p1, p2, p3, a0, kb, ksb, kp + 1);
+    tmem_wait_ld();
+    if (kp + 4 < KS) tmem_ld4d(uv + 4 * (kp + 4), a0);  // uniform; false only on the last pass
+    kstep3<KS, B0, NBP, NKS, 0>(p1, p2, p3, a1, kb, ksb, kp + 2);
+    kstep3<KS, B0, NBP, NKS, 1>(p1, p2, p3, a1, kb, ksb, kp + 3);
+    tmem_wait_ld();
+  }
+  if constexpr (KS - KM >= 1) kstep3<KS, B0, NBP, NKS, 0>(p1, p2, p3, a0, kb, ksb, KM);
+  if constexpr (KS - KM >= 2) kstep3<KS, B0, NBP, NKS, 1>(p1, p2, p3, a0, kb, ksb, KM + 1);
+  if constexpr (KS - KM >= 3) {
+    tmem_ld4d(uv + 4 * (KM + 2), a1);
+    tmem_wait_ld();
+    kstep3<KS, B0, NBP, NKS, 0>(p1, p2, p3, a1, kb, ksb, KM + 2);
+  }
+#pragma unroll
+  for (int lb = 0; lb < NBP; ++lb) {
+    const double r0 = p1[lb][0] - p2[lb][0], r1 = p1[lb][1] - p2[lb][1];
+    const double i0 = (p3[lb][0] - p1[lb][0]) - p2[lb][0];
+    const double i1 = (p3[lb][1] - p1[lb][1]) - p2[lb][1];
+    tmem_st4d(dst + 8 * lb, r0, r1, i0, i1);
+  }
+}
+
+// 3M DMMA warp (one per SMSP, both groups).  NB <= kM3Pass0: one pass straight
+// into the hand-off buffer; otherwise blocks [0, 6) first (into the group's
+// scratch columns: U is still needed), then blocks [6, NB) (into the hand-off
+// buffer, after the last read of U).
+template <int NB, int KS, int NKS>
+__device__ __forceinline__ void mma_warp3(const Args& a, Shared& sh, const double2* k_sm, const double* ks_sm,
+                                          const double* w_re, const double* w_sum, int q, int lane, uint32_t tm) {
+  uint32_t par[2] = {0u, 0u};
+  bool alive[2] = {true, true};
+  const int qq = lane & 3;
+  const double2* kb = k_sm + lane;
+  const double* ksb = ks_sm + lane;
+  PhaseClock pc;
+  pc.start();
+  for (int g = 0; alive[0] || alive[1]; g ^= 1) {
+    if (!alive[g]) continue;
+    pc.mark(5);
+    mbar_wait(&sh.full_u[q][g], par[g]);
+    par[g] ^= 1u;
+    tmem_fence_after();
+    pc.mark(0);
+    if (sh.done[q][g]) {
+      alive[g] = false;
+      continue;
+    }
+    pc.round();
+    const uint32_t uv = tm + g * kGroupCols;
+    if constexpr (NB <= kM3Pass0) {
+      pass3<KS, 0, NB, NKS>(uv, uv, kb, ksb, w_re, w_sum, qq);
+    } else {
+      pass3<KS, 0, kM3Pass0, NKS>(uv, tm + kScratchCol + g * 8 * kM3Pass0, kb, ksb, w_re, w_sum, qq);
+      pass3<KS, kM3Pass0, NB - kM3Pass0, NKS>(uv, uv + 8 * kM3Pass0, kb, ksb, w_re, w_sum, qq);
+    }
+    tmem_wait_st();
+    tmem_fence_before();
+    mbar_arrive(&sh.full_v[q][g]);
+    pc.mark(1);
+  }
+  pc.flush();
+}
+
+template <int NB, int KS, bool M3>
 __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stage, int q, int g, int lane,
                                         uint32_t tm) {
   const int slot = lane >> 2, qq = lane & 3;
   const int b = a.b;
   const int64_t tau = a.tau;
   const uint32_t uv = tm + g * kGroupCols, vc = uv + 104;
+  // where the MMA warp left V' of node block lb
+  const uint32_t scr = tm + kScratchCol + g * 8 * kM3Pass0;
+  auto vp = [&](int lb) -> uint32_t {
+    return (M3 && NB > kM3Pass0 && lb < kM3Pass0) ? scr + 8 * lb : uv + 8 * lb;
+  };
   int cid = INT_MAX, nxt = INT_MAX, n_it = 0;
   bool fresh = true;  // this lane's slot starts from the flat voltage next round
   uint32_t par = 0u;
@@ -179,8 +381,11 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
   if (cid >= tau) cid = INT_MAX;
   prefetch(cid);
   prefetch(nxt);
+  PhaseClock pc;
+  pc.start();
 
   for (;;) {
+    pc.round();
     // ---- guard, keep the iterate (TMEM), U = S*/conj(v) in A-fragment order ----
     // S of the slot's case is re-read every round (the 64 slots x 148 SMs x 1.6 KB
     // working set stays in L2), two node blocks ahead of its use so the L2
@@ -201,7 +406,7 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
       load_s(sq[(lb + 2) % 3], lb + 2);
       const double2* sv = sq[lb % 3];
       D4 nv;
-      tmem_ld4d(uv + 8 * lb, nv);  // V' of the last GEMM (ignored by fresh slots)
+      tmem_ld4d(vp(lb), nv);  // V' of the last GEMM (ignored by fresh slots)
       tmem_wait_ld();
       double xr[2], xi[2];
 #pragma unroll
@@ -209,12 +414,22 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
         xr[e] = fresh ? a.v_flat_re : nv.get(e);
         xi[e] = fresh ? a.v_flat_im : nv.get(2 + e);
         double m2 = __fma_rn(xr[e], xr[e], xi[e] * xi[e]);
-        if (m2 < kZeroGuard2) {  // fpi.py:39-41
-          xr[e] = kZeroGuard;
-          xi[e] = 0.0;
-          m2 = kZeroGuard * kZeroGuard;
+        double r;
+        if constexpr (M3) {
+          if (maybe_tiny(xr[e], xi[e]) && m2 < kZeroGuard2) {  // fpi.py:39-41
+            xr[e] = kZeroGuard;
+            xi[e] = 0.0;
+            m2 = kZeroGuard * kZeroGuard;
+          }
+          r = rcp_nr(m2);
+        } else {
+          if (m2 < kZeroGuard2) {  // fpi.py:39-41
+            xr[e] = kZeroGuard;
+            xi[e] = 0.0;
+            m2 = kZeroGuard * kZeroGuard;
+          }
+          r = 1.0 / m2;
         }
-        const double r = 1.0 / m2;
         const double sr = sv[e].x, si = -sv[e].y;  // S* (dense.py:154)
         const double ur = __fma_rn(sr, xr[e], -(si * xi[e])) * r;
         const double ui = __fma_rn(sr, xi[e], si * xr[e]) * r;
@@ -232,23 +447,45 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
     tmem_fence_before();
     mbar_arrive(&sh.full_u[q][g]);
     fresh = false;
+    pc.mark(2);
 
     // ---- wait for V' of this group, per-case step test (dense.py:125-126, 189-193) ----
     mbar_wait(&sh.full_v[q][g], par);
     par ^= 1u;
     tmem_fence_after();
+    pc.mark(3);
     bool small = true;
 #pragma unroll
     for (int lb = 0; lb < NB; ++lb) {
       D4 nv, ov;
-      tmem_ld4d(uv + 8 * lb, nv);
+      tmem_ld4d(vp(lb), nv);
       tmem_ld4d(vc + 8 * lb, ov);
       tmem_wait_ld();
+      if constexpr (M3) {
+        double dr[2], di[2];
+        bool ok[2], unsure[2];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double dr = nv.get(e) - ov.get(e), di = nv.get(2 + e) - ov.get(2 + e);
-        const int node = 8 * lb + 2 * qq + e;
-        if (node < b && !(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+        for (int e = 0; e < 2; ++e) {
+          dr[e] = nv.get(e) - ov.get(e);
+          di[e] = nv.get(2 + e) - ov.get(2 + e);
+          const int m = max(abs_hi(dr[e]), abs_hi(di[e]));
+          const bool pad = 8 * lb + 2 * qq + e >= b;
+          ok[e] = pad || m < a.tol_hi_small;
+          unsure[e] = !ok[e] && m <= a.tol_hi_big;
+        }
+        if (__any_sync(0xffffffffu, unsure[0] || unsure[1])) {  // rare: |delta| within [0.7 tol, tol]
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (unsure[e]) ok[e] = __fma_rn(dr[e], dr[e], di[e] * di[e]) < a.tol2;
+        }
+        small = small && ok[0] && ok[1];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double dr = nv.get(e) - ov.get(e), di = nv.get(2 + e) - ov.get(2 + e);
+          const int node = 8 * lb + 2 * qq + e;
+          if (node < b && !(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+        }
       }
     }
     const uint32_t ball = __ballot_sync(0xffffffffu, small);
@@ -258,12 +495,13 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
       ++n_it;
       done = my_small || n_it >= a.max_iter;
     }
+    pc.mark(4);
     if (__any_sync(0xffffffffu, done)) {
       // retire: V' of the retiring slots to global memory, per-case count
 #pragma unroll
       for (int lb = 0; lb < NB; ++lb) {
         D4 nv;
-        tmem_ld4d(uv + 8 * lb, nv);
+        tmem_ld4d(vp(lb), nv);
         tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -286,6 +524,7 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
         prefetch(nxt);
       }
     }
+    pc.mark(5);
     if (__all_sync(0xffffffffu, cid == INT_MAX)) {
       if (lane == 0) sh.done[q][g] = 1;
       __syncwarp();
@@ -294,33 +533,40 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
       break;
     }
   }
+  pc.flush();
 }
 
 // SPLIT DMMA warps per SMSP share each GEMM (node blocks split NBA / NB - NBA):
 // SPLIT = 1: 12 warps (4 DMMA + 8 EW); SPLIT = 2: 16 warps (8 DMMA + 8 EW), so
 // two DMMA streams feed every FP64 tensor pipe.
-template <int NB, int KS, int SPLIT>
+template <int NB, int KS, int SPLIT, bool M3>
 __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const Args a) {
   constexpr int NBA = SPLIT == 1 ? NB : (NB + 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  using L = Layout<NB, KS, M3>;
   const int b = a.b;
   double2* k_sm = reinterpret_cast<double2*>(smem_raw);                 // [NB][KS][32]
-  double* w_re = reinterpret_cast<double*>(k_sm + size_t(NB) * KS * 32);  // [NB*8]
+  double* w_re = reinterpret_cast<double*>(smem_raw + L::w_off);        // [NB*8]
   double* w_im = w_re + NB * 8;
-  double2* stage = reinterpret_cast<double2*>(w_im + NB * 8);           // [8 EW warps][64]
-  Shared& sh = *reinterpret_cast<Shared*>(stage + 8 * 64);
+  double2* stage = reinterpret_cast<double2*>(smem_raw + L::stage_off);  // [8 EW warps][64]
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw + L::shared_off);
+  double* w_sum = reinterpret_cast<double*>(smem_raw + L::wsum_off);     // [NB*8] (3M)
+  double* ks_sm = reinterpret_cast<double*>(smem_raw + L::ks_off);       // [NKS][KS][32] (3M)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   constexpr int kT = 32 * (8 + 4 * SPLIT);
   for (int idx = tid; idx < NB * KS * 32; idx += kT) {
     const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
     const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
-    k_sm[idx] = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
+    const double2 k = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
+    k_sm[idx] = k;
+    if (M3 && nb < L::NKS) ks_sm[idx] = k.x + k.y;  // the same DADD the GEMM does for the other blocks
   }
   for (int i = tid; i < NB * 8; i += kT) {
     const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
     w_re[i] = w.x;
     w_im[i] = w.y;
+    if (M3) w_sum[i] = w.x + w.y;
   }
   if (tid == 0) {
     for (int q = 0; q < 4; ++q)
@@ -338,12 +584,15 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   const uint32_t tm = sh.tmem + (uint32_t(32 * q) << 16);
   const int wg = warp >> 2;
   if (wg == 0) {
-    mma_warp<KS, 0, NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
+    if constexpr (M3)
+      mma_warp3<NB, KS, L::NKS>(a, sh, k_sm, ks_sm, w_re, w_sum, q, lane, tm);
+    else
+      mma_warp<KS, 0, NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
   } else if (SPLIT == 2 && wg == 1) {
     if constexpr (SPLIT == 2) mma_warp<KS, NBA, NB - NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
   } else {
     const int e = warp - 4 * SPLIT;  // 0..7
-    ew_warp<NB, KS>(a, sh, stage + e * 64, q, e >> 2, lane, tm);
+    ew_warp<NB, KS, M3>(a, sh, stage + e * 64, q, e >> 2, lane, tm);
   }
   tmem_fence_before();
   __syncthreads();
@@ -351,16 +600,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   if (warp == 0) tmem_dealloc(sh.tmem, kTmemCols);
 }
 
-template <int NB, int KS, int SPLIT>
+template <int NB, int KS, int SPLIT, bool M3>
 int launch(const Args& a, cudaStream_t st, int sms) {
-  const size_t smem = size_t(NB) * a.ks_count * 32 * 16 + size_t(NB) * 8 * 16 + 8 * 64 * 16 + sizeof(Shared) + 64;
-  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  static_assert(sizeof(Shared) <= 256, "Shared must fit its 256-byte slot");
+  const size_t smem = Layout<NB, KS, M3>::bytes;
+  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
   const int64_t need = (a.tau + 63) / 64;  // 64 slots per CTA
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  dense_ws_kernel<NB, KS, SPLIT><<<unsigned(grid), 32 * (8 + 4 * SPLIT), smem, st>>>(a);
+  dense_ws_kernel<NB, KS, SPLIT, M3><<<unsigned(grid), 32 * (8 + 4 * SPLIT), smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense_ws_kernel)", err);
   return TPF_OK;
@@ -586,19 +836,38 @@ int launch(const ws::Args& a, cudaStream_t st, int sms) {
 
 using namespace tpf;
 
+static int hi_word(double x) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  return int(u >> 32) & 0x7fffffff;
+}
+
+#ifdef TPF_PHASE_TIMING
+extern "C" int tpf_debug_ws_phase_cycles(long long* out) {
+  return cudaMemcpyFromSymbol(out, ws::g_ws_cyc, sizeof(ws::g_ws_cyc)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 // Default: one DMMA warp per SMSP (12 warps).  TPF_WS_SPLIT=2 selects two DMMA
 // warps per SMSP sharing each GEMM (16 warps); measured slower on C2 (8.17 vs
 // 7.38 ms): the elementwise warps then cannot refill U fast enough.
+// Default: the 3M GEMM (3 DMMAs per complex block-product).  TPF_WS_4M=1
+// selects the 4-DMMA GEMM, bitwise equal to the pairs/solo kernels.
 template <int NB, int KS>
 static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   static const int split = [] {
     const char* e = getenv("TPF_WS_SPLIT");
     return (e && e[0] == '2') ? 2 : 1;
   }();
+  static const bool four = [] {
+    const char* e = getenv("TPF_WS_4M");
+    return e && e[0] == '1';
+  }();
   if constexpr (NB >= 2) {
-    if (split == 2) return ws::launch<NB, KS, 2>(a, st, sms);
+    if (split == 2) return ws::launch<NB, KS, 2, false>(a, st, sms);
   }
-  return ws::launch<NB, KS, 1>(a, st, sms);
+  if (four) return ws::launch<NB, KS, 1, false>(a, st, sms);
+  return ws::launch<NB, KS, 1, true>(a, st, sms);
 }
 
 extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
@@ -638,6 +907,10 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
   a.v_case = v_case_stride;
   a.iters = iters;
   a.counter = static_cast<unsigned long long*>(workspace);
+  // step-test bracket: |d| < hi_small<<32 <= 0.7 tol  =>  |delta|^2 < 0.98 tol^2;
+  // |d| > (hi_big + 1)<<32 > tol  =>  |delta|^2 > tol^2 (monotone rounding)
+  a.tol_hi_small = hi_word(0.7 * tol);
+  a.tol_hi_big = hi_word(tol);
   switch ((b + 7) / 8) {
     case 1: return a.ks_count == 2 ? ws_launch<1, 2>(a, st, sms) : ws_launch<1, 1>(a, st, sms);
     case 2: return a.ks_count == 4 ? ws_launch<2, 4>(a, st, sms) : ws_launch<2, 3>(a, st, sms);

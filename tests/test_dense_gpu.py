@@ -191,8 +191,8 @@ def test_large_b_permutation_invariance_bitwise(golden):
 @pytest.mark.parametrize("kernel", ["pairs", "solo"])
 @pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
                                   "nine_zero_batch"])
-def test_ws_and_pair_kernels_bitwise_equal(golden, name, kernel):
-    """Warp-specialised, pair and solo kernels: same DMMA order per element -> same bits."""
+def test_ws_and_pair_kernels_agree(golden, name, kernel):
+    """Warp-specialised (3M GEMM) vs the 4M pair/solo kernels: same counts, values to GEMM rounding."""
     import torch
     from paper_2403_04578_b200 import DenseOperator
     g = golden(name)
@@ -202,7 +202,10 @@ def test_ws_and_pair_kernels_bitwise_equal(golden, name, kernel):
     V1, it1 = op.solve(S, o, kernel="ws")
     V2, it2 = op.solve(S, o, kernel=kernel)
     assert torch.equal(it1, it2)
-    assert torch.equal(V1, V2)
+    fin = torch.isfinite(V2).all(dim=0)
+    assert torch.equal(fin, torch.isfinite(V1).all(dim=0))
+    if fin.any():
+        assert (V1[:, fin] - V2[:, fin]).abs().max().item() <= 1e-13
 
 
 def test_ws_kernel_full_c2_counts():
@@ -213,9 +216,10 @@ def test_ws_kernel_full_c2_counts():
     S = torch.from_numpy(gen_scenarios(model, 525600, spec).values).cuda()
     op = DenseOperator(model)
     V1, it1 = op.solve(S, kernel="ws")
-    assert int(it1.sum()) == 2615281
+    assert int(it1.sum()) == 2615281  # the reference's per-case total
     V2, it2 = op.solve(S, kernel="pairs")
-    assert torch.equal(V1, V2)
+    assert torch.equal(it1, it2)
+    assert (V1 - V2).abs().max().item() <= 1e-13
 
 
 @pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 64, 96, 100, 101, 104, 105, 128])
@@ -271,26 +275,30 @@ def test_max_iterations_cap_and_tolerance_options(golden):
     assert loose.iterations < 7
 
 
-def test_ws_two_dmma_warps_variant_bitwise_equal(golden):
-    """TPF_WS_SPLIT=2 (two DMMA warps per SMSP) gives the same bits (run in a subprocess:
-    the variant is chosen once per process)."""
+def _ws_variant_run(env_extra: dict, kernel: str = "ws"):
+    """Solve c2_slice192 in a subprocess (the ws variant is chosen once per process)."""
+    import os
     import subprocess
     import sys
+    import tempfile
     code = ("import numpy as np, torch, sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
             "from conftest import Golden;"
             "from paper_2403_04578_b200 import DenseOperator;"
             "g = Golden('c2_slice192'); op = DenseOperator(g.model);"
-            "V, it = op.solve(torch.from_numpy(g.S).cuda(), g.opts(), kernel='ws');"
+            f"V, it = op.solve(torch.from_numpy(g.S).cuda(), g.opts(), kernel='{kernel}');"
             "np.save(sys.argv[1], V.cpu().numpy())")
-    import os
-    import tempfile
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with tempfile.TemporaryDirectory() as d:
-        outs = []
-        for split in ("1", "2"):
-            f = os.path.join(d, f"v{split}.npy")
-            env = dict(os.environ, TPF_WS_SPLIT=split)
-            r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True)
-            assert r.returncode == 0, r.stderr[-2000:]
-            outs.append(np.load(f))
-        assert np.array_equal(outs[0], outs[1])
+        f = os.path.join(d, "v.npy")
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=dict(os.environ, **env_extra),
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return np.load(f)
+
+
+def test_ws_4m_and_split_variants_bitwise_equal_pairs():
+    """TPF_WS_4M=1 (one DMMA warp, 4M GEMM) and TPF_WS_SPLIT=2 (two DMMA warps per
+    SMSP) issue the pair kernel's DMMAs in the same order per element: same bits."""
+    pairs = _ws_variant_run({}, kernel="pairs")
+    assert np.array_equal(_ws_variant_run({"TPF_WS_4M": "1"}), pairs)
+    assert np.array_equal(_ws_variant_run({"TPF_WS_SPLIT": "2"}), pairs)
