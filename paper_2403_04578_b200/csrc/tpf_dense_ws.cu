@@ -122,6 +122,7 @@ __device__ __forceinline__ bool maybe_tiny(double x, double y) {
 struct Shared {
   uint64_t full_u[4][2];  // EW -> MMA: U of group g ready (or group finished)
   uint64_t full_v[4][2];  // MMA -> EW: V' of group g ready
+  uint64_t ew_u[4][2];    // EW -> MMA (3M, NE > 0): the EW warp's share of the GEMM has read U
   int done[4][2];
   uint32_t tmem;
 };
@@ -248,12 +249,12 @@ struct Layout {
   static constexpr size_t bytes = ks_off + size_t(NKS) * plane;
 };
 
-// One pass over all k-steps for node blocks [B0, B0 + NBP); V' written to
-// TMEM at dst + 8 lb (C-fragment order, same layout as the 4M path).  The
+// One pass over all k-steps for node blocks [B0, B0 + NBP); returns V' of
+// those blocks in C-fragment order (v[lb] = re0, re1, im0, im1).  The
 // accumulators start at P1 = Re W, P2 = 0, P3 = Re W + Im W, so
 // V' = (P1 - P2) + i ((P3 - P1) - P2).
 template <int KS, int B0, int NBP, int NKS>
-__device__ __forceinline__ void pass3(uint32_t uv, uint32_t dst, const double2* kb, const double* ksb,
+__device__ __forceinline__ void pass3(uint32_t uv, double (&v)[NBP][4], const double2* kb, const double* ksb,
                                       const double* w_re, const double* w_sum, int qq) {
   double p1[NBP][2], p2[NBP][2], p3[NBP][2];
 #pragma unroll
@@ -292,21 +293,33 @@ __device__ __forceinline__ void pass3(uint32_t uv, uint32_t dst, const double2* 
   }
 #pragma unroll
   for (int lb = 0; lb < NBP; ++lb) {
-    const double r0 = p1[lb][0] - p2[lb][0], r1 = p1[lb][1] - p2[lb][1];
-    const double i0 = (p3[lb][0] - p1[lb][0]) - p2[lb][0];
-    const double i1 = (p3[lb][1] - p1[lb][1]) - p2[lb][1];
-    tmem_st4d(dst + 8 * lb, r0, r1, i0, i1);
+    v[lb][0] = p1[lb][0] - p2[lb][0];
+    v[lb][1] = p1[lb][1] - p2[lb][1];
+    v[lb][2] = (p3[lb][0] - p1[lb][0]) - p2[lb][0];
+    v[lb][3] = (p3[lb][1] - p1[lb][1]) - p2[lb][1];
   }
 }
 
-// 3M DMMA warp (one per SMSP, both groups).  NB <= kM3Pass0: one pass straight
-// into the hand-off buffer; otherwise blocks [0, 6) first (into the group's
-// scratch columns: U is still needed), then blocks [6, NB) (into the hand-off
-// buffer, after the last read of U).
-template <int NB, int KS, int NKS>
+template <int NBP>
+__device__ __forceinline__ void store3(uint32_t dst, const double (&v)[NBP][4]) {
+#pragma unroll
+  for (int lb = 0; lb < NBP; ++lb) tmem_st4d(dst + 8 * lb, v[lb][0], v[lb][1], v[lb][2], v[lb][3]);
+}
+
+// The 3M GEMM of a group is shared: the MMA warp does node blocks [0, NM),
+// the group's EW warp the last NE = NB - NM blocks (it is otherwise idle while
+// the MMA warp works), so two DMMA streams feed the SMSP's tensor pipe.
+// V' of blocks [0, kM3Pass0) goes to the group's scratch columns; every other
+// block's V' overwrites U in the hand-off buffer, so it is stored only once
+// both warps are done reading U (mbarriers ew_u and full_v).
+// 3M DMMA warp (one per SMSP, both groups), node blocks [0, NM).
+template <int NB, int KS, int NKS, int NM>
 __device__ __forceinline__ void mma_warp3(const Args& a, Shared& sh, const double2* k_sm, const double* ks_sm,
                                           const double* w_re, const double* w_sum, int q, int lane, uint32_t tm) {
-  uint32_t par[2] = {0u, 0u};
+  constexpr int NE = NB - NM;
+  constexpr int P0 = NM < kM3Pass0 ? NM : kM3Pass0;  // blocks of the first pass (to scratch)
+  static_assert(NE == 0 || NM >= kM3Pass0 || NB <= kM3Pass0, "EW blocks must lie past the scratch blocks");
+  uint32_t par[2] = {0u, 0u}, epar[2] = {0u, 0u};
   bool alive[2] = {true, true};
   const int qq = lane & 3;
   const double2* kb = k_sm + lane;
@@ -326,11 +339,26 @@ __device__ __forceinline__ void mma_warp3(const Args& a, Shared& sh, const doubl
     }
     pc.round();
     const uint32_t uv = tm + g * kGroupCols;
-    if constexpr (NB <= kM3Pass0) {
-      pass3<KS, 0, NB, NKS>(uv, uv, kb, ksb, w_re, w_sum, qq);
+    if constexpr (NB <= kM3Pass0) {  // everything fits the scratch-free single pass
+      double v[NB][4];
+      pass3<KS, 0, NB, NKS>(uv, v, kb, ksb, w_re, w_sum, qq);
+      store3<NB>(uv, v);
     } else {
-      pass3<KS, 0, kM3Pass0, NKS>(uv, tm + kScratchCol + g * 8 * kM3Pass0, kb, ksb, w_re, w_sum, qq);
-      pass3<KS, kM3Pass0, NB - kM3Pass0, NKS>(uv, uv + 8 * kM3Pass0, kb, ksb, w_re, w_sum, qq);
+      {
+        double v[P0][4];
+        pass3<KS, 0, P0, NKS>(uv, v, kb, ksb, w_re, w_sum, qq);
+        store3<P0>(tm + kScratchCol + g * 8 * kM3Pass0, v);
+      }
+      if constexpr (NM > P0) {
+        double v[NM - P0][4];
+        pass3<KS, P0, NM - P0, NKS>(uv, v, kb, ksb, w_re, w_sum, qq);
+        if constexpr (NE > 0) {  // the EW warp may still be reading U
+          mbar_wait(&sh.ew_u[q][g], epar[g]);
+          epar[g] ^= 1u;
+          tmem_fence_after();
+        }
+        store3<NM - P0>(uv + 8 * P0, v);
+      }
     }
     tmem_wait_st();
     tmem_fence_before();
@@ -340,9 +368,11 @@ __device__ __forceinline__ void mma_warp3(const Args& a, Shared& sh, const doubl
   pc.flush();
 }
 
-template <int NB, int KS, bool M3>
+template <int NB, int KS, bool M3, int NKS, int NM>
 __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stage, int q, int g, int lane,
-                                        uint32_t tm) {
+                                        uint32_t tm, const double2* k_sm, const double* ks_sm, const double* w_re,
+                                        const double* w_sum) {
+  constexpr int NE = NB - NM;
   const int slot = lane >> 2, qq = lane & 3;
   const int b = a.b;
   const int64_t tau = a.tau;
@@ -449,11 +479,25 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
     fresh = false;
     pc.mark(2);
 
-    // ---- wait for V' of this group, per-case step test (dense.py:125-126, 189-193) ----
-    mbar_wait(&sh.full_v[q][g], par);
-    par ^= 1u;
-    tmem_fence_after();
+    if constexpr (M3 && NE > 0) {
+      // this warp's share of the group's GEMM: node blocks [NM, NB)
+      double v[NE > 0 ? NE : 1][4];
+      pass3<KS, NM, NE, NKS>(uv, v, k_sm + lane, ks_sm + lane, w_re, w_sum, qq);
+      tmem_fence_before();
+      mbar_arrive(&sh.ew_u[q][g]);  // done reading U
+      mbar_wait(&sh.full_v[q][g], par);
+      par ^= 1u;
+      tmem_fence_after();
+      store3<NE>(uv + 8 * NM, v);
+      tmem_wait_st();
+    } else {
+      // ---- wait for V' of this group ----
+      mbar_wait(&sh.full_v[q][g], par);
+      par ^= 1u;
+      tmem_fence_after();
+    }
     pc.mark(3);
+    // ---- per-case step test (dense.py:125-126, 189-193) ----
     bool small = true;
 #pragma unroll
     for (int lb = 0; lb < NB; ++lb) {
@@ -539,7 +583,7 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
 // SPLIT DMMA warps per SMSP share each GEMM (node blocks split NBA / NB - NBA):
 // SPLIT = 1: 12 warps (4 DMMA + 8 EW); SPLIT = 2: 16 warps (8 DMMA + 8 EW), so
 // two DMMA streams feed every FP64 tensor pipe.
-template <int NB, int KS, int SPLIT, bool M3>
+template <int NB, int KS, int SPLIT, bool M3, int NM>
 __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const Args a) {
   constexpr int NBA = SPLIT == 1 ? NB : (NB + 1) / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -573,6 +617,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
       for (int g = 0; g < 2; ++g) {
         mbar_init(&sh.full_u[q][g], 32);
         mbar_init(&sh.full_v[q][g], 32 * SPLIT);
+        mbar_init(&sh.ew_u[q][g], 32);
         sh.done[q][g] = 0;
       }
   }
@@ -585,14 +630,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   const int wg = warp >> 2;
   if (wg == 0) {
     if constexpr (M3)
-      mma_warp3<NB, KS, L::NKS>(a, sh, k_sm, ks_sm, w_re, w_sum, q, lane, tm);
+      mma_warp3<NB, KS, L::NKS, NM>(a, sh, k_sm, ks_sm, w_re, w_sum, q, lane, tm);
     else
       mma_warp<KS, 0, NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
   } else if (SPLIT == 2 && wg == 1) {
     if constexpr (SPLIT == 2) mma_warp<KS, NBA, NB - NBA, SPLIT>(a, sh, k_sm, w_re, w_im, q, lane, tm);
   } else {
     const int e = warp - 4 * SPLIT;  // 0..7
-    ew_warp<NB, KS, M3>(a, sh, stage + e * 64, q, e >> 2, lane, tm);
+    ew_warp<NB, KS, M3, L::NKS, NM>(a, sh, stage + e * 64, q, e >> 2, lane, tm, k_sm, ks_sm, w_re, w_sum);
   }
   tmem_fence_before();
   __syncthreads();
@@ -600,17 +645,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   if (warp == 0) tmem_dealloc(sh.tmem, kTmemCols);
 }
 
-template <int NB, int KS, int SPLIT, bool M3>
+template <int NB, int KS, int SPLIT, bool M3, int NM = NB>
 int launch(const Args& a, cudaStream_t st, int sms) {
   static_assert(sizeof(Shared) <= 256, "Shared must fit its 256-byte slot");
   const size_t smem = Layout<NB, KS, M3>::bytes;
-  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT, M3, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
   const int64_t need = (a.tau + 63) / 64;  // 64 slots per CTA
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  dense_ws_kernel<NB, KS, SPLIT, M3><<<unsigned(grid), 32 * (8 + 4 * SPLIT), smem, st>>>(a);
+  dense_ws_kernel<NB, KS, SPLIT, M3, NM><<<unsigned(grid), 32 * (8 + 4 * SPLIT), smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense_ws_kernel)", err);
   return TPF_OK;
@@ -866,7 +911,23 @@ static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   if constexpr (NB >= 2) {
     if (split == 2) return ws::launch<NB, KS, 2, false>(a, st, sms);
   }
+  // node blocks of the GEMM done by the elementwise warps (TPF_WS_NE; default 5 at b in (96, 104], else b/8 - 4)
+  static const int ne = [] {
+    const char* e = getenv("TPF_WS_NE");
+    return e ? atoi(e) : 5;
+  }();
   if (four) return ws::launch<NB, KS, 1, false>(a, st, sms);
+  if constexpr (NB == 13) {
+    if (ne == 2) return ws::launch<NB, KS, 1, true, NB - 2>(a, st, sms);
+    if (ne == 3) return ws::launch<NB, KS, 1, true, NB - 3>(a, st, sms);
+    if (ne == 5) return ws::launch<NB, KS, 1, true, NB - 5>(a, st, sms);
+
+  }
+  if constexpr (NB > ws::kM3Pass0) {
+    // the EW blocks must lie past the scratch blocks: NM >= kM3Pass0
+    constexpr int nm = NB - 4 >= ws::kM3Pass0 ? NB - 4 : ws::kM3Pass0;
+    if (ne != 0) return ws::launch<NB, KS, 1, true, nm>(a, st, sms);
+  }
   return ws::launch<NB, KS, 1, true>(a, st, sms);
 }
 
