@@ -326,7 +326,8 @@ def run_ours():
                         kernel="dense_ws_kernel", kernel_ms=kms,
                         peak_source="measured in-run: DMMA-only probe (tpf_probe_fp64_tflops); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                        algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch")
+                        algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch",
+                        executed=executed_dense(b, sum_n, kms, peak_tf))
     else:
         alg = 48.0 * b * sum_n  # BYTES_alg = 48 b sum_j n_j
         achieved = alg / (kms * 1e-3) / 1e9
@@ -360,11 +361,25 @@ def run_ours():
                                 parallelism=f"tau-sharded x{world} (independent scenario batches)",
                                 **({"c4_full_1000_scenarios_s_extrapolated": 1000 * tau / value} if scenarios else {})),
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
-                    gpu_launches=3 * ARGS.steps,
+                    gpu_launches=(3 if method == "dense" else 2) * ARGS.steps,
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def executed_dense(b, sum_n, kms, peak_tf):
+    """FP64 tensor work the default kernel actually issues (b <= 104: 3M GEMM,
+    3 real DMMAs per complex 8x8x4 block-product on the padded 8*ceil(b/8) x
+    4*ceil(b/4) operator; b > 104: the 4M tiled kernel on 64-padded tiles)."""
+    if b <= 104:
+        flop = 6.0 * (8 * -(-b // 8)) * (4 * -(-b // 4)) * sum_n
+        how = "3M: 6 * 8ceil(b/8) * 4ceil(b/4) * sum(n_j)"
+    else:
+        flop = 8.0 * b * b * sum_n
+        how = "4M: 8 b^2 sum(n_j) (padding not counted)"
+    tf = flop / (kms * 1e-3) / 1e12
+    return dict(flop=flop, tflops=tf, frac=tf / peak_tf if peak_tf else None, formula=how)
 
 
 def ctypes_probe(lib):
