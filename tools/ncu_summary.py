@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (run here, on the CPU box).
 
-    python tools/ncu_summary.py gpurun_out/prof_dense_v1.ncu-rep dense_fpi_kernel profiles/r1_dense_ncu.md
+    python tools/ncu_summary.py gpurun_out/prof_dense_v1.ncu-rep dense_fpi_kernel profiles/r1_dense_ncu.md [tau]
     python tools/ncu_summary.py --launches gpurun_out/launches.csv profiles/r1_launches.md
 
 Also merges per-kernel DRAM bytes per launch into profiles/ncu_summary.json,
@@ -47,7 +47,7 @@ def raw(rep):
     return res
 
 
-def summarise(rep, kernel, md_path):
+def summarise(rep, kernel, md_path, tau=None):
     rows = [r for r in raw(rep) if kernel in r.get("Kernel Name", ("", ""))[0]]
     if not rows:
         raise SystemExit(f"kernel {kernel} not in {rep}")
@@ -84,6 +84,8 @@ def summarise(rep, kernel, md_path):
     js[kernel] = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                   "duration": vals["gpu__time_duration.sum"][0] + " " + vals["gpu__time_duration.sum"][1],
                   "source": os.path.basename(rep)}
+    if tau:
+        js[kernel]["tau"] = int(tau)
     json.dump(js, open(js_path, "w"), indent=1, sort_keys=True)
     print(open(md_path).read())
 
@@ -114,4 +116,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        summarise(sys.argv[1], sys.argv[2], sys.argv[3])
+        summarise(sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
