@@ -215,6 +215,11 @@ int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
  * workspace: device scratch of >= tpf_*_solve_host_workspace_bytes(...)
  * bytes, or NULL to let the call cudaMalloc/cudaFree its own.
  * Synchronous: returns when every output is on the host.                  */
+/* Page-lock a host range for the duration of several concurrent host-pipeline
+ * calls (multi-device use): returns 1 if this call registered it (release with
+ * tpf_host_unpin), 0 if it was already page-locked or cannot be.          */
+int tpf_host_pin(void* ptr, size_t bytes);
+int tpf_host_unpin(void* ptr);
 size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz);
 int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t levels,
                                     const int32_t* level_info, const int32_t* node_info, const double* node_coef,

@@ -80,6 +80,8 @@ SIGNATURES = {
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
+    "tpf_host_pin": (ctypes.c_int, [_c_ptr, _c_sz]),
+    "tpf_host_unpin": (ctypes.c_int, [_c_ptr]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),
 }
 

@@ -147,3 +147,88 @@ def device_workspace(device: torch.device, nbytes: int) -> torch.Tensor:
         ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
         _WS[device] = ws
     return ws
+
+
+def resolve_devices(device=None, devices=None) -> list[torch.device]:
+    """The CUDA devices of one call: ``devices`` (a list) wins over ``device``."""
+    if devices is None:
+        return [require_cuda(device)]
+    devs = [require_cuda(d) for d in devices]
+    if not devs:
+        raise ValueError("devices must name at least one CUDA device")
+    return devs
+
+
+def case_slices(tau: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous, near-equal case ranges [lo, hi) (SURVEY 8(e) partitioning)."""
+    base, extra = divmod(tau, parts)
+    out, lo = [], 0
+    for k in range(parts):
+        hi = lo + base + (1 if k < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class _PinScope:
+    """Page-lock host arrays for the duration of a multi-device call, so the
+    per-device pipelines (which would otherwise each register the same span)
+    all see page-locked memory and never unregister under each other."""
+
+    def __init__(self, *arrays):
+        self.arrays = [a for a in arrays if a is not None and a.nbytes > 0]
+        self.done = []
+
+    def __enter__(self):
+        lib = _capi.load()
+        for a in self.arrays:
+            if lib.tpf_host_pin(a.ctypes.data, a.nbytes) == 1:  # 0: already page-locked or not pinnable
+                self.done.append(a.ctypes.data)
+        return self
+
+    def __exit__(self, *exc):
+        lib = _capi.load()
+        for p in self.done:
+            lib.tpf_host_unpin(p)
+        return False
+
+
+def run_sliced(devices: list[torch.device], tau: int, call, arrays) -> list:
+    """Run ``call(device, lo, hi, slot)`` for contiguous case slices, one per
+    device entry, concurrently (the C pipelines release the GIL).  ``arrays``
+    are the host buffers the calls read/write (page-locked for the call)."""
+    import threading
+    slices = case_slices(tau, len(devices))
+    results: list = [None] * len(devices)
+    errors: list = []
+
+    def work(k):
+        lo, hi = slices[k]
+        try:
+            with torch.cuda.device(devices[k]):
+                results[k] = call(devices[k], lo, hi, k)
+        except BaseException as exc:  # re-raised in the caller's thread
+            errors.append(exc)
+
+    with _PinScope(*arrays):
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(1, len(devices))]
+        for t in threads:
+            t.start()
+        work(0)
+        for t in threads:
+            t.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
+def device_workspace_slot(device: torch.device, nbytes: int, slot: int) -> torch.Tensor:
+    """Like ``device_workspace`` but one buffer per (device, slot): concurrent
+    calls on the same device never share scratch."""
+    key = (device, slot)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _WS.pop(key, None)
+        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws

@@ -370,6 +370,29 @@ struct TreeChunk : ChunkSolver {
 
 using namespace tpf;
 
+extern "C" int tpf_host_pin(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return 0;
+  cudaPointerAttributes attr;
+  cudaError_t err = cudaPointerGetAttributes(&attr, ptr);
+  if (err == cudaSuccess && (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged)) return 0;
+  cudaGetLastError();
+  err = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return 1;
+}
+
+extern "C" int tpf_host_unpin(void* ptr) {
+  cudaError_t err = cudaHostUnregister(ptr);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return set_cuda_error("cudaHostUnregister", err);
+  }
+  return TPF_OK;
+}
+
 extern "C" size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases,
                                                              int64_t ydd_nnz) {
   const int64_t chunk = pick_chunk(tau, b, chunk_cases);

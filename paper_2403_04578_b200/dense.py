@@ -25,8 +25,9 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
-                      device_workspace, loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
+from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads, device_workspace_slot,
+                      loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
+                      stream_ptr)
 from ._types import LoadMatrix, SolveOptions, VoltageBatch
 
 __all__ = ["batch_solve_dense", "DenseOperator"]
@@ -118,12 +119,14 @@ class DenseOperator:
 
 
 def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
-                      workers: int = 1, *, device=None, return_on_device: bool = False,
+                      workers: int = 1, *, device=None, devices=None, return_on_device: bool = False,
                       chunk_cases: int = 0) -> VoltageBatch:
     """GPU ``batch_solve_dense`` (dense.py:129-205); see module docstring.
 
     Host (numpy) loads go through the native chunked H2D/solve/D2H pipeline
-    (``tpf_dense_solve_host_c128``) and come back as numpy arrays.  With
+    (``tpf_dense_solve_host_c128``) and come back as numpy arrays; with
+    ``devices=[...]`` the cases are split into contiguous slices, one pipeline
+    per device, run concurrently (bitwise the same result).  With
     ``return_on_device=True`` the loads are copied once and the result stays
     on the device as torch tensors.
     """
@@ -137,8 +140,10 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
             "mixed ZIP loads are not on the batched hot path; the reference routes them "
             "through its single-case solver (tpflow.dense._batch_via_single -> fpi_solve)")
     if not return_on_device:
-        return _solve_host_pipeline(model, loads, opts, device, chunk_cases)
-    op = DenseOperator(model, device)
+        return _solve_host_pipeline(model, loads, opts, resolve_devices(device, devices), chunk_cases)
+    if devices is not None and len(devices) > 1:
+        raise ValueError("return_on_device=True needs a single device")
+    op = DenseOperator(model, devices[0] if devices else device)
     S = loads_to_device(loads.values, op.device)
     V, iters = op.solve(S, opts)
     resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
@@ -155,8 +160,7 @@ def finish(V, iters, resid, mask, summ, on_device: bool) -> VoltageBatch:
                         residuals=resid.cpu().numpy(), iterations_per_case=iters.cpu().numpy())
 
 
-def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int):
-    dev = require_cuda(device)
+def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chunk_cases: int):
     c = ModelContract.of(model)
     K, W = dense_kw(c)
     rp, ci, yv = host_csr(c)
@@ -166,14 +170,24 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, c
     iters = host_empty((tau,), np.int32)
     resid = host_empty((tau,), np.float64)
     mask = host_empty((tau,), np.uint8)
-    summ = np.zeros(2, dtype=np.int32)
     v_flat = complex(abs(c.v_s))
     lib = _capi.load()
-    ws = device_workspace(dev, lib.tpf_dense_solve_host_workspace_bytes(tau, b, int(chunk_cases), yv.size))
-    torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
-    _capi.call("tpf_dense_solve_host_c128", tau, b, ptr(S), sn, sc, ptr(K), ptr(W), ptr(rp), ptr(ci),
-               ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
-               int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
-               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
-    return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
+
+    def call(dev, lo, hi, slot):
+        n = hi - lo
+        summ = np.zeros(2, dtype=np.int32)
+        if n == 0:
+            return summ
+        ws = device_workspace_slot(dev, lib.tpf_dense_solve_host_workspace_bytes(n, b, int(chunk_cases), yv.size),
+                                   slot)
+        torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
+        _capi.call("tpf_dense_solve_host_c128", n, b, ptr(S) + 16 * lo * sc, sn, sc, ptr(K), ptr(W), ptr(rp),
+                   ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
+                   int(opts.max_iterations), float(opts.residual_tolerance), ptr(V) + 16 * lo, tau, 1,
+                   ptr(iters) + 4 * lo, ptr(resid) + 8 * lo, ptr(mask) + lo, ptr(summ), int(chunk_cases),
+                   dev.index, ws.data_ptr(), ws.numel())
+        return summ
+
+    parts = run_sliced(devs, tau, call, (S,)) if len(devs) > 1 else [call(devs[0], 0, tau, 0)]
+    return VoltageBatch(values=V, iterations=max(int(p[0]) for p in parts), converged_mask=mask.astype(bool),
                         residuals=resid, iterations_per_case=iters)

@@ -32,8 +32,9 @@ from scipy import sparse
 from scipy.sparse.linalg import splu
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads,
-                      device_workspace, loads_to_device, ptr, require_cuda, residual_and_summary, stream_ptr)
+from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads, device_workspace_slot,
+                      loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
+                      stream_ptr)
 from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
 from .dense import finish
 
@@ -428,10 +429,15 @@ class SparseOperator:
 
 
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
-                       max_nnz: int | None = None, *, device=None,
+                       max_nnz: int | None = None, *, device=None, devices=None,
                        return_on_device: bool = False, chunk_cases: int = 0,
                        use_tree: bool = True) -> VoltageBatch:
-    """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring."""
+    """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring.
+
+    ``devices=[...]``: contiguous case slices solved concurrently, one host
+    pipeline per device, after the one host factorization (bitwise the same
+    result as one device).
+    """
     if not isinstance(loads, LoadMatrix):
         loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
     if not model.zip.is_constant_power:
@@ -445,8 +451,10 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
                 f"block system would hold {total} nonzeros (> {max_nnz}); "
                 "chunk the batch over cases and solve the chunks separately")
     if not return_on_device:
-        return _solve_host_pipeline(model, loads, opts, device, chunk_cases, use_tree)
-    op = SparseOperator(model, device, use_tree=use_tree)
+        return _solve_host_pipeline(model, loads, opts, resolve_devices(device, devices), chunk_cases, use_tree)
+    if devices is not None and len(devices) > 1:
+        raise ValueError("return_on_device=True needs a single device")
+    op = SparseOperator(model, devices[0] if devices else device, use_tree=use_tree)
     S = loads_to_device(loads.values, op.device)
     resid = torch.empty(S.shape[1], dtype=torch.float64, device=op.device)
     V, iters = op.solve(S, opts, resid=resid)
@@ -462,11 +470,10 @@ def _nonempty(a):
     return a if a.size else np.zeros(1, dtype=a.dtype)
 
 
-def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, chunk_cases: int,
+def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chunk_cases: int,
                          use_tree: bool = True):
-    dev = require_cuda(device)
     c = ModelContract.of(model)
-    f = factorize_ydd(c.y_dd)
+    f = factorize_ydd(c.y_dd)  # one factorization per batch, shared by every device
     tree = tree_schedule(f, c.src) if use_tree else None
     rp, ci, yv = host_csr(c)
     S, sn, sc = host_loads(loads.values)
@@ -475,27 +482,36 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, device, c
     iters = host_empty((tau,), np.int32)
     resid = host_empty((tau,), np.float64)
     mask = host_empty((tau,), np.uint8)
-    summ = np.zeros(2, dtype=np.int32)
     v_flat = complex(abs(c.v_s))
     arrs = [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val, f.u_diag_inv,
                                     f.perm)]
     lib = _capi.load()
-    if tree is not None:
-        ws = device_workspace(dev, lib.tpf_sparse_tree_solve_host_workspace_bytes(tau, b, int(chunk_cases), yv.size))
-        torch.cuda.current_stream(dev).synchronize()
-        _capi.call("tpf_sparse_tree_solve_host_c128", tau, b, tree.levels, ptr(tree.level_info),
-                   ptr(tree.node_info), ptr(tree.node_coef), ptr(S), sn, sc, ptr(rp), ptr(ci), ptr(yv),
-                   ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
-                   float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters), ptr(resid), ptr(mask),
-                   ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
-        return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
-                            residuals=resid, iterations_per_case=iters)
-    ws = device_workspace(dev, lib.tpf_sparse_solve_host_workspace_bytes(
-        tau, b, int(chunk_cases), yv.size, f.l_col.size, f.u_col.size))
-    torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
-    _capi.call("tpf_sparse_solve_host_c128", tau, b, ptr(S), sn, sc, *[ptr(x) for x in arrs],
-               ptr(rp), ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
-               int(opts.max_iterations), float(opts.residual_tolerance), ptr(V), tau, 1, ptr(iters),
-               ptr(resid), ptr(mask), ptr(summ), int(chunk_cases), dev.index, ws.data_ptr(), ws.numel())
-    return VoltageBatch(values=V, iterations=int(summ[0]), converged_mask=mask.astype(bool),
+
+    def call(dev, lo, hi, slot):
+        n = hi - lo
+        summ = np.zeros(2, dtype=np.int32)
+        if n == 0:
+            return summ
+        outs = (ptr(V) + 16 * lo, tau, 1, ptr(iters) + 4 * lo, ptr(resid) + 8 * lo, ptr(mask) + lo, ptr(summ),
+                int(chunk_cases), dev.index)
+        s_lo = ptr(S) + 16 * lo * sc
+        if tree is not None:
+            ws = device_workspace_slot(
+                dev, lib.tpf_sparse_tree_solve_host_workspace_bytes(n, b, int(chunk_cases), yv.size), slot)
+            torch.cuda.current_stream(dev).synchronize()
+            _capi.call("tpf_sparse_tree_solve_host_c128", n, b, tree.levels, ptr(tree.level_info),
+                       ptr(tree.node_info), ptr(tree.node_coef), s_lo, sn, sc, ptr(rp), ptr(ci), ptr(yv),
+                       ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                       float(opts.residual_tolerance), *outs, ws.data_ptr(), ws.numel())
+            return summ
+        ws = device_workspace_slot(dev, lib.tpf_sparse_solve_host_workspace_bytes(
+            n, b, int(chunk_cases), yv.size, f.l_col.size, f.u_col.size), slot)
+        torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
+        _capi.call("tpf_sparse_solve_host_c128", n, b, s_lo, sn, sc, *[ptr(x) for x in arrs],
+                   ptr(rp), ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
+                   int(opts.max_iterations), float(opts.residual_tolerance), *outs, ws.data_ptr(), ws.numel())
+        return summ
+
+    parts = run_sliced(devs, tau, call, (S,)) if len(devs) > 1 else [call(devs[0], 0, tau, 0)]
+    return VoltageBatch(values=V, iterations=max(int(p[0]) for p in parts), converged_mask=mask.astype(bool),
                         residuals=resid, iterations_per_case=iters)

@@ -302,3 +302,21 @@ def test_ws_4m_and_split_variants_bitwise_equal_pairs():
     pairs = _ws_variant_run({}, kernel="pairs")
     assert np.array_equal(_ws_variant_run({"TPF_WS_4M": "1"}), pairs)
     assert np.array_equal(_ws_variant_run({"TPF_WS_SPLIT": "2"}), pairs)
+
+
+@pytest.mark.parametrize("devs", [["cuda:0", "cuda:0"], ["cuda:0", "cuda:0", "cuda:0"]])
+def test_devices_split_bitwise_equal(golden, devs):
+    """devices=[...]: contiguous case slices on concurrent per-device pipelines
+    (here the same B200 several times) give the single-device bits."""
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_dense
+    g = golden("c2_slice192")
+    one = batch_solve_dense(g.model, LoadMatrix(g.S), g.opts())
+    many = batch_solve_dense(g.model, LoadMatrix(g.S), g.opts(), devices=devs)
+    assert np.array_equal(one.values, many.values)
+    assert np.array_equal(one.iterations_per_case, many.iterations_per_case)
+    assert np.array_equal(one.residuals, many.residuals)
+    assert np.array_equal(one.converged_mask, many.converged_mask)
+    assert one.iterations == many.iterations
+    # a pageable F-order input takes the same route
+    many_f = batch_solve_dense(g.model, LoadMatrix(np.asfortranarray(g.S)), g.opts(), devices=devs)
+    assert np.array_equal(one.values, many_f.values)

@@ -196,3 +196,14 @@ class TestDenseOperatorCache:
                           src=np.zeros(2, dtype=complex), v_s=1 + 0j, constant_power=True)
         with pytest.raises(np.linalg.LinAlgError):
             dense_kw(c)
+
+
+class TestCaseSlices:
+    @pytest.mark.parametrize("tau,parts", [(0, 1), (1, 3), (7, 3), (525600, 8), (10, 10)])
+    def test_contiguous_cover(self, tau, parts):
+        from paper_2403_04578_b200._device import case_slices
+        sl = case_slices(tau, parts)
+        assert len(sl) == parts and sl[0][0] == 0 and sl[-1][1] == tau
+        assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+        sizes = [hi - lo for lo, hi in sl]
+        assert max(sizes) - min(sizes) <= 1

@@ -164,3 +164,16 @@ def test_fused_residual_nonfinite_case():
     assert np.isnan(a[4]) and np.isnan(b[4])
     keep = np.arange(40) != 4
     assert np.array_equal(a[keep], b[keep])
+
+
+@pytest.mark.parametrize("use_tree", [True, False], ids=["tree", "general"])
+def test_devices_split_bitwise_equal(golden, use_tree):
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_sparse
+    g = golden("c1_slice512")
+    one = batch_solve_sparse(g.model, LoadMatrix(g.S), g.opts(), use_tree=use_tree)
+    many = batch_solve_sparse(g.model, LoadMatrix(g.S), g.opts(), use_tree=use_tree,
+                              devices=["cuda:0", "cuda:0", "cuda:0"])
+    assert np.array_equal(one.values, many.values)
+    assert np.array_equal(one.iterations_per_case, many.iterations_per_case)
+    assert np.array_equal(one.residuals, many.residuals)
+    assert one.iterations == many.iterations
