@@ -183,6 +183,34 @@ int tpf_sparse_tree_build_ell(int32_t b, int32_t width, const int32_t* node_info
                               const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
                               int32_t* ell_col, double* ell_val);
 
+/* ------------------------------------------------------- complex64 twins --
+ * Same contracts as the c128 entry points above, in FP32 (complex64 arrays,
+ * float scalars).  FP32 cannot resolve tol = 1e-10: use tol >= ~1e-6.
+ *   tpf_dense_fpi_c64:  b <= tpf_dense_c64_max_nodes() (104); K, W complex64;
+ *                       workspace >= tpf_dense_c64_workspace_bytes(tau, b).
+ *   tpf_sparse_fpi_c64: L/U values, 1/U[k,k] and src complex64; workspace
+ *                       >= tpf_sparse_c64_workspace_bytes(tau, b).
+ *   tpf_residual_c64:   the post-check of a complex64 solution, in FP64
+ *                       (Y_dd, src complex128; resid float64).            */
+int tpf_dense_c64_max_nodes(void);
+size_t tpf_dense_c64_workspace_bytes(int64_t tau, int32_t b);
+int tpf_dense_fpi_c64(int64_t tau, int32_t b, const float* S, int64_t s_node_stride, int64_t s_case_stride,
+                      const float* K, const float* W, float v_flat_re, float v_flat_im, float tol,
+                      int32_t max_iter, float* V, int64_t v_node_stride, int64_t v_case_stride,
+                      int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
+size_t tpf_sparse_c64_workspace_bytes(int64_t tau, int32_t b);
+int tpf_sparse_fpi_c64(int64_t tau, int32_t b, const float* S, int64_t s_node_stride, int64_t s_case_stride,
+                       const int32_t* l_ptr, const int32_t* l_col, const float* l_val,
+                       const int32_t* u_ptr, const int32_t* u_col, const float* u_val,
+                       const float* u_diag_inv, const int32_t* perm, const float* src,
+                       float v_flat_re, float v_flat_im, float tol, int32_t max_iter,
+                       float* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int tpf_residual_c64(int64_t tau, int32_t b, const float* S, int64_t s_node_stride, int64_t s_case_stride,
+                     const float* V, int64_t v_node_stride, int64_t v_case_stride,
+                     const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                     const double* src, double* resid, void* stream);
+
 /* -------------------------------------------------------------- residual --
  * residual_per_case (fpi.py:221-240, constant-power branch) as used by
  * _safe_residuals (dense.py:208-211):

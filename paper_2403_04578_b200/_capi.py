@@ -21,6 +21,7 @@ TPF_ERR_MEMORY = 5
 
 _c_i32, _c_i64, _c_dbl, _c_ptr, _c_sz = (ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
                                          ctypes.c_void_p, ctypes.c_size_t)
+_c_flt = ctypes.c_float
 
 # name -> (restype, argtypes); must match include/tpf.h exactly
 SIGNATURES = {
@@ -80,6 +81,18 @@ SIGNATURES = {
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
+    "tpf_dense_c64_max_nodes": (ctypes.c_int, []),
+    "tpf_dense_c64_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "tpf_dense_fpi_c64": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_flt, _c_flt, _c_flt, _c_i32, _c_ptr, _c_i64,
+        _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_sparse_c64_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "tpf_sparse_fpi_c64": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr, _c_flt, _c_flt, _c_flt, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
+    "tpf_residual_c64": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr]),
     "tpf_host_pin": (ctypes.c_int, [_c_ptr, _c_sz]),
     "tpf_host_unpin": (ctypes.c_int, [_c_ptr]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),

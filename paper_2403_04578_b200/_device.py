@@ -71,13 +71,13 @@ def complex_strides(t: torch.Tensor) -> tuple[int, int]:
     return int(t.stride(0)), int(t.stride(1))
 
 
-def loads_to_device(values: np.ndarray, device: torch.device) -> torch.Tensor:
+def loads_to_device(values: np.ndarray, device: torch.device, dtype=np.complex128) -> torch.Tensor:
     """Copy a b x tau complex load matrix to the device keeping its C/F order."""
-    arr = np.asarray(values, dtype=np.complex128)
+    arr = np.asarray(values, dtype=dtype)
     if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
         arr = np.ascontiguousarray(arr)
     host = torch.from_numpy(arr)
-    out = torch.empty_strided(host.shape, host.stride(), dtype=torch.complex128, device=device)
+    out = torch.empty_strided(host.shape, host.stride(), dtype=host.dtype, device=device)
     out.copy_(host)
     return out
 
@@ -104,11 +104,20 @@ def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tens
     vn, vc = complex_strides(V)
     if not have_resid:
         rp, ci, val, src = csr if csr is not None else contract.csr_on(device)
-        _capi.call("tpf_residual_c128", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+        fn = "tpf_residual_c64" if V.dtype == torch.complex64 else "tpf_residual_c128"
+        _capi.call(fn, tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
                    rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
     _capi.call("tpf_batch_summary", tau, iters.data_ptr(), resid.data_ptr(), float(residual_tol),
                mask.data_ptr(), summ.data_ptr(), st)
     return resid, mask, summ
+
+
+def engine_dtype(dtype) -> np.dtype:
+    """complex128 (default, the reference's arithmetic) or complex64 (the c64 twins)."""
+    dt = np.dtype(np.complex128 if dtype is None else dtype)
+    if dt not in (np.dtype(np.complex128), np.dtype(np.complex64)):
+        raise ValueError(f"dtype must be complex128 or complex64, got {dt}")
+    return dt
 
 
 def host_empty(shape, dtype) -> np.ndarray:

@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads, device_workspace_slot,
+from ._device import (ModelContract, complex_strides, engine_dtype, host_csr, host_empty, host_loads,
+                      device_workspace_slot,
                       loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
                       stream_ptr)
 from ._types import LoadMatrix, SolveOptions, VoltageBatch
@@ -66,15 +67,17 @@ class DenseOperator:
     what ``batch_solve_dense`` and ``bench.py`` call.
     """
 
-    def __init__(self, model, device=None):
+    def __init__(self, model, device=None, dtype=None):
         self.device = require_cuda(device)
         self.contract = ModelContract.of(model)
+        self.dtype = engine_dtype(dtype)
         b = self.contract.b
         K, W = dense_kw(self.contract)
         self.K_host = K
         self.W_host = W
-        self.K = torch.from_numpy(np.array(K)).to(self.device)  # (the cached arrays are read-only)
-        self.W = torch.from_numpy(np.array(W)).to(self.device)
+        # K, W in the engine's dtype (c64: rounded from the float64 inverse)
+        self.K = torch.from_numpy(np.array(K, dtype=self.dtype)).to(self.device)
+        self.W = torch.from_numpy(np.array(W, dtype=self.dtype)).to(self.device)
         self.large = b > _capi.load().tpf_dense_max_nodes()
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
@@ -100,10 +103,24 @@ class DenseOperator:
         b, tau = S.shape
         if b != self.b:
             raise ValueError(f"load matrix has {b} rows, model has {self.b}")
+        tdt = torch.complex64 if self.dtype == np.complex64 else torch.complex128
+        if S.dtype != tdt:
+            raise ValueError(f"loads are {S.dtype}, the operator computes in {tdt}")
         if V is None:
-            V = torch.empty((b, tau), dtype=torch.complex128, device=self.device)
+            V = torch.empty((b, tau), dtype=tdt, device=self.device)
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
+        if self.dtype == np.complex64:  # the c64 twin (include/tpf.h)
+            need = int(_capi.load().tpf_dense_c64_workspace_bytes(tau, b))
+            if self._ws is None or self._ws.numel() < need:
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            sn, sc = complex_strides(S)
+            vn, vc = complex_strides(V)
+            _capi.call("tpf_dense_fpi_c64", tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
+                       self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                       V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                       stream_ptr(self.device))
+            return V, iters
         ws = self.workspace(tau)
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
@@ -120,7 +137,7 @@ class DenseOperator:
 
 def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
                       workers: int = 1, *, device=None, devices=None, return_on_device: bool = False,
-                      chunk_cases: int = 0) -> VoltageBatch:
+                      chunk_cases: int = 0, dtype=None) -> VoltageBatch:
     """GPU ``batch_solve_dense`` (dense.py:129-205); see module docstring.
 
     Host (numpy) loads go through the native chunked H2D/solve/D2H pipeline
@@ -128,7 +145,8 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
     ``devices=[...]`` the cases are split into contiguous slices, one pipeline
     per device, run concurrently (bitwise the same result).  With
     ``return_on_device=True`` the loads are copied once and the result stays
-    on the device as torch tensors.
+    on the device as torch tensors.  ``dtype=numpy.complex64`` runs the c64
+    twin (FP32, b <= 104, one device; pass a tolerance >= ~1e-6).
     """
     del workers  # accepted for signature compatibility; partitioning never changes bits
     if not isinstance(loads, LoadMatrix):
@@ -139,12 +157,13 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
         raise NotImplementedError(
             "mixed ZIP loads are not on the batched hot path; the reference routes them "
             "through its single-case solver (tpflow.dense._batch_via_single -> fpi_solve)")
-    if not return_on_device:
+    dt = engine_dtype(dtype)
+    if not return_on_device and dt == np.complex128:
         return _solve_host_pipeline(model, loads, opts, resolve_devices(device, devices), chunk_cases)
     if devices is not None and len(devices) > 1:
-        raise ValueError("return_on_device=True needs a single device")
-    op = DenseOperator(model, devices[0] if devices else device)
-    S = loads_to_device(loads.values, op.device)
+        raise ValueError("return_on_device=True and dtype=complex64 run on a single device")
+    op = DenseOperator(model, devices[0] if devices else device, dtype=dt)
+    S = loads_to_device(loads.values, op.device, dt)
     V, iters = op.solve(S, opts)
     resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
     return finish(V, iters, resid, mask, summ, return_on_device)

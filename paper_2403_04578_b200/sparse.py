@@ -32,7 +32,8 @@ from scipy import sparse
 from scipy.sparse.linalg import splu
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, host_csr, host_empty, host_loads, device_workspace_slot,
+from ._device import (ModelContract, complex_strides, engine_dtype, host_csr, host_empty, host_loads,
+                      device_workspace_slot,
                       loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
                       stream_ptr)
 from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
@@ -331,9 +332,11 @@ def lu_solve_host(f: TreeLU, rhs: np.ndarray) -> np.ndarray:
 class SparseOperator:
     """One factorization of Y_dd resident on a device; ``solve`` iterates."""
 
-    def __init__(self, model, device=None, use_tree: bool = True):
+    def __init__(self, model, device=None, use_tree: bool = True, dtype=None):
         self.device = require_cuda(device)
         self.contract = ModelContract.of(model)
+        self.dtype = engine_dtype(dtype)
+        c64 = self.dtype == np.complex64
         self.lu = factorize_ydd(self.contract.y_dd)
         d = self.device
         def t(a):  # never hand a 0-element (null) buffer to the C ABI
@@ -342,9 +345,11 @@ class SparseOperator:
                 a = np.zeros(1, dtype=a.dtype)
             return torch.from_numpy(a).to(d)
         f = self.lu
-        self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(f.l_val), u_ptr=t(f.u_ptr),
-                        u_col=t(f.u_col), u_val=t(f.u_val), u_diag_inv=t(f.u_diag_inv),
-                        perm=t(f.perm), src=t(self.contract.src))
+        cx = (lambda a: np.asarray(a).astype(np.complex64)) if c64 else (lambda a: a)
+        self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(cx(f.l_val)), u_ptr=t(f.u_ptr),
+                        u_col=t(f.u_col), u_val=t(cx(f.u_val)), u_diag_inv=t(cx(f.u_diag_inv)),
+                        perm=t(f.perm), src=t(cx(self.contract.src)))
+        use_tree = use_tree and not c64  # the c64 twin is the general CSR kernel
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
         self._csr = None
@@ -380,8 +385,11 @@ class SparseOperator:
         b, tau = S.shape
         if b != self.b:
             raise ValueError(f"load matrix has {b} rows, model has {self.b}")
+        tdt = torch.complex64 if self.dtype == np.complex64 else torch.complex128
+        if S.dtype != tdt:
+            raise ValueError(f"loads are {S.dtype}, the operator computes in {tdt}")
         if V is None:
-            V = torch.empty((b, tau), dtype=torch.complex128, device=self.device)
+            V = torch.empty((b, tau), dtype=tdt, device=self.device)
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
         if self.tree is not None:
@@ -402,13 +410,15 @@ class SparseOperator:
             if resid is not None:
                 self._residual(S, V, resid)
             return V, iters
-        need = int(_capi.load().tpf_sparse_workspace_bytes(tau, b))
+        c64 = self.dtype == np.complex64
+        lib = _capi.load()
+        need = int(lib.tpf_sparse_c64_workspace_bytes(tau, b) if c64 else lib.tpf_sparse_workspace_bytes(tau, b))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
         g = self.dev
-        _capi.call("tpf_sparse_fpi_c128", tau, b, S.data_ptr(), sn, sc,
+        _capi.call("tpf_sparse_fpi_c64" if c64 else "tpf_sparse_fpi_c128", tau, b, S.data_ptr(), sn, sc,
                    g["l_ptr"].data_ptr(), g["l_col"].data_ptr(), g["l_val"].data_ptr(),
                    g["u_ptr"].data_ptr(), g["u_col"].data_ptr(), g["u_val"].data_ptr(),
                    g["u_diag_inv"].data_ptr(), g["perm"].data_ptr(), g["src"].data_ptr(),
@@ -423,7 +433,7 @@ class SparseOperator:
         rp, ci, val, src = self.csr()
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
-        _capi.call("tpf_residual_c128", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+        _capi.call("tpf_residual_c64" if V.dtype == torch.complex64 else "tpf_residual_c128", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
                    rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(),
                    stream_ptr(self.device))
 
@@ -431,12 +441,13 @@ class SparseOperator:
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
                        max_nnz: int | None = None, *, device=None, devices=None,
                        return_on_device: bool = False, chunk_cases: int = 0,
-                       use_tree: bool = True) -> VoltageBatch:
+                       use_tree: bool = True, dtype=None) -> VoltageBatch:
     """GPU ``batch_solve_sparse`` (sparse.py:167-207); see module docstring.
 
     ``devices=[...]``: contiguous case slices solved concurrently, one host
     pipeline per device, after the one host factorization (bitwise the same
-    result as one device).
+    result as one device).  ``dtype=numpy.complex64`` runs the c64 twin (FP32
+    general CSR kernel, one device; pass a tolerance >= ~1e-6).
     """
     if not isinstance(loads, LoadMatrix):
         loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
@@ -450,12 +461,13 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
             raise MemoryGuardError(
                 f"block system would hold {total} nonzeros (> {max_nnz}); "
                 "chunk the batch over cases and solve the chunks separately")
-    if not return_on_device:
+    dt = engine_dtype(dtype)
+    if not return_on_device and dt == np.complex128:
         return _solve_host_pipeline(model, loads, opts, resolve_devices(device, devices), chunk_cases, use_tree)
     if devices is not None and len(devices) > 1:
-        raise ValueError("return_on_device=True needs a single device")
-    op = SparseOperator(model, devices[0] if devices else device, use_tree=use_tree)
-    S = loads_to_device(loads.values, op.device)
+        raise ValueError("return_on_device=True and dtype=complex64 run on a single device")
+    op = SparseOperator(model, devices[0] if devices else device, use_tree=use_tree, dtype=dt)
+    S = loads_to_device(loads.values, op.device, dt)
     resid = torch.empty(S.shape[1], dtype=torch.float64, device=op.device)
     V, iters = op.solve(S, opts, resid=resid)
     out = (resid, torch.empty(S.shape[1], dtype=torch.uint8, device=op.device),

@@ -207,3 +207,12 @@ class TestCaseSlices:
         assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
         sizes = [hi - lo for lo, hi in sl]
         assert max(sizes) - min(sizes) <= 1
+
+
+def test_engine_dtype_validation():
+    from paper_2403_04578_b200._device import engine_dtype
+    assert engine_dtype(None) == np.complex128
+    assert engine_dtype(np.complex64) == np.complex64
+    assert engine_dtype("complex64") == np.complex64
+    with pytest.raises(ValueError):
+        engine_dtype(np.float32)
