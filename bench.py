@@ -232,8 +232,15 @@ def run_ours():
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # TPF_BENCH_ONE_GPU=1 (plumbing check only): every rank on cuda:0 over gloo.
+    # The ranks never wait on each other inside a kernel, only at the barriers.
+    if os.environ.get("TPF_BENCH_ONE_GPU") == "1":
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("TPF_BENCH_ONE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2403_04578_b200 import DenseOperator, SparseOperator, LoadMatrix, _capi
