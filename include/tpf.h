@@ -243,6 +243,26 @@ int tpf_batch_summary(int64_t tau, const int32_t* iters, const double* resid,
  * workspace: device scratch of >= tpf_*_solve_host_workspace_bytes(...)
  * bytes, or NULL to let the call cudaMalloc/cudaFree its own.
  * Synchronous: returns when every output is on the host.                  */
+/* ------------------------------------------------------------ file tables --
+ * Host-only, multi-threaded (threads <= 0: all hardware threads).
+ * Load table (reference fileio.py:196-234): header p_1,q_1,...,p_b,q_b, one
+ * row per case, blank lines skipped.  tpf_loads_csv_scan validates the
+ * header and counts the cases; tpf_loads_csv_read parses them (correctly
+ * rounded) into values = complex128 b x tau node-major.  A malformed row gives
+ * TPF_ERR_INVALID and *bad_line (1-based); a field whose float() reading
+ * could differ from strtod (inf/nan words, hex, underscores, > 63 chars)
+ * gives TPF_ERR_UNSUPPORTED.
+ * tpf_write_pairs_csv: the header line, then per case j one row
+ * x[0,j],y[0,j],...,x[b-1,j],y[b-1,j][,flag[j]] with "%.17g" cells ("nan"
+ * for every NaN): the voltage table (x = |V|, y = angle V, flag = converged;
+ * fileio.py:237-253) and the load table writer (fileio.py:184-193).       */
+int tpf_loads_csv_scan(const char* path, int32_t* b, int64_t* tau);
+int tpf_loads_csv_read(const char* path, int32_t b, int64_t tau, double* values, int64_t* bad_line,
+                       int32_t threads);
+int tpf_write_pairs_csv(const char* path, const char* header, int32_t b, int64_t tau, const double* x,
+                        const double* y, int64_t node_stride, int64_t case_stride, const uint8_t* flag,
+                        int32_t threads);
+
 /* Page-lock a host range for the duration of several concurrent host-pipeline
  * calls (multi-device use): returns 1 if this call registered it (release with
  * tpf_host_unpin), 0 if it was already page-locked or cannot be.          */

@@ -93,6 +93,12 @@ SIGNATURES = {
     "tpf_residual_c64": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr]),
+    "tpf_loads_csv_scan": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32),
+                                          ctypes.POINTER(ctypes.c_int64)]),
+    "tpf_loads_csv_read": (ctypes.c_int, [ctypes.c_char_p, _c_i32, _c_i64, _c_ptr, ctypes.POINTER(ctypes.c_int64),
+                                          _c_i32]),
+    "tpf_write_pairs_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _c_i32, _c_i64, _c_ptr, _c_ptr, _c_i64,
+                                           _c_i64, _c_ptr, _c_i32]),
     "tpf_host_pin": (ctypes.c_int, [_c_ptr, _c_sz]),
     "tpf_host_unpin": (ctypes.c_int, [_c_ptr]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),
