@@ -145,8 +145,9 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
  *               first), then the first TMEM slot of each level
  *   node_info   int32[4*b]: per level-ordered node {original node, parent,
  *               first child, child count} (parent -1 at the roots)
- *   node_coef   complex[4*b]: {e = Y[parent,m], g = U[m,parent]/U[m,m],
- *               1/U[m,m], src} (symmetric Y_dd; src nonzero only at the
+ *   node_coef   complex[4*b], four planes of b (coalesced per level):
+ *               [0*b + m] e = Y[parent,m], [1*b + m] g = U[m,parent]/U[m,m],
+ *               [2*b + m] 1/U[m,m], [3*b + m] src (symmetric Y_dd; src nonzero only at the
  *               root level, at most 512 root-level nodes, at most 6 slots
  *               (ceil(level size / 512)) per level)
  * Limits: b <= 7,800 and sum over levels of ceil(n_level/512) <=

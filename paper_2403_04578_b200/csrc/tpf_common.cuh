@@ -55,6 +55,19 @@ __device__ __forceinline__ void stg_c128(double* base, int64_t idx, double2 v) {
   reinterpret_cast<double2*>(base)[idx] = v;
 }
 
+// 1/x for an iterate's |v|^2 (in [1e-24, ~1e300]): MUFU seed + two Newton
+// steps, faithfully rounded; 4 FP64 instructions and a short dependency chain
+// instead of the IEEE divide's ~10 (on the dense path every FP64 instruction
+// also costs the SMSP's DMMA stream ~9 cycles).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // NaN-propagating running max, matching numpy's max reduction.
 __device__ __forceinline__ double nanmax(double m, double x) {
   return (x > m || x != x) ? x : m;

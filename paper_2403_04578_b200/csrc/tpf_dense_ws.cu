@@ -95,18 +95,6 @@ __device__ __forceinline__ int claim(unsigned long long* counter) {
   return c < (unsigned long long)INT_MAX ? int(c) : INT_MAX;
 }
 
-// 1/x for the iterate's |v|^2 (in [1e-24, ~1e300]): MUFU seed + two Newton
-// steps, faithfully rounded; 4 FP64 instructions instead of the IEEE divide's
-// ~10 (every FP64 instruction here costs the SMSP's DMMA stream ~9 cycles).
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = __fma_rn(-x, r, 1.0);
-  r = __fma_rn(r, e, r);
-  e = __fma_rn(-x, r, 1.0);
-  return __fma_rn(r, e, r);
-}
-
 __device__ __forceinline__ int abs_hi(double x) { return __double2hiint(x) & 0x7fffffff; }
 
 // Step test of the 3M variant: |dr + i di|^2 < tol^2 is decided on the

@@ -434,14 +434,17 @@ extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t l
   std::vector<int32_t> h_ec;
   std::vector<double> h_ev;
   DevBuf dec, dev_;
-  const bool fuse = ydd_col && ydd_val && ell_w >= 1 && ell_w <= tpf_sparse_tree_max_ell_width();
+  bool fuse = ydd_col && ydd_val && ell_w >= 1 && ell_w <= tpf_sparse_tree_max_ell_width();
   if (fuse) {
     h_ec.resize(size_t(ell_w) * b);
     h_ev.resize(size_t(ell_w) * b * 2);
-    int rc = tpf_sparse_tree_build_ell(b, ell_w, node_info, ydd_row_ptr, ydd_col, ydd_val, h_ec.data(), h_ev.data());
-    if (rc != TPF_OK) return rc;
-    TPF_CK(upload(dec, h_ec.data(), h_ec.size(), st), "upload(ell_col)");
-    TPF_CK(upload(dev_, h_ev.data(), h_ev.size(), st), "upload(ell_val)");
+    if (tpf_sparse_tree_build_ell(b, ell_w, node_info, ydd_row_ptr, ydd_col, ydd_val, h_ec.data(), h_ev.data()) ==
+        TPF_OK) {
+      TPF_CK(upload(dec, h_ec.data(), h_ec.size(), st), "upload(ell_col)");
+      TPF_CK(upload(dev_, h_ev.data(), h_ev.size(), st), "upload(ell_val)");
+    } else {
+      fuse = false;  // not a plain tree pattern: separate residual kernel
+    }
   }
   TreeChunk sv;
   if (fuse) {

@@ -28,6 +28,18 @@ namespace tpf {
 namespace {
 
 constexpr int kTreeThreads = 512;
+
+#ifdef TPF_PHASE_TIMING
+// debug build only (tools/build_timing.sh): thread 0 of every CTA accumulates
+// cycles per phase: {case load, up-sweep, down-sweep, retire, residual, cases, iterations, total}
+__device__ long long g_tree_cyc[148 * 8];
+#define TREE_T(v) const long long v = clock64()
+#define TREE_ACC(i, t0) \
+  if (threadIdx.x == 0) tc[i] += clock64() - (t0)
+#else
+#define TREE_T(v)
+#define TREE_ACC(i, t0)
+#endif
 constexpr int kMaxSlots = 16;
 constexpr int kMaxLevels = 64;
 
@@ -42,7 +54,7 @@ struct TreeArgs {
   unsigned long long* counter;
   const int32_t* lvl;     // [levels+1] level offsets in level order (root level first), then [levels+1] slot starts
   const int4* info;       // per level-ordered node m: {original node, parent m or -1, first child m, child count}
-  const double2* coef;    // per m: {e = Y[parent, m], g = U[m,parent]/U[m,m], uinv = 1/U[m,m], src}
+  const double2* coef;    // planes [4][b] (level order m): e = Y[parent, m], g = U[m,parent]/U[m,m], uinv = 1/U[m,m], src
   double2 v_flat;
   double tol2;
   int max_iter;
@@ -79,7 +91,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
   __shared__ int s_off[kMaxLevels + 1], s_j0[kMaxLevels + 1];
   __shared__ double2 s_src[kMaxRoots];  // source injection of the root level (zero elsewhere)
   __shared__ int s_slot_lvl[kMaxSlots];
-  __shared__ int s_case;
+  __shared__ int s_case, s_next;
   __shared__ double s_red[kTreeThreads / 32];
   __shared__ uint32_t s_tmem;
 
@@ -95,7 +107,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     par[m] = inf.y;
   }
   __syncthreads();
-  for (int m = tid; m < s_off[1] && m < kMaxRoots; m += kTreeThreads) s_src[m] = __ldg(&a.coef[4 * m + 3]);
+  for (int m = tid; m < s_off[1] && m < kMaxRoots; m += kTreeThreads) s_src[m] = __ldg(&a.coef[3 * a.b + m]);
   if (tid < kMaxSlots) {
     int lv = 0;
     for (int d = 0; d < L; ++d)
@@ -117,13 +129,25 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     return m < s_off[d + 1] ? m : -1;
   };
 
+#ifdef TPF_PHASE_TIMING
+  long long tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_begin = clock64();
+#endif
+  // cases are claimed one ahead: while case k iterates, the loads of case
+  // k + 1 are already on their way from HBM into L2 (prefetch at k's load)
+  auto claim = [&]() {
+    const unsigned long long c = atomicAdd(a.counter, 1ull);
+    return c < (unsigned long long)a.tau ? int(c) : -1;
+  };
+  if (tid == 0) s_next = claim();
   for (;;) {
+    TREE_T(t_load);
     if (tid == 0) {
-      const unsigned long long c = atomicAdd(a.counter, 1ull);
-      s_case = c < (unsigned long long)a.tau ? int(c) : -1;
+      s_case = s_next;
+      s_next = s_case < 0 ? -1 : claim();
     }
     __syncthreads();
-    const int cs = s_case;
+    const int cs = s_case, nx = s_next;
     if (cs < 0) break;
 
     // ---- load the case: S into TMEM, flat start V (dense.py:155) ----
@@ -136,7 +160,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       for (int j = 0; j < 4; ++j) {
         const int m = slot_node(j0 + j);
         sv[j] = make_double2(0.0, 0.0);
-        if (m >= 0) sv[j] = __ldg(a.S + __ldg(&a.info[m].x) * a.s_node + int64_t(cs) * a.s_case);
+        if (m >= 0) {
+          const int64_t row = int64_t(__ldg(&a.info[m].x)) * a.s_node;
+          sv[j] = __ldg(a.S + row + int64_t(cs) * a.s_case);
+          if (nx >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.S + row + int64_t(nx) * a.s_case));
+        }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -154,7 +182,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     // BEFORE the barrier, so their latency overlaps the barrier wait.
     //   up:   z_m = r_m - sum_c P_c,  P_m = g_m z_m            (g = U[m,p] / U[m,m])
     //   down: w_m = z_m / U_mm - g_m w_p
-    D2 vv[1], ss[1];
+    D2 vv[2], ss[2];
     double2 cg[kLS], cu[kLS];
     // global coefficient loads of a level, issued before the barrier that precedes it
     auto issue_up = [&](int d) {
@@ -162,7 +190,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 #pragma unroll
       for (int u = 0; u < kLS; ++u) {
         const int m = off + u * kTreeThreads + tid;
-        cg[u] = (jb + u < je && m < end) ? __ldg(&a.coef[4 * m + 1]) : make_double2(0.0, 0.0);
+#ifdef TPF_TREE_NOCOEF
+        cg[u] = make_double2(0.01 * m, 0.0);
+#else
+        cg[u] = (jb + u < je && m < end) ? __ldg(&a.coef[a.b + m]) : make_double2(0.0, 0.0);
+#endif
       }
     };
     auto issue_down = [&](int d) {
@@ -171,46 +203,63 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       for (int u = 0; u < kLS; ++u) {
         const int m = off + u * kTreeThreads + tid;
         const bool ok = jb + u < je && m < end;
-        cu[u] = ok ? __ldg(&a.coef[4 * m + 2]) : make_double2(0.0, 0.0);
-        cg[u] = (ok && d > 0) ? __ldg(&a.coef[4 * m + 1]) : make_double2(0.0, 0.0);
+#ifdef TPF_TREE_NOCOEF
+        cu[u] = make_double2(ok ? 1.0 : 0.0, 0.0);
+        cg[u] = make_double2(0.01 * m, 0.0);
+#else
+        cu[u] = ok ? __ldg(&a.coef[2 * a.b + m]) : make_double2(0.0, 0.0);
+        cg[u] = (ok && d > 0) ? __ldg(&a.coef[a.b + m]) : make_double2(0.0, 0.0);
+#endif
       }
     };
 
+    TREE_ACC(0, t_load);
+#ifdef TPF_PHASE_TIMING
+    if (tid == 0) tc[5] += 1;
+#endif
     int it = 0;
     issue_up(L - 1);
     while (it < a.max_iter) {
+      TREE_T(t_up);
       // ---- up-sweep: deepest level first ----
       for (int d = L - 1; d >= 0; --d) {
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
+        // slots in pairs: both TMEM loads, one wait, two independent chains
 #pragma unroll
-        for (int u = 0; u < kLS; ++u) {
-          const int m = off + u * kTreeThreads + tid;
-          if (jb + u < je) {  // warp-uniform
-            tmem_ld2(tm_v + 4 * (jb + u), vv[0]);
-            tmem_ld2(tm_s + 4 * (jb + u), ss[0]);
-            tmem_wait_ld();
-          }
-          if (jb + u < je && m < end) {
-            double2 v = vv[0].get();
-            const double2 sl = ss[0].get();
-            double m2 = __fma_rn(v.x, v.x, v.y * v.y);
-            if (m2 < kZeroGuard2) {  // fpi.py:39-41
-              v = make_double2(kZeroGuard, 0.0);
-              m2 = kZeroGuard * kZeroGuard;
+        for (int u0 = 0; u0 < kLS; u0 += 2) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (jb + u0 + h < je) {  // warp-uniform
+              tmem_ld2(tm_v + 4 * (jb + u0 + h), vv[h]);
+              tmem_ld2(tm_s + 4 * (jb + u0 + h), ss[h]);
             }
-            const double r = 1.0 / m2;
-            const double2 src = d == 0 ? s_src[m] : make_double2(0.0, 0.0);
-            // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
-            double2 z = make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
-                                     -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
-            const int2 k = kids[m];
-            for (int c = k.x; c < k.x + k.y; ++c) {
-              const double2 pc = P[c];
-              z.x -= pc.x;
-              z.y -= pc.y;
+          if (jb + u0 < je) tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int u = u0 + h;
+            const int m = off + u * kTreeThreads + tid;
+            if (jb + u < je && m < end) {
+              double2 v = vv[h].get();
+              const double2 sl = ss[h].get();
+              double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+              if (m2 < kZeroGuard2) {  // fpi.py:39-41
+                v = make_double2(kZeroGuard, 0.0);
+                m2 = kZeroGuard * kZeroGuard;
+              }
+              const double r = rcp_nr(m2);
+              const double2 src = d == 0 ? s_src[m] : make_double2(0.0, 0.0);
+              // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
+              double2 z = make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
+                                       -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
+              const int2 k = kids[m];
+              for (int c = k.x; c < k.x + k.y; ++c) {
+                const double2 pc = P[c];
+                z.x -= pc.x;
+                z.y -= pc.y;
+              }
+              T[m] = z;
+              P[m] = cmul2(cg[u], z);
             }
-            T[m] = z;
-            P[m] = cmul2(cg[u], z);
           }
         }
         if (d > 0)
@@ -219,29 +268,37 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
           issue_down(0);
         __syncthreads();
       }
+      TREE_ACC(1, t_up);
+      TREE_T(t_down);
       // ---- down-sweep: root level first, step test, iterate update ----
       bool small = true;
       int all_small = 0;
       for (int d = 0; d < L; ++d) {
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
 #pragma unroll
-        for (int u = 0; u < kLS; ++u) {
-          if (jb + u < je) {
-            const int m = off + u * kTreeThreads + tid;
-            tmem_ld2(tm_v + 4 * (jb + u), vv[0]);
-            tmem_wait_ld();
-            double2 v = vv[0].get();
-            double2 w = v;
-            if (m < end) {
-              w = cmul2(T[m], cu[u]);
-              const int p = par[m];
-              if (p >= 0) w = cfma_sub(w, cg[u], T[p]);
-              T[m] = w;
-              if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
-              const double dr = w.x - v.x, di = w.y - v.y;
-              if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+        for (int u0 = 0; u0 < kLS; u0 += 2) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (jb + u0 + h < je) tmem_ld2(tm_v + 4 * (jb + u0 + h), vv[h]);
+          if (jb + u0 < je) tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int u = u0 + h;
+            if (jb + u < je) {
+              const int m = off + u * kTreeThreads + tid;
+              double2 v = vv[h].get();
+              double2 w = v;
+              if (m < end) {
+                w = cmul2(T[m], cu[u]);
+                const int p = par[m];
+                if (p >= 0) w = cfma_sub(w, cg[u], T[p]);
+                T[m] = w;
+                if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+                const double dr = w.x - v.x, di = w.y - v.y;
+                if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+              }
+              tmem_st2(tm_v + 4 * (jb + u), w);
             }
-            tmem_st2(tm_v + 4 * (jb + u), w);
           }
         }
         tmem_wait_st();
@@ -252,11 +309,13 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
           all_small = __syncthreads_and(small);
         }
       }
+      TREE_ACC(2, t_down);
       ++it;
       if (all_small) break;
       issue_up(L - 1);
     }
 
+    TREE_T(t_ret);
     // ---- retire: V out, per-case count; with the fused residual V also goes
     // to T (the sweeps are done with it) ----
 #pragma unroll
@@ -276,6 +335,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         }
       }
     }
+    TREE_ACC(3, t_ret);
+    TREE_T(t_res);
     if (a.resid) {
       // residual_per_case (fpi.py:221-240): max_i |s_i + v_i conj(src_i + (Y_dd v)_i)|,
       // the operations of residual_kernel in the same order (bit-identical)
@@ -289,17 +350,19 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         tmem_ld2(tm_s + 4 * j, sd);
         const int m = slot_node(j);
         double ar = 0.0, ai = 0.0;
+        int len = 0;  // row length = diagonal + parent + children (checked by tpf_sparse_tree_build_ell)
         if (m >= 0) {
-          const double2 si = __ldg(&a.coef[4 * m + 3]);
+          const double2 si = __ldg(&a.coef[3 * a.b + m]);
           ar = si.x;
           ai = si.y;
+          len = 1 + (par[m] >= 0) + kids[m].y;
         }
         for (int r0 = 0; r0 < a.ell_w; r0 += kEllChunk) {
           int c[kEllChunk];
           double2 y[kEllChunk];
 #pragma unroll
           for (int r = 0; r < kEllChunk; ++r) {
-            const bool ok = m >= 0 && r0 + r < a.ell_w;
+            const bool ok = r0 + r < len;  // padding entries are not loaded
             c[r] = ok ? __ldg(a.ell_col + (r0 + r) * a.b + m) : -1;
             y[r] = ok ? __ldg(a.ell_val + (r0 + r) * a.b + m) : make_double2(0.0, 0.0);
           }
@@ -330,8 +393,18 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         a.resid[cs] = w;
       }
     }
+    TREE_ACC(4, t_res);
+#ifdef TPF_PHASE_TIMING
+    if (tid == 0) tc[6] += it;
+#endif
     if (tid == 0) a.iters[cs] = it;
   }
+#ifdef TPF_PHASE_TIMING
+  if (tid == 0 && blockIdx.x < 148) {
+    tc[7] = clock64() - t_begin;
+    for (int i = 0; i < 8; ++i) g_tree_cyc[blockIdx.x * 8 + i] = tc[i];
+  }
+#endif
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -344,6 +417,12 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 using namespace tpf;
 
 extern "C" int tpf_sparse_tree_max_slots(void) { return kMaxSlots; }
+
+#ifdef TPF_PHASE_TIMING
+extern "C" int tpf_debug_tree_phase_cycles(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tree_cyc, sizeof(g_tree_cyc)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info, const int32_t* node_info,
                        const double* node_coef, const double* S, int64_t s_node_stride, int64_t s_case_stride,
@@ -449,6 +528,9 @@ extern "C" int tpf_sparse_tree_build_ell(int32_t b, int32_t width, const int32_t
     const int i = node_info[4 * m];
     const int lo = ydd_row_ptr[i], n = ydd_row_ptr[i + 1] - lo;
     if (n > width) return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_build_ell: row wider than width");
+    // the kernel reads row m's length from the tree (diagonal + parent + children)
+    if (n != 1 + (node_info[4 * m + 1] >= 0 ? 1 : 0) + node_info[4 * m + 3])
+      return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_build_ell: Y_dd row is not diagonal + tree edges");
     for (int r = 0; r < width; ++r) {
       const size_t at = size_t(r) * b + m;
       if (r < n) {

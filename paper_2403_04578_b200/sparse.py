@@ -177,8 +177,8 @@ class TreeSchedule:
     children of the same parent are contiguous.  ``level_info`` = level
     offsets (levels+1) followed by per-level first TMEM slot (levels+1);
     ``node_info`` = int32[4 per node] {original node, parent, first child,
-    child count}; ``node_coef`` = complex[4 per node] {L[parent, m],
-    U[m, parent], 1/U[m, m], src[original node]}.
+    child count}; ``node_coef`` = complex, four planes of b (level order):
+    e = Y[parent, m], g = U[m, parent] / U[m, m], 1/U[m, m], src[original node].
     """
 
     b: int
@@ -272,7 +272,7 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
     return TreeSchedule(b=b, levels=levels,
                         level_info=np.concatenate([offs, j0]).astype(np.int32),
                         node_info=np.ascontiguousarray(info.ravel()),
-                        node_coef=np.ascontiguousarray(coef.ravel()), slots=int(j0[-1]))
+                        node_coef=np.ascontiguousarray(coef.T.ravel()), slots=int(j0[-1]))
 
 
 def tree_ell(t: TreeSchedule, contract) -> tuple[int, np.ndarray, np.ndarray] | None:
@@ -284,7 +284,8 @@ def tree_ell(t: TreeSchedule, contract) -> tuple[int, np.ndarray, np.ndarray] | 
         return None
     col = np.empty(w * t.b, dtype=np.int32)
     val = np.empty(w * t.b, dtype=np.complex128)
-    _capi.call("tpf_sparse_tree_build_ell", t.b, w, ptr(t.node_info), ptr(rp), ptr(ci), ptr(yv), ptr(col), ptr(val))
+    if lib.tpf_sparse_tree_build_ell(t.b, w, ptr(t.node_info), ptr(rp), ptr(ci), ptr(yv), ptr(col), ptr(val)) != 0:
+        return None  # rows beyond diagonal + tree edges: the separate residual kernel
     return w, col, val
 
 
@@ -292,7 +293,7 @@ def tree_solve_host(t: TreeSchedule, rhs: np.ndarray) -> np.ndarray:
     """Numpy emulation of the tree kernel's two sweeps (host-logic tests only)."""
     b = t.b
     info = t.node_info.reshape(b, 4)
-    coef = t.node_coef.reshape(b, 4)
+    coef = t.node_coef.reshape(4, b).T
     offs = t.level_info[:t.levels + 1]
     T = np.zeros(b, dtype=complex)
     for d in range(t.levels - 1, -1, -1):
