@@ -6,6 +6,8 @@
     python -m paper_2403_04578_b200 gen-net --buses N [--kmax 5] [--seed 0] ... --out NET.json
     python -m paper_2403_04578_b200 gen-loads --network NET.json --tau T [--seed 0] [--scale 1]
         [--correlation 0.5] --out LOADS.csv
+    python -m paper_2403_04578_b200 bench [--methods dense,sparse] [--sizes 9,100] [--taus 1,100] --out R.csv
+    python -m paper_2403_04578_b200 fit --records R.csv --variable tau|b_phi [--method dense]
 
 ``solve`` runs the GPU engine (cli.py:54-76 semantics: same metadata keys,
 non-convergence is data, exit 1 with ``error: ...`` on FileFormatError /
@@ -13,7 +15,9 @@ NetworkError / ValueError / MemoryError, cli.py:315-317); ``gen-net`` and
 ``gen-loads`` are the reference's seeded generators (bit-identical networks and
 loads, cli.py:79-95).  Tables are read and written by the native file layer
 (fileio.py in this package); identical invocations produce byte-identical
-data files.  The reference's twobus / bench / fit subcommands are outside the
+data files.  ``bench`` / ``fit`` are the reference's harness (bench.py:120-222)
+over the GPU methods, in the same record format, plus per-cell roofline
+figures in the metadata.  The reference's twobus subcommands are outside the
 accelerated path.
 """
 
@@ -114,6 +118,41 @@ def _cmd_gen_loads(args) -> int:
     return 0
 
 
+def _int_list(text: str) -> tuple[int, ...]:
+    try:
+        return tuple(int(x) for x in text.split(",") if x.strip())
+    except ValueError as exc:
+        raise ValueError(f"expected a comma-separated integer list, got {text!r}") from exc
+
+
+def _cmd_bench(args) -> int:
+    from .harness import BenchConfig, roofline_meta, run_benchmark, write_bench_records
+    config = BenchConfig(methods=tuple(args.methods.split(",")), sizes=_int_list(args.sizes),
+                         taus=_int_list(args.taus), seed=args.seed, repeats=args.repeats, timeout=args.timeout,
+                         options=SolveOptions(tolerance=args.tol, max_iterations=args.max_iter))
+    cells: list = []
+    records = run_benchmark(config, roofline=cells)
+    write_bench_records(args.out, records)
+    fileio.write_metadata(args.meta or f"{args.out}.meta.json", {
+        "methods": list(config.methods), "sizes": list(config.sizes), "taus": list(config.taus),
+        "seed": config.seed, "repeats": config.repeats, "failed_cells": sum(not r.ok for r in records),
+        "roofline": roofline_meta(cells)})
+    return 0
+
+
+def _cmd_fit(args) -> int:
+    from .harness import fit_complexity, read_bench_records
+    records = read_bench_records(args.records)
+    if args.method:
+        records = [r for r in records if r.method == args.method]
+    fit = fit_complexity(records, args.variable)
+    print(f"t = {fit.c:.6g} * {fit.variable}^{fit.k:.4f}   (R^2 = {fit.r_squared:.6f}, {fit.n_points} points)")
+    if args.out:
+        fileio.write_metadata(args.out, {"c": fit.c, "k": fit.k, "r_squared": fit.r_squared,
+                                         "variable": fit.variable, "n_points": fit.n_points})
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2403_04578_b200",
                                      description="B200 engine for batched fixed-point power flow")
@@ -152,6 +191,26 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--correlation", type=float, default=0.5)
     p.add_argument("--out", required=True)
     p.set_defaults(func=_cmd_gen_loads)
+
+    p = sub.add_parser("bench", help="time (method x size x tau) cells on the GPU (bench.py:120-176)")
+    p.add_argument("--methods", default="dense,sparse")
+    p.add_argument("--sizes", default="9,100")
+    p.add_argument("--taus", default="1,100")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--repeats", type=int, default=3)
+    p.add_argument("--timeout", type=float, default=300.0, help="per-cell wall-time cutoff in seconds")
+    p.add_argument("--tol", type=float, default=1e-10)
+    p.add_argument("--max-iter", type=int, default=100)
+    p.add_argument("--out", required=True)
+    p.add_argument("--meta", default=None)
+    p.set_defaults(func=_cmd_bench)
+
+    p = sub.add_parser("fit", help="fit t = c * n^k to benchmark records")
+    p.add_argument("--records", required=True)
+    p.add_argument("--variable", choices=("tau", "b_phi"), required=True)
+    p.add_argument("--method", default=None)
+    p.add_argument("--out", default=None)
+    p.set_defaults(func=_cmd_fit)
     return parser
 
 

@@ -73,3 +73,14 @@ def test_solve_devices_and_c64_flags(tmp_path):
     _, v, _ = table(c)
     _, rv, _ = table(fx("v9_dense.csv"))
     assert np.abs(v - rv).max() <= 2e-5
+
+
+def test_bench_and_fit_subcommands(tmp_path, capsys):
+    from paper_2403_04578_b200.cli import main
+    out = tmp_path / "r.csv"
+    assert main(["bench", "--methods", "dense,sparse", "--sizes", "9", "--taus", "10,100,1000", "--repeats", "2",
+                 "--out", str(out)]) == 0
+    meta = json.loads((tmp_path / "r.csv.meta.json").read_text())
+    assert meta["failed_cells"] == 0 and len(meta["roofline"]) == 6
+    assert main(["fit", "--records", str(out), "--variable", "tau", "--method", "dense"]) == 0
+    assert "t = " in capsys.readouterr().out
