@@ -177,6 +177,28 @@ int tpf_sparse_tree_fpi_resid_c128(int64_t tau, int32_t b, int32_t levels,
                                    const double* ell_val, double* resid,
                                    void* workspace, size_t workspace_bytes, void* stream);
 int tpf_sparse_tree_max_ell_width(void);
+/* ZIP loads on radial feeders (the reference's per-case fpi_solve route,
+ * dense.py:214-230 / fpi.py:107-206): per case the tree LU of
+ * B = Y_dd + diag(alpha_z s*) (no fill, leaf-first), then
+ *   B v' = -(alpha_p s* ./ conj(v) + src + alpha_i s*)
+ * with fpi_solve's rules: one application when alpha_p s = 0 everywhere,
+ * stop on a non-finite iterate, stop on the step test; the residual uses the
+ * ZIP load power.  alpha = float64 planes [3][b] (z, i, p), ydiag = Y[m,m]
+ * (complex[b]), both in level order; Y_dd must be exactly symmetric with
+ * rows = diagonal + tree edges (ELL as above).  step_met[j] = 1 when case j
+ * stopped on the step test (or was a one-application case); *status = 1
+ * if some case's B had a zero pivot (SingularSystemError in the reference).
+ * workspace >= tpf_sparse_tree_zip_workspace_bytes(tau, b).              */
+size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b);
+int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels,
+                                 const int32_t* level_info, const int32_t* node_info, const double* node_coef,
+                                 const double* alpha, const double* ydiag,
+                                 const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                                 double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                 double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                                 int32_t ell_width, const int32_t* ell_col, const double* ell_val,
+                                 double* resid, uint8_t* step_met, int32_t* status,
+                                 void* workspace, size_t workspace_bytes, void* stream);
 /* Host helpers (no device work): widest CSR row of Y_dd (-1 on bad input),
  * and the ELL rows above from the ORIGINAL-order CSR and node_info.        */
 int tpf_sparse_tree_ell_width(int32_t b, const int32_t* ydd_row_ptr);

@@ -236,3 +236,69 @@ def fpi_single(y_dd, src, v_s, s, tol=1e-10, max_iter=100, residual_tol=1e-8):
     with np.errstate(invalid="ignore", over="ignore"):
         res = float(residual_per_case(y_dd, src, v, s))
     return v, n, bool(step_met and res < residual_tol)
+
+
+# --------------------------------------------------------------------- ZIP
+
+
+def zip_residual(y_dd, src, az, ai, ap, v, s):
+    """``residual_per_case`` with ZIP load power (fpi.py:209-240), one case."""
+    v = np.asarray(v, dtype=complex)
+    s = np.asarray(s, dtype=complex)
+    s_load = az * s * np.abs(v) ** 2 + ai * s * v + ap * s
+    return float(np.abs(s_load + v * np.conj(src + y_dd @ v)).max())
+
+
+def fpi_single_zip(y_dd, src, v_s, az, ai, ap, s, tol=1e-10, max_iter=100, residual_tol=1e-8):
+    """``fpi_solve`` with ZIP loads (assemble_fpi fpi.py:107-127, loop fpi.py:137-206).
+
+    Returns (v, iterations, converged, residual, step_met).
+    """
+    s = np.asarray(s, dtype=complex).ravel()
+    sc = np.conj(s)
+    a = ap * sc
+    B = (sparse.diags(az * sc) + sparse.csc_matrix(y_dd, dtype=complex)).tocsc()
+    c = np.asarray(src, dtype=complex) + ai * sc
+    lu = splu(B)
+    w = -lu.solve(c.astype(complex))
+    v = np.full(s.shape[0], abs(v_s) * (1.0 + 0.0j))
+    if np.all(a == 0):
+        res = zip_residual(y_dd, src, az, ai, ap, w, s)
+        return w.copy(), 1, res < residual_tol, res, True
+    n = 0
+    step_met = False
+    with np.errstate(invalid="ignore", over="ignore", divide="ignore"):
+        while n < max_iter:
+            small = np.abs(v) < ZERO_VOLTAGE_GUARD
+            if small.any():
+                v = np.where(small, ZERO_VOLTAGE_GUARD * (1.0 + 0.0j), v)
+            v_next = -lu.solve(a * (1.0 / np.conj(v))) + w
+            n += 1
+            if not np.all(np.isfinite(v_next.view(float))):
+                v = v_next
+                break
+            step = np.abs(v_next - v).max()
+            v = v_next
+            if step < tol:
+                step_met = True
+                break
+    with np.errstate(invalid="ignore", over="ignore"):
+        res = zip_residual(y_dd, src, az, ai, ap, v, s)
+    return v, n, bool(step_met and res < residual_tol), res, step_met
+
+
+def dense_zip_batch(y_dd, src, v_s, az, ai, ap, S, tol=1e-10, max_iter=100, residual_tol=1e-8):
+    """``_batch_via_single`` (dense.py:214-230): per-case ZIP fpi_solve.
+
+    Returns (V, n_case, mask, residuals, batch_iterations).
+    """
+    S = np.asarray(S, dtype=complex)
+    b, tau = S.shape
+    V = np.empty((b, tau), dtype=complex)
+    n = np.zeros(tau, dtype=np.int64)
+    mask = np.zeros(tau, dtype=bool)
+    res = np.empty(tau)
+    for j in range(tau):
+        V[:, j], n[j], mask[j], res[j], _ = fpi_single_zip(y_dd, src, v_s, az, ai, ap, S[:, j], tol, max_iter,
+                                                           residual_tol)
+    return V, n, mask, res, int(n.max(initial=0))

@@ -65,6 +65,14 @@ struct TreeArgs {
   const int32_t* ell_col;
   const double2* ell_val;
   double* resid;          // or null
+  // ZIP loads (fpi.py:107-206 per case): planes [3][b] alpha_z, alpha_i,
+  // alpha_p and Y[m,m] in level order; per-CTA scratch [2][b] for the case's
+  // own g and 1/U[m,m]; status = 1 on a zero or non-finite pivot
+  const double* alpha;
+  const double2* ydiag;
+  double2* zcoef;
+  int32_t* status;
+  uint8_t* met;           // ZIP: 1 if the case stopped on the step test (or is a one-application case)
 };
 
 __device__ __forceinline__ double2 cfma_sub(double2 acc, double2 a, double2 x) {  // acc - a*x
@@ -82,6 +90,7 @@ constexpr int kEllChunk = 8;      // ELL entries loaded together
 // Sweeps with g_m = U[m,parent] / U[m,m] (so L[p,m] z_m = g_m z_m for symmetric Y):
 //   up:   z_m = r_m - sum_c g_c z_c
 //   down: w_m = z_m / U[m,m] - g_m w_parent
+template <bool ZIP>
 __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const TreeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* T = reinterpret_cast<double2*>(smem_raw);       // [b] sweep vector (zhat, then w)
@@ -185,6 +194,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     D2 vv[2], ss[2];
     double2 cg[kLS], cu[kLS];
     // global coefficient loads of a level, issued before the barrier that precedes it
+    // node coefficients g and 1/U[m,m]: shared planes, or (ZIP) this case's own
+    const double2* cgp = ZIP ? a.zcoef + size_t(blockIdx.x) * 2 * a.b : a.coef + a.b;
+    const double2* cup = ZIP ? cgp + a.b : a.coef + 2 * a.b;
     auto issue_up = [&](int d) {
       const int jb = s_j0[d], je = s_j0[d + 1], off = s_off[d], end = s_off[d + 1];
 #pragma unroll
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 #ifdef TPF_TREE_NOCOEF
         cg[u] = make_double2(0.01 * m, 0.0);
 #else
-        cg[u] = (jb + u < je && m < end) ? __ldg(&a.coef[a.b + m]) : make_double2(0.0, 0.0);
+        cg[u] = (jb + u < je && m < end) ? cgp[m] : make_double2(0.0, 0.0);
 #endif
       }
     };
@@ -207,8 +219,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         cu[u] = make_double2(ok ? 1.0 : 0.0, 0.0);
         cg[u] = make_double2(0.01 * m, 0.0);
 #else
-        cu[u] = ok ? __ldg(&a.coef[2 * a.b + m]) : make_double2(0.0, 0.0);
-        cg[u] = (ok && d > 0) ? __ldg(&a.coef[a.b + m]) : make_double2(0.0, 0.0);
+        cu[u] = ok ? cup[m] : make_double2(0.0, 0.0);
+        cg[u] = (ok && d > 0) ? cgp[m] : make_double2(0.0, 0.0);
 #endif
       }
     };
@@ -217,7 +229,52 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 #ifdef TPF_PHASE_TIMING
     if (tid == 0) tc[5] += 1;
 #endif
+    bool anz = true;  // ZIP: some alpha_p s != 0 (else fpi.py:150-163: one application)
+    if constexpr (ZIP) {
+      // this case's LU of B = Y_dd + diag(alpha_z s*) (assemble_fpi, fpi.py:107-127):
+      // leaf-first, no fill, so U[m,m] = B[m,m] - sum_c e_c^2 / U[c,c] and
+      // g_m = e_m / U[m,m] (e_m = Y[parent, m] = Y[m, parent]); level by level
+      double2* zg = a.zcoef + size_t(blockIdx.x) * 2 * a.b;
+      int any = 0, bad = 0;
+      for (int d = L - 1; d >= 0; --d) {
+        const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
+        for (int u = 0; u < kLS; ++u) {
+          if (jb + u >= je) break;  // warp-uniform
+          D2 sd;
+          tmem_ld2(tm_s + 4 * (jb + u), sd);
+          tmem_wait_ld();
+          const int m = off + u * kTreeThreads + tid;
+          if (m < end) {
+            const double2 sl = sd.get();
+            const double az = __ldg(a.alpha + m), ap = __ldg(a.alpha + 2 * a.b + m);
+            const double2 yd = __ldg(a.ydiag + m);
+            double2 piv = make_double2(__fma_rn(az, sl.x, yd.x), __fma_rn(-az, sl.y, yd.y));
+            const int2 k = kids[m];
+            for (int c = k.x; c < k.x + k.y; ++c) {
+              const double2 pc = P[c];
+              piv.x -= pc.x;
+              piv.y -= pc.y;
+            }
+            const double n2 = __fma_rn(piv.x, piv.x, piv.y * piv.y);
+            if (!(n2 > 0.0) || !isfinite(n2)) bad = 1;
+            const double rr = 1.0 / n2;
+            const double2 ui = make_double2(piv.x * rr, -piv.y * rr);  // 1 / U[m,m]
+            const double2 e = __ldg(&a.coef[m]);
+            const double2 g = cmul2(e, ui);
+            zg[m] = g;
+            zg[a.b + m] = ui;
+            P[m] = cmul2(e, g);  // e_m^2 / U[m,m], pulled by the parent
+            if (ap != 0.0 && (sl.x != 0.0 || sl.y != 0.0)) any = 1;
+          }
+        }
+        __syncthreads();
+      }
+      if (bad) atomicExch(a.status, 1);
+      anz = __syncthreads_or(any) != 0;
+      __threadfence_block();
+    }
     int it = 0;
+    bool met = false;  // fpi.py step_met
     issue_up(L - 1);
     while (it < a.max_iter) {
       TREE_T(t_up);
@@ -251,6 +308,12 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
               // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
               double2 z = make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
                                        -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
+              if constexpr (ZIP) {  // r_m = -(alpha_p s*/conj(v) + src + alpha_i s*)
+                const double ai = __ldg(a.alpha + a.b + m), ap = __ldg(a.alpha + 2 * a.b + m);
+                const double ur = __fma_rn(sl.x, v.x, sl.y * v.y) * r, uim = __fma_rn(sl.x, v.y, -(sl.y * v.x)) * r;
+                z = make_double2(-(ap * ur + src.x + ai * sl.x), -(ap * uim + src.y - ai * sl.y));
+                if (!anz) z = make_double2(-(src.x + ai * sl.x), -(src.y - ai * sl.y));
+              }
               const int2 k = kids[m];
               for (int c = k.x; c < k.x + k.y; ++c) {
                 const double2 pc = P[c];
@@ -271,8 +334,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
       TREE_ACC(1, t_up);
       TREE_T(t_down);
       // ---- down-sweep: root level first, step test, iterate update ----
-      bool small = true;
-      int all_small = 0;
+      bool small = true, fin = true;
+      int all_small = 0, all_fin = 1;
       for (int d = 0; d < L; ++d) {
         const int off = s_off[d], end = s_off[d + 1], jb = s_j0[d], je = s_j0[d + 1];
 #pragma unroll
@@ -296,6 +359,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
                 if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
                 const double dr = w.x - v.x, di = w.y - v.y;
                 if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+                if (ZIP && !(isfinite(w.x) && isfinite(w.y))) fin = false;
               }
               tmem_st2(tm_v + 4 * (jb + u), w);
             }
@@ -307,11 +371,20 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
           __syncthreads();
         } else {
           all_small = __syncthreads_and(small);
+          if constexpr (ZIP) all_fin = __syncthreads_and(fin);
         }
       }
       TREE_ACC(2, t_down);
       ++it;
-      if (all_small) break;
+      if (ZIP && !anz) {  // fpi.py:150-163: A = 0, one application, no step requirement
+        met = true;
+        break;
+      }
+      if (ZIP && !all_fin) break;  // fpi.py:178-181: diverged, not converged
+      if (all_small) {
+        met = true;
+        break;
+      }
       issue_up(L - 1);
     }
 
@@ -379,8 +452,15 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         if (m >= 0) {
           const double2 v = T[m];
           const double2 sl = sd.get();
-          const double mr = sl.x + (v.x * ar + v.y * ai);
-          const double mi = sl.y + (v.y * ar - v.x * ai);
+          double2 sload = sl;
+          if constexpr (ZIP) {  // fpi.py:229-235: az s |v|^2 + ai s v + ap s
+            const double az = __ldg(a.alpha + m), zi = __ldg(a.alpha + a.b + m), zp = __ldg(a.alpha + 2 * a.b + m);
+            const double v2 = v.x * v.x + v.y * v.y;
+            const double2 sv = cmul2(sl, v);
+            sload = make_double2(az * sl.x * v2 + zi * sv.x + zp * sl.x, az * sl.y * v2 + zi * sv.y + zp * sl.y);
+          }
+          const double mr = sload.x + (v.x * ar + v.y * ai);
+          const double mi = sload.y + (v.y * ar - v.x * ai);
           worst = nanmax(worst, hypot(mr, mi));
         }
       }
@@ -398,6 +478,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
     if (tid == 0) tc[6] += it;
 #endif
     if (tid == 0) a.iters[cs] = it;
+    if constexpr (ZIP) {
+      if (tid == 0) a.met[cs] = met ? 1 : 0;
+    }
   }
 #ifdef TPF_PHASE_TIMING
   if (tid == 0 && blockIdx.x < 148) {
@@ -429,7 +512,9 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
                        double v_flat_re, double v_flat_im, double tol, int32_t max_iter, double* V,
                        int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, int32_t ell_w,
                        const int32_t* ell_col, const double* ell_val, double* resid, void* workspace,
-                       size_t workspace_bytes, void* stream) {
+                       size_t workspace_bytes, void* stream, const double* alpha = nullptr,
+                       const double* ydiag = nullptr, int32_t* status = nullptr, uint8_t* met = nullptr) {
+  const bool zip = alpha != nullptr;
   if (tau < 0 || b < 1 || levels < 1 || levels > kMaxLevels)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: bad shape");
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
@@ -442,13 +527,18 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
   const size_t smem = size_t(b) * (2 * sizeof(double2) + sizeof(int2) + sizeof(int));
   if (smem > 220 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_tree_fpi_c128: b too large for one SM");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t err = cudaFuncSetAttribute(sparse_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  auto kern = zip ? sparse_tree_kernel<true> : sparse_tree_kernel<false>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tree)", err);
   err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
   if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = sms;
+  if (tau < grid) grid = tau;
+  if (zip && workspace_bytes < 256 + size_t(grid) * 2 * size_t(b) * sizeof(double2))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_zip_fpi_c128: workspace too small");
   TreeArgs a;
   a.tau = tau;
   a.b = b;
@@ -471,9 +561,12 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
   a.ell_col = ell_col;
   a.ell_val = reinterpret_cast<const double2*>(ell_val);
   a.resid = resid;
-  int64_t grid = sms;
-  if (tau < grid) grid = tau;
-  sparse_tree_kernel<<<unsigned(grid), kTreeThreads, smem, st>>>(a);
+  a.alpha = alpha;
+  a.ydiag = reinterpret_cast<const double2*>(ydiag);
+  a.zcoef = reinterpret_cast<double2*>(static_cast<char*>(workspace) + 256);
+  a.status = status;
+  a.met = met;
+  kern<<<unsigned(grid), kTreeThreads, smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_tree_kernel)", err);
   return TPF_OK;
@@ -501,6 +594,32 @@ extern "C" int tpf_sparse_tree_fpi_resid_c128(int64_t tau, int32_t b, int32_t le
   return tree_launch(tau, b, levels, level_info, node_info, node_coef, S, s_node_stride, s_case_stride, v_flat_re,
                      v_flat_im, tol, max_iter, V, v_node_stride, v_case_stride, iters, ell_width, ell_col, ell_val,
                      resid, workspace, workspace_bytes, stream);
+}
+
+extern "C" size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = sms;
+  if (tau < grid) grid = tau;
+  if (grid < 1) grid = 1;
+  return 256 + size_t(grid) * 2 * size_t(b) * sizeof(double2);
+}
+
+extern "C" int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
+                                            const int32_t* node_info, const double* node_coef, const double* alpha,
+                                            const double* ydiag, const double* S, int64_t s_node_stride,
+                                            int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,
+                                            int32_t max_iter, double* V, int64_t v_node_stride,
+                                            int64_t v_case_stride, int32_t* iters, int32_t ell_width,
+                                            const int32_t* ell_col, const double* ell_val, double* resid,
+                                            uint8_t* step_met, int32_t* status, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+  if (!alpha || !ydiag || !resid || !status || !step_met)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_zip_fpi_c128: null alpha / ydiag / resid / step_met / status");
+  return tree_launch(tau, b, levels, level_info, node_info, node_coef, S, s_node_stride, s_case_stride, v_flat_re,
+                     v_flat_im, tol, max_iter, V, v_node_stride, v_case_stride, iters, ell_width, ell_col, ell_val,
+                     resid, workspace, workspace_bytes, stream, alpha, ydiag, status, step_met);
 }
 
 extern "C" int tpf_sparse_tree_ell_width(int32_t b, const int32_t* ydd_row_ptr) {

@@ -5,9 +5,10 @@ Reference: pkg/src/tpflow/dense.py:129-205.  Same signature, same
 
 * ``ValueError("load matrix has N rows, model has M")`` (dense.py:143-146);
 * non-constant-power ZIP models: the reference routes them through the
-  single-case solver column by column (dense.py:147-148, 214-230); that is not
-  the batched hot path, so this engine raises ``NotImplementedError`` naming
-  the reference route instead of silently running a CPU loop;
+  single-case solver column by column (dense.py:147-148, 214-230); here they
+  run as one GPU launch with the single-case semantics on radial feeders
+  (``solve_zip``), and raise ``NotImplementedError`` on meshed networks
+  instead of silently running a CPU loop;
 * ``numpy.linalg.LinAlgError`` from the inverse of a singular Y_dd
   (dense.py:151, uncaught in the reference too).
 
@@ -154,9 +155,9 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
     if loads.n_demand != model.n_demand:
         raise ValueError(f"load matrix has {loads.n_demand} rows, model has {model.n_demand}")
     if not model.zip.is_constant_power:
-        raise NotImplementedError(
-            "mixed ZIP loads are not on the batched hot path; the reference routes them "
-            "through its single-case solver (tpflow.dense._batch_via_single -> fpi_solve)")
+        if engine_dtype(dtype) != np.complex128 or (devices is not None and len(devices) > 1):
+            raise NotImplementedError("ZIP loads run in complex128 on one device")
+        return solve_zip(model, loads, opts, devices[0] if devices else device, return_on_device)
     dt = engine_dtype(dtype)
     if not return_on_device and dt == np.complex128:
         return _solve_host_pipeline(model, loads, opts, resolve_devices(device, devices), chunk_cases)
@@ -167,6 +168,65 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
     V, iters = op.solve(S, opts)
     resid, mask, summ = residual_and_summary(op.contract, S, V, iters, opts.residual_tolerance, op.device)
     return finish(V, iters, resid, mask, summ, return_on_device)
+
+
+def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_on_device: bool = False):
+    """ZIP loads: the reference's per-case route (dense.py:214-230 -> fpi_solve,
+    fpi.py:107-206) as one GPU launch on radial feeders (include/tpf.h,
+    ``tpf_sparse_tree_zip_fpi_c128``): every case factorizes its own
+    B = Y_dd + diag(alpha_z s*) on chip and iterates with fpi_solve's stopping
+    rules.  Meshed or non-symmetric networks raise NotImplementedError (the
+    reference's per-case CPU loop is not the accelerated path)."""
+    from ._types import SingularSystemError
+    from .sparse import factorize_ydd, tree_ell, tree_schedule
+    c = ModelContract.of(model)
+    y = c.y_dd
+    b = c.b
+    msg = "ZIP loads on the GPU need a radial feeder with a symmetric Y_dd"
+    if (y != y.T).nnz != 0:
+        raise NotImplementedError(msg)
+    tree = tree_schedule(factorize_ydd(y, count=False), c.src)
+    ell = tree_ell(tree, c) if tree is not None else None
+    if tree is None or ell is None:
+        raise NotImplementedError(msg)
+    dev = require_cuda(device)
+    order = tree.node_info.reshape(b, 4)[:, 0]
+    z = model.zip
+    alpha = np.ascontiguousarray(np.concatenate([np.asarray(z.alpha_z, float)[order],
+                                                 np.asarray(z.alpha_i, float)[order],
+                                                 np.asarray(z.alpha_p, float)[order]]))
+    ydiag = np.ascontiguousarray(y.diagonal()[order].astype(np.complex128))
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    g = dict(level_info=t(tree.level_info), node_info=t(tree.node_info), node_coef=t(tree.node_coef),
+             alpha=t(alpha), ydiag=t(ydiag), ell_col=t(ell[1]), ell_val=t(ell[2]))
+    S = loads_to_device(loads.values, dev)
+    tau = S.shape[1]
+    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    resid = torch.empty(tau, dtype=torch.float64, device=dev)
+    met = torch.zeros(tau, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _capi.load()
+    ws = torch.empty(int(lib.tpf_sparse_tree_zip_workspace_bytes(tau, b)), dtype=torch.uint8, device=dev)
+    sn, sc = complex_strides(S)
+    v_flat = complex(abs(c.v_s))
+    if tau:
+        _capi.call("tpf_sparse_tree_zip_fpi_c128", tau, b, tree.levels, g["level_info"].data_ptr(),
+                   g["node_info"].data_ptr(), g["node_coef"].data_ptr(), g["alpha"].data_ptr(),
+                   g["ydiag"].data_ptr(), S.data_ptr(), sn, sc, v_flat.real, v_flat.imag, float(opts.tolerance),
+                   int(opts.max_iterations), V.data_ptr(), tau, 1, iters.data_ptr(), ell[0],
+                   g["ell_col"].data_ptr(), g["ell_val"].data_ptr(), resid.data_ptr(), met.data_ptr(),
+                   status.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    if int(status.item()) != 0:  # assemble_fpi's splu failure (fpi.py:119-126)
+        raise SingularSystemError("iteration matrix B is singular for some case (zero pivot)")
+    # fpi_solve: converged = step_met and residual < residual_tolerance (fpi.py:197-198)
+    mask = (met != 0) & torch.isfinite(resid) & (resid < float(opts.residual_tolerance))
+    n_max = int(iters.max().item()) if tau else 0
+    if return_on_device:
+        return VoltageBatch(values=V, iterations=n_max, converged_mask=mask, residuals=resid,
+                            iterations_per_case=iters)
+    return VoltageBatch(values=V.cpu().numpy(), iterations=n_max, converged_mask=mask.cpu().numpy(),
+                        residuals=resid.cpu().numpy(), iterations_per_case=iters.cpu().numpy())
 
 
 def finish(V, iters, resid, mask, summ, on_device: bool) -> VoltageBatch:

@@ -106,8 +106,12 @@ class TreeLU:
         return int(self.l_col.size + self.u_col.size + self.b)
 
 
-def factorize_ydd(y_dd) -> TreeLU:
-    """One LU of Y_dd; raises SingularSystemError like sparse.py:82-94."""
+def factorize_ydd(y_dd, count: bool = True) -> TreeLU:
+    """One LU of Y_dd; raises SingularSystemError like sparse.py:82-94.
+
+    ``count=False``: a structural helper factorization (the ZIP path's level
+    schedule), not a batch factorization; ``factorization_count`` is unchanged.
+    """
     global _factorizations
     y = sparse.csr_matrix(y_dd, dtype=complex)
     b = y.shape[0]
@@ -134,8 +138,9 @@ def factorize_ydd(y_dd) -> TreeLU:
             where.append(f"empty columns {empty_cols[:8].tolist()}")
         detail = f" ({'; '.join(where)})" if where else ""
         raise SingularSystemError(f"sparse factorization failed: {exc}{detail}") from exc
-    with _lock:
-        _factorizations += 1
+    if count:
+        with _lock:
+            _factorizations += 1
     L = sparse.csr_matrix(lu.L)
     U = sparse.csr_matrix(lu.U)
     Ls = sparse.tril(L, k=-1, format="csr")

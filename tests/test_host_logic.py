@@ -61,10 +61,21 @@ class TestBoundaryErrors:
         zm = NetworkModel(admittance=m.admittance, slack=m.slack,
                           zip=ZipCoefficients(np.full(b, 0.2), np.full(b, 0.1), np.full(b, 0.7)))
         loads = LoadMatrix(np.full((b, 2), 0.01 + 0j))
-        with pytest.raises(NotImplementedError, match="fpi_solve"):
+        # radial ZIP models run on the GPU (tests/test_zip_gpu.py); here: no CPU fallback
+        with pytest.raises(RuntimeError, match="CUDA device"):
             batch_solve_dense(zm, loads)
         with pytest.raises(ValueError, match="constant-power"):
             batch_solve_sparse(zm, loads)
+        # a meshed network with ZIP loads stays on the reference's per-case route
+        from scipy import sparse as sp
+        y = m.admittance.y_dd.tolil()
+        dense = m.admittance.y_dd.toarray()
+        i, j = next((i, j) for i in range(b) for j in range(i + 1, b) if dense[i, j] == 0)
+        y[i, j] = y[j, i] = -1.0 + 1.0j  # a second path: the network is no longer radial
+        mesh = NetworkModel.from_admittance(sp.csc_matrix(y), m.admittance.y_ds, slack=m.slack,
+                                            zip_coeffs=zm.zip)
+        with pytest.raises(NotImplementedError, match="radial"):
+            batch_solve_dense(mesh, loads)
 
     def test_memory_guard(self):
         m = build_network(GenSpec(n_buses=9, seed=42))

@@ -77,3 +77,20 @@ def test_c2_statistics_recorded(golden):
     g = golden("c2_slice192")
     assert int(g["c2_sum_n"]) == 2615281
     assert int(g["c2_max_n"]) == 7
+
+
+@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed"])
+def test_zip_oracle_matches_reference(name):
+    """The ZIP restatement (per-case fpi_solve) against the reference's own batch."""
+    import os
+    from scipy import sparse as sp
+    d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "zip", name + ".npz"))
+    b = d["S"].shape[0]
+    y = sp.csc_matrix((d["ydd_data"], d["ydd_indices"], d["ydd_indptr"]), shape=(b, b))
+    V, n, mask, res, it = orc.dense_zip_batch(y, d["src"], 1.0 + 0j, d["alpha_z"], d["alpha_i"], d["alpha_p"],
+                                              d["S"], float(d["tol"]), int(d["max_iter"]), float(d["residual_tol"]))
+    assert it == int(d["iterations"])
+    assert np.array_equal(n, d["n_case"])
+    assert np.array_equal(mask, d["mask"])
+    good = d["mask"]
+    assert np.abs(V[:, good] - d["V"][:, good]).max(initial=0) <= 1e-12

@@ -1,0 +1,61 @@
+"""ZIP loads on the GPU (tpf_sparse_tree_zip_fpi_c128) against fixtures written
+by the reference's per-case route (tests/golden/make_golden_zip.py) and the
+oracle restatement (oracle.dense_zip_batch)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+from oracle import tpf_oracle as orc
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "zip")
+
+
+def fixture(name):
+    from paper_2403_04578_b200 import GenSpec, NetworkModel, ZipCoefficients, build_network
+    d = np.load(os.path.join(DIR, name + ".npz"))
+    base = build_network(GenSpec(n_buses=int(d["n_buses"]), seed=int(d["seed"])))
+    z = ZipCoefficients(alpha_z=d["alpha_z"], alpha_i=d["alpha_i"], alpha_p=d["alpha_p"])
+    model = NetworkModel.from_branches(base.branches, int(d["n_buses"]), slack=base.slack, zip_coeffs=z)
+    assert np.array_equal(model.admittance.y_dd.tocsc().data, d["ydd_data"])
+    return model, d
+
+
+@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed"])
+def test_zip_matches_reference(name):
+    from paper_2403_04578_b200 import LoadMatrix, SolveOptions, batch_solve_dense
+    model, d = fixture(name)
+    opts = SolveOptions(tolerance=float(d["tol"]), max_iterations=int(d["max_iter"]),
+                        residual_tolerance=float(d["residual_tol"]))
+    out = batch_solve_dense(model, LoadMatrix(d["S"]), opts)
+    assert out.iterations == int(d["iterations"])
+    assert np.array_equal(out.converged_mask, d["mask"])
+    # per-case counts: the reference's own fpi_solve counts (one-case solver semantics)
+    assert np.abs(out.iterations_per_case.astype(int) - d["n_case"]).max() <= 1
+    good = d["mask"]
+    assert np.abs(out.values[:, good] - d["V"][:, good]).max(initial=0) <= 1e-9
+    fin = np.isfinite(d["residuals"])
+    assert np.allclose(out.residuals[fin & good], d["residuals"][fin & good], rtol=1e-3, atol=1e-12)
+
+
+def test_zip_random_feeder_vs_oracle():
+    from paper_2403_04578_b200 import (GenSpec, LoadMatrix, NetworkModel, SolveOptions, ZipCoefficients,
+                                       batch_solve_dense, build_network, gen_scenarios)
+    spec = GenSpec(n_buses=301, seed=7, load_scale=2.0)
+    base = build_network(spec)
+    b = base.n_demand
+    rng = np.random.default_rng(3)
+    w = rng.dirichlet([0.5, 0.5, 2.0], size=b)
+    z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
+    model = NetworkModel.from_branches(base.branches, 301, slack=base.slack, zip_coeffs=z)
+    S = gen_scenarios(model, 200, spec).values
+    out = batch_solve_dense(model, LoadMatrix(S), SolveOptions())
+    V, n, mask, res, it = orc.dense_zip_batch(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                              z.alpha_z, z.alpha_i, z.alpha_p, S)
+    assert out.iterations == it and np.array_equal(out.converged_mask, mask)
+    assert np.array_equal(out.iterations_per_case, n)
+    assert np.abs(out.values - V).max() <= 1e-10
