@@ -368,11 +368,23 @@ def run_ours():
                                 parallelism=f"tau-sharded x{world} (independent scenario batches)",
                                 **({"c4_full_1000_scenarios_s_extrapolated": 1000 * tau / value} if scenarios else {})),
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
-                    gpu_launches=(3 if method == "dense" else 2) * ARGS.steps,
+                    gpu_launches=launches_per_step(method, op, tau) * ARGS.steps,
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def launches_per_step(method, op, tau):
+    """Our kernels per timed step: dense = solve + residual + summary; sparse =
+    one tree launch per compact chunk (SparseOperator) + summary, or the
+    general kernel + residual + summary."""
+    if method == "dense":
+        return 3
+    from paper_2403_04578_b200.sparse import TREE_CHUNK
+    if op.tree is not None:
+        return (-(-tau // TREE_CHUNK) if tau > TREE_CHUNK else 1) + 1
+    return 3
 
 
 def executed_dense(b, sum_n, kms, peak_tf):

@@ -19,6 +19,7 @@
 // CTA = 512 threads (16 warps, 4 per TMEM lane quadrant, 128 columns each =
 // 16 slots), one CTA per SM (all 512 TMEM columns), persistent over cases.
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "tpf_common.cuh"
@@ -73,6 +74,7 @@ struct TreeArgs {
   double2* zcoef;
   int32_t* status;
   uint8_t* met;           // ZIP: 1 if the case stopped on the step test (or is a one-application case)
+  int prefetch;           // prefetch the next case's loads into L2 (TPF_TREE_PREFETCH=1; default off)
 };
 
 __device__ __forceinline__ double2 cfma_sub(double2 acc, double2 a, double2 x) {  // acc - a*x
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
         if (m >= 0) {
           const int64_t row = int64_t(__ldg(&a.info[m].x)) * a.s_node;
           sv[j] = __ldg(a.S + row + int64_t(cs) * a.s_case);
-          if (nx >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.S + row + int64_t(nx) * a.s_case));
+          if (nx >= 0 && a.prefetch) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.S + row + int64_t(nx) * a.s_case));
         }
       }
 #pragma unroll
@@ -566,6 +568,11 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
   a.zcoef = reinterpret_cast<double2*>(static_cast<char*>(workspace) + 256);
   a.status = status;
   a.met = met;
+  static const int pf = [] {
+    const char* e = getenv("TPF_TREE_PREFETCH");
+    return e ? atoi(e) : 0;  // off: measured neutral at 1 MB node stride, -10% at 8 MB (TLB reach)
+  }();
+  a.prefetch = pf;
   kern<<<unsigned(grid), kTreeThreads, smem, st>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_tree_kernel)", err);

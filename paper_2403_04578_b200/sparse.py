@@ -171,6 +171,7 @@ TREE_THREADS = 512      # CTA size of tpf_sparse_tree_fpi_c128
 TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
 TREE_LEVEL_SLOTS = 6    # slots of one depth level held in registers at a time
 TREE_MAX_ROOTS = 512    # root-level nodes (source injections kept in shared memory)
+TREE_CHUNK = 65536      # cases per compact chunk on long node-major batches (SparseOperator)
 TREE_MAX_NODES = 7800  # shared memory: sweep vector, child products, child ranges, parents: 44 B per node
 
 
@@ -359,6 +360,7 @@ class SparseOperator:
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
         self._csr = None
+        self._chunk = None
         self.tree = tree_schedule(f, self.contract.src) if use_tree else None
         if self.tree is not None:
             self.tree_dev = dict(level_info=t(self.tree.level_info), node_info=t(self.tree.node_info),
@@ -401,6 +403,8 @@ class SparseOperator:
         if self.tree is not None:
             if self._ws is None:
                 self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+            if tau > TREE_CHUNK and S.stride(1) == 1 and V.stride(1) == 1:
+                return self._solve_tree_chunked(S, opts, V, iters, resid)
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
             g = self.tree_dev
@@ -433,6 +437,29 @@ class SparseOperator:
                    stream_ptr(self.device))
         if resid is not None:
             self._residual(S, V, resid)
+        return V, iters
+
+    def _solve_tree_chunked(self, S, opts, V, iters, resid):
+        """Node-major batches longer than TREE_CHUNK cases: the tree kernel's
+        one-case-per-SM accesses stride a whole row of S / V per node; past a
+        few MB per row they miss the TLB (C3, 8.4 MB rows: 127 vs 105 us per
+        case per SM).  Each chunk is copied into compact buffers (rows of
+        TREE_CHUNK cases), solved, and copied back (tools/c3_chunk_probe.py:
+        450 -> 400 ms at full C3, copies included).  Bits are unchanged: every
+        case's arithmetic is independent of its position."""
+        b, tau = S.shape
+        ch = TREE_CHUNK
+        if self._chunk is None or self._chunk[0].shape != (b, ch) or self._chunk[0].dtype != S.dtype:
+            self._chunk = (torch.empty((b, ch), dtype=S.dtype, device=self.device),
+                           torch.empty((b, ch), dtype=S.dtype, device=self.device))
+        sc_buf, vc_buf = self._chunk
+        for lo in range(0, tau, ch):
+            hi = min(tau, lo + ch)
+            n = hi - lo
+            sc_buf[:, :n].copy_(S[:, lo:hi])
+            self.solve(sc_buf[:, :n], opts, V=vc_buf[:, :n], iters=iters[lo:hi],
+                       resid=None if resid is None else resid[lo:hi])
+            V[:, lo:hi].copy_(vc_buf[:, :n])
         return V, iters
 
     def _residual(self, S, V, resid):

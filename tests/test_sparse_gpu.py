@@ -177,3 +177,20 @@ def test_devices_split_bitwise_equal(golden, use_tree):
     assert np.array_equal(one.iterations_per_case, many.iterations_per_case)
     assert np.array_equal(one.residuals, many.residuals)
     assert one.iterations == many.iterations
+
+
+def test_tree_chunked_long_batches_bitwise(golden, monkeypatch):
+    """Long node-major batches are solved in compact chunks (SparseOperator): same bits."""
+    import torch
+    import paper_2403_04578_b200.sparse as sp
+    from paper_2403_04578_b200 import SparseOperator
+    g = golden("c1_slice512")
+    S = torch.from_numpy(np.ascontiguousarray(g.S)).cuda()
+    op = SparseOperator(g.model, "cuda:0")
+    tau = S.shape[1]
+    r1 = torch.empty(tau, dtype=torch.float64, device="cuda:0")
+    V1, it1 = op.solve(S, g.opts(), resid=r1)
+    monkeypatch.setattr(sp, "TREE_CHUNK", 100)
+    r2 = torch.empty(tau, dtype=torch.float64, device="cuda:0")
+    V2, it2 = op.solve(S, g.opts(), resid=r2)
+    assert torch.equal(V1, V2) and torch.equal(it1, it2) and torch.equal(r1, r2)
