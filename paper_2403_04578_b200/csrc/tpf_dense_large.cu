@@ -147,11 +147,16 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  double cr[MFR][NFR][2], ci[MFR][NFR][2];
+  // 3M complex products (Gauss, as in the b <= 104 kernel): per fragment pair
+  // P1 = sum ar br, P2 = sum ai bi, P3 = sum (ar + ai)(br + bi); re = P1 - P2,
+  // im = (P3 - P1) - P2 -- 3 DMMAs instead of 4, at MFR + NFR DADDs per k-step
+  double p1[MFR][NFR][2], p2[MFR][NFR][2], p3[MFR][NFR][2];
 #pragma unroll
   for (int i = 0; i < MFR; ++i)
 #pragma unroll
-    for (int j = 0; j < NFR; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < NFR; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) p1[i][j][e] = p2[i][j][e] = p3[i][j][e] = 0.0;
 
   const int nslabs = (b + TK - 1) / TK;
   load_slab(0, 0);
@@ -167,24 +172,39 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
       double2 af[MFR], bf[NFR];
-#pragma unroll
-      for (int i = 0; i < MFR; ++i) af[i] = As[stage][(ks * MFT + wm * MFR + i) * 32 + lane];
-#pragma unroll
-      for (int j = 0; j < NFR; ++j) bf[j] = Bs[stage][(ks * NF + wn * NFR + j) * 32 + lane];
+      double as[MFR], bs[NFR];
 #pragma unroll
       for (int i = 0; i < MFR; ++i) {
-        const double nui = neg_int(af[i].y);
+        af[i] = As[stage][(ks * MFT + wm * MFR + i) * 32 + lane];
+        as[i] = af[i].x + af[i].y;
+      }
+#pragma unroll
+      for (int j = 0; j < NFR; ++j) {
+        bf[j] = Bs[stage][(ks * NF + wn * NFR + j) * 32 + lane];
+        bs[j] = bf[j].x + bf[j].y;
+      }
+#pragma unroll
+      for (int i = 0; i < MFR; ++i) {
 #pragma unroll
         for (int j = 0; j < NFR; ++j) {
-          dmma884(cr[i][j][0], cr[i][j][1], af[i].x, bf[j].x);
-          dmma884(ci[i][j][0], ci[i][j][1], af[i].x, bf[j].y);
-          dmma884(cr[i][j][0], cr[i][j][1], nui, bf[j].y);
-          dmma884(ci[i][j][0], ci[i][j][1], af[i].y, bf[j].x);
+          dmma884(p1[i][j][0], p1[i][j][1], af[i].x, bf[j].x);
+          dmma884(p2[i][j][0], p2[i][j][1], af[i].y, bf[j].y);
+          dmma884(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
         }
       }
     }
     __syncthreads();
   }
+  double cr[MFR][NFR][2], ci[MFR][NFR][2];
+#pragma unroll
+  for (int i = 0; i < MFR; ++i)
+#pragma unroll
+    for (int j = 0; j < NFR; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        cr[i][j][e] = p1[i][j][e] - p2[i][j][e];
+        ci[i][j][e] = (p3[i][j][e] - p1[i][j][e]) - p2[i][j][e];
+      }
 
   // epilogue: V' = acc + W, step test against the (guarded) old iterate, in-place update
   const int* act = a.act[cur];
