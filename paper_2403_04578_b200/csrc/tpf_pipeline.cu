@@ -13,6 +13,7 @@
 // summary kernel and copy.  Pageable host buffers are page-locked in place for
 // the duration of the call (cudaHostRegister) so every copy is a DMA.
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "tpf_common.cuh"
@@ -43,6 +44,58 @@ struct HostPin {
     if (registered) cudaHostUnregister(ptr);
   }
 };
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes attr;
+  cudaError_t err = cudaPointerGetAttributes(&attr, p);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged;
+}
+
+// Page-locked staging for pageable loads: registering a caller's 841 MB array
+// costs ~75 ms per call (page pinning at ~11 GB/s), more than the whole C2
+// transfer; instead each chunk is copied by host threads into one of two
+// pinned staging buffers (grow-only, per calling thread) while the GPU works
+// on the previous chunk.
+struct Staging {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~Staging() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaHostAlloc(&p, n, cudaHostAllocPortable);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+};
+thread_local Staging g_staging;
+
+// Copy `rows` rows of `row_bytes` (source pitch src_pitch) into dst (pitch
+// dst_pitch) with a few host threads.
+void parallel_copy2d(char* dst, size_t dst_pitch, const char* src, size_t src_pitch, size_t row_bytes,
+                     int64_t rows) {
+  int nt = int(std::thread::hardware_concurrency());
+  if (nt > 16) nt = 16;
+  const size_t total = row_bytes * size_t(rows);
+  if (total < (size_t(8) << 20) || nt < 2) nt = 1;
+  if (int64_t(nt) > rows) nt = int(rows > 0 ? rows : 1);
+  auto work = [&](int w) {
+    const int64_t lo = rows * w / nt, hi = rows * (w + 1) / nt;
+    for (int64_t r = lo; r < hi; ++r) memcpy(dst + size_t(r) * dst_pitch, src + size_t(r) * src_pitch, row_bytes);
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < nt; ++w) pool.emplace_back(work, w);
+  work(0);
+  for (auto& t : pool) t.join();
+}
 
 // Layout of a b x tau complex host matrix: either node-major (case stride 1,
 // the reference LoadMatrix / VoltageBatch layout) or case-major (node stride 1).
@@ -186,7 +239,12 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
   if (!LS.ok(b, tau, s_node, s_case)) return set_error(TPF_ERR_INVALID, "host S must be node-major or case-major");
   if (!LV.ok(b, tau, v_node, v_case)) return set_error(TPF_ERR_INVALID, "host V must be node-major or case-major");
   HostPin pin_s, pin_v, pin_i, pin_r, pin_m;
-  pin_s.pin(S, LS.span_bytes(b, tau), true);
+  const bool stage_s = !host_pinned(S) && tau > chunk;  // one-chunk calls: registration is as cheap
+  if (stage_s) {
+    TPF_CK(g_staging.ensure(size_t(2) * size_t(chunk) * b * 16), "cudaHostAlloc(staging)");
+  } else {
+    pin_s.pin(S, LS.span_bytes(b, tau), true);
+  }
   pin_v.pin(V, LV.span_bytes(b, tau), false);
   if (iters) pin_i.pin(iters, size_t(tau) * 4, false);
   if (resid) pin_r.pin(resid, size_t(tau) * 8, false);
@@ -226,7 +284,26 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     const int k = int(c & 1);
     const int64_t lo = c * chunk, n = (tau - lo < chunk) ? tau - lo : chunk;
     if (c >= 2) cudaStreamWaitEvent(sin, ss.comp_done[k], 0);
-    TPF_CK(copy_chunk(true, LS, const_cast<double*>(S), d_S[k].as<double>(), b, lo, n, chunk, sin), "H2D(S chunk)");
+    if (stage_s) {
+      // staging slot k was last read by the H2D of chunk c - 2
+      if (c >= 2) TPF_CK(cudaEventSynchronize(ss.in_done[k]), "staging reuse");
+      char* stg = static_cast<char*>(g_staging.p) + size_t(k) * size_t(chunk) * b * 16;
+      const char* hs = reinterpret_cast<const char*>(S);
+      if (LS.case_contig) {  // b rows of n cases -> [b][chunk] pitch chunk
+        parallel_copy2d(stg, size_t(chunk) * 16, hs + size_t(lo) * 16, size_t(LS.ld) * 16, size_t(n) * 16, b);
+        TPF_CK(cudaMemcpy2DAsync(d_S[k].as<double>(), size_t(chunk) * 16, stg, size_t(chunk) * 16, size_t(n) * 16,
+                                 size_t(b), cudaMemcpyHostToDevice, sin),
+               "H2D(S chunk)");
+      } else {  // n cases of b nodes -> [n][b]
+        parallel_copy2d(stg, size_t(b) * 16, hs + size_t(lo) * size_t(LS.ld) * 16, size_t(LS.ld) * 16,
+                        size_t(b) * 16, n);
+        TPF_CK(cudaMemcpyAsync(d_S[k].as<double>(), stg, size_t(n) * b * 16, cudaMemcpyHostToDevice, sin),
+               "H2D(S chunk)");
+      }
+    } else {
+      TPF_CK(copy_chunk(true, LS, const_cast<double*>(S), d_S[k].as<double>(), b, lo, n, chunk, sin),
+             "H2D(S chunk)");
+    }
     cudaEventRecord(ss.in_done[k], sin);
     cudaStreamWaitEvent(scomp, ss.in_done[k], 0);
     if (c >= 2) cudaStreamWaitEvent(scomp, ss.out_done[k], 0);

@@ -320,3 +320,18 @@ def test_devices_split_bitwise_equal(golden, devs):
     # a pageable F-order input takes the same route
     many_f = batch_solve_dense(g.model, LoadMatrix(np.asfortranarray(g.S)), g.opts(), devices=devs)
     assert np.array_equal(one.values, many_f.values)
+
+
+@pytest.mark.parametrize("order", ["C", "F"])
+def test_pageable_staging_matches_pinned(golden, order):
+    """Pageable loads go through pinned staging chunk by chunk: same bits as pinned input."""
+    import torch
+    from paper_2403_04578_b200 import LoadMatrix, batch_solve_dense
+    g = golden("c1_slice512")
+    S = np.array(g.S, order=order)
+    pinned = torch.from_numpy(np.ascontiguousarray(g.S)).pin_memory().numpy()
+    a = batch_solve_dense(g.model, LoadMatrix(S), g.opts(), chunk_cases=64)        # staged (pageable)
+    b = batch_solve_dense(g.model, LoadMatrix(pinned), g.opts(), chunk_cases=64)   # direct DMA
+    assert np.array_equal(a.values, b.values)
+    assert np.array_equal(a.iterations_per_case, b.iterations_per_case)
+    assert np.array_equal(a.residuals, b.residuals)
