@@ -19,8 +19,18 @@
 //   * mbarriers (32 arrivals, one per lane) order the hand-offs, with
 //     tcgen05 fences around them;
 //   * K^T stays in shared memory in B-fragment order (one LDS.128 per
-//     fragment); the GEMM issues, per k-step, the 26 DMMAs that do not depend
-//     on each other before the 26 that accumulate onto them.
+//     fragment).
+//
+// Default variant (M3 = true): the complex GEMM is done with 3 real DMMAs per
+// block-product (Gauss: P1 = Ur Kr, P2 = Ui Ki, P3 = (Ur+Ui)(Kr+Ki)), Kr+Ki
+// staged in shared memory for the node blocks that fit, and the EW warp of a
+// group computes the last node blocks of its own group's GEMM right after
+// handing U over, so two DMMA streams feed each SMSP's FP64 tensor pipe.
+// The EW arithmetic avoids FP64 instructions where it exactly can (every
+// scalar FP64 instruction on the SMSP stalls the DMMA stream ~5-9 cycles):
+// Newton reciprocal, integer-bracketed step test and zero guard.
+// TPF_WS_4M=1 selects the 4-DMMA single-stream variant (bitwise equal to the
+// pair/solo kernels), TPF_WS_SPLIT=2 the two-DMMA-warp 4M variant.
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -881,11 +891,11 @@ extern "C" int tpf_debug_ws_phase_cycles(long long* out) {
 }
 #endif
 
-// Default: one DMMA warp per SMSP (12 warps).  TPF_WS_SPLIT=2 selects two DMMA
-// warps per SMSP sharing each GEMM (16 warps); measured slower on C2 (8.17 vs
-// 7.38 ms): the elementwise warps then cannot refill U fast enough.
-// Default: the 3M GEMM (3 DMMAs per complex block-product).  TPF_WS_4M=1
-// selects the 4-DMMA GEMM, bitwise equal to the pairs/solo kernels.
+// Variants (chosen once per process): default 3M GEMM with the EW warps taking
+// TPF_WS_NE node blocks (C2: 6.25 ms); TPF_WS_4M=1 the 4-DMMA GEMM on one DMMA
+// warp per SMSP (7.43 ms, bitwise equal to the pair/solo kernels);
+// TPF_WS_SPLIT=2 two 4M DMMA warps per SMSP (8.17 ms: the EW warps cannot
+// refill U fast enough).
 template <int NB, int KS>
 static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   static const int split = [] {
@@ -899,7 +909,8 @@ static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   if constexpr (NB >= 2) {
     if (split == 2) return ws::launch<NB, KS, 2, false>(a, st, sms);
   }
-  // node blocks of the GEMM done by the elementwise warps (TPF_WS_NE; default 5 at b in (96, 104], else b/8 - 4)
+  // node blocks of the GEMM done by the elementwise warps (TPF_WS_NE: default 5 at 13 node blocks,
+  // otherwise min(4, blocks - 6) so the EW blocks lie past the 6 scratch blocks)
   static const int ne = [] {
     const char* e = getenv("TPF_WS_NE");
     return e ? atoi(e) : 5;
