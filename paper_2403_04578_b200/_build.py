@@ -47,16 +47,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs_dir = os.path.join(PKG, "build")
     os.makedirs(objs_dir, exist_ok=True)
-    objs = []
-    log = []
-    for src in sources():
+    # translation units compile in parallel (the warp-specialised dense file,
+    # with its template instantiations, dominates)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = os.path.join(objs_dir, os.path.basename(src) + ".o")
         cmd = [nvcc(), "-c", src, "-o", obj, "-I", os.path.join(ROOT, "include")] + NVCC_FLAGS
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
-        objs.append(obj)
+        return obj, r.stdout + r.stderr
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as pool:
+        done = list(pool.map(compile_one, srcs))
+    objs = [o for o, _ in done]
+    log = [t for _, t in done]
     tmp = LIB + ".tmp"
     cmd = [nvcc(), "-shared", "-o", tmp] + objs + ["-gencode", "arch=compute_100a,code=sm_100a",
                                                   "-Xcompiler", "-fPIC", "-lcudart"]
