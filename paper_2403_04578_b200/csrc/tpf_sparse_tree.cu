@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
               piv.y -= pc.y;
             }
             const double n2 = __fma_rn(piv.x, piv.x, piv.y * piv.y);
-            if (!(n2 > 0.0) || !isfinite(n2)) bad = 1;
+            if (!(n2 > 0.0) || !isfinite(n2)) bad = 1;  // splu: "Factor is exactly singular" (also for NaN)
             const double rr = 1.0 / n2;
             const double2 ui = make_double2(piv.x * rr, -piv.y * rr);  // 1 / U[m,m]
             const double2 e = __ldg(&a.coef[m]);

@@ -222,7 +222,7 @@ def test_ws_kernel_full_c2_counts():
     assert (V1 - V2).abs().max().item() <= 1e-13
 
 
-@pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 64, 96, 100, 101, 104, 105, 128])
+@pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 50, 56, 64, 72, 80, 88, 96, 100, 101, 104, 105, 128])
 def test_feeder_sizes_across_kernel_boundaries(b):
     """Every node-block count of the shared-memory kernels (b <= 104) and the
     switch to the large-b kernel (b = 105): counts exact vs the oracle."""

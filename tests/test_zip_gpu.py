@@ -59,3 +59,29 @@ def test_zip_random_feeder_vs_oracle():
     assert out.iterations == it and np.array_equal(out.converged_mask, mask)
     assert np.array_equal(out.iterations_per_case, n)
     assert np.abs(out.values - V).max() <= 1e-10
+
+
+@pytest.mark.parametrize("n_buses", [2, 3, 40])
+def test_zip_small_feeders_nan_and_empty(n_buses):
+    """Edge cases: b = 1 and 2, empty batch, and a NaN load -- which makes the
+    reference's splu of that case's B fail ("Factor is exactly singular" ->
+    SingularSystemError for the whole batch), so it raises here too."""
+    from paper_2403_04578_b200 import (GenSpec, LoadMatrix, NetworkModel, SingularSystemError, SolveOptions,
+                                       ZipCoefficients, batch_solve_dense, build_network, gen_scenarios)
+    spec = GenSpec(n_buses=n_buses, seed=5)
+    base = build_network(spec)
+    b = base.n_demand
+    w = np.random.default_rng(n_buses).dirichlet([1.0, 1.0, 1.0], size=b)
+    z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
+    model = NetworkModel.from_branches(base.branches, n_buses, slack=base.slack, zip_coeffs=z)
+    S = gen_scenarios(model, 30, spec).values.copy()
+    out = batch_solve_dense(model, LoadMatrix(S), SolveOptions())
+    V, n, mask, res, it = orc.dense_zip_batch(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                              z.alpha_z, z.alpha_i, z.alpha_p, S)
+    assert np.array_equal(out.iterations_per_case, n) and np.array_equal(out.converged_mask, mask)
+    assert np.abs(out.values - V).max() <= 1e-10
+    empty = batch_solve_dense(model, LoadMatrix(np.zeros((b, 0), dtype=complex)), SolveOptions())
+    assert empty.values.shape == (b, 0) and empty.iterations == 0
+    S[0, 4] = np.nan
+    with pytest.raises(SingularSystemError):
+        batch_solve_dense(model, LoadMatrix(S), SolveOptions())
