@@ -481,6 +481,7 @@ __device__ __forceinline__ void ew_warp(const Args& a, Shared& sh, double2* stag
       // this warp's share of the group's GEMM: node blocks [NM, NB)
       double v[NE > 0 ? NE : 1][4];
       pass3<KS, NM, NE, NKS>(uv, v, k_sm + lane, ks_sm + lane, w_re, w_sum, qq);
+      pc.mark(1);  // (timing build) the EW warp's GEMM share
       tmem_fence_before();
       mbar_arrive(&sh.ew_u[q][g]);  // done reading U
       mbar_wait(&sh.full_v[q][g], par);

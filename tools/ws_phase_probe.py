@@ -29,6 +29,7 @@ mma = b[:, 0:4].reshape(-1, 8); ew = b[:, 4:12].reshape(-1, 8)
 print("MMA: rounds %.0f, wait-U %.1f%%, gemm %.1f%%, per-round gemm %.0f clk wait %.0f clk, DMMA/round %d" % (
     mma[:, 6].mean(), 100 * mma[:, 0].mean() / mma[:, 7].mean(), 100 * mma[:, 1].mean() / mma[:, 7].mean(),
     mma[:, 1].mean() / mma[:, 6].mean(), mma[:, 0].mean() / mma[:, 6].mean(), 13 * 25 * 3))
+print("EW GEMM share: %.0f clk per round (%.1f%%)" % (ew[:, 1].mean() / ew[:, 6].mean(), 100 * ew[:, 1].mean() / ew[:, 7].mean()))
 names = ["U round", "wait V'", "test", "retire/refill"]
 print("EW: rounds %.0f" % ew[:, 6].mean(), " ".join("%s %.0f clk (%.1f%%)" % (n, ew[:, 2 + i].mean() / ew[:, 6].mean(),
       100 * ew[:, 2 + i].mean() / ew[:, 7].mean()) for i, n in enumerate(names)))
