@@ -20,6 +20,7 @@ independent of any partitioning, like the reference's, test_dense.py:96-102).
 
 from __future__ import annotations
 
+import threading
 from collections import OrderedDict
 
 import numpy as np
@@ -36,6 +37,7 @@ __all__ = ["batch_solve_dense", "DenseOperator"]
 
 _KW_CACHE: "OrderedDict[bytes, tuple[np.ndarray, np.ndarray]]" = OrderedDict()
 _KW_CACHE_MAX = 8
+_KW_LOCK = threading.Lock()
 
 
 def dense_kw(contract: ModelContract) -> tuple[np.ndarray, np.ndarray]:
@@ -47,17 +49,19 @@ def dense_kw(contract: ModelContract) -> tuple[np.ndarray, np.ndarray]:
     then skip the O(b^3) host inverse.
     """
     key = contract.fingerprint()
-    hit = _KW_CACHE.get(key)
-    if hit is not None:
-        _KW_CACHE.move_to_end(key)
-        return hit
+    with _KW_LOCK:
+        hit = _KW_CACHE.get(key)
+        if hit is not None:
+            _KW_CACHE.move_to_end(key)
+            return hit
     K = np.ascontiguousarray(-np.linalg.inv(contract.y_dd.toarray()))  # dense.py:151
     W = np.ascontiguousarray(K @ contract.src)                          # dense.py:152
     K.setflags(write=False)
     W.setflags(write=False)
-    _KW_CACHE[key] = (K, W)
-    while len(_KW_CACHE) > _KW_CACHE_MAX:
-        _KW_CACHE.popitem(last=False)
+    with _KW_LOCK:
+        _KW_CACHE[key] = (K, W)
+        while len(_KW_CACHE) > _KW_CACHE_MAX:
+            _KW_CACHE.popitem(last=False)
     return K, W
 
 
