@@ -150,7 +150,7 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
  *               [2*b + m] 1/U[m,m], [3*b + m] src (symmetric Y_dd; src nonzero only at the
  *               root level, at most 512 root-level nodes, at most 6 slots
  *               (ceil(level size / 512)) per level)
- * Limits: b <= 7,800 and sum over levels of ceil(n_level/512) <=
+ * Limits: b <= 5,120 (44 B of shared memory per node) and sum over levels of ceil(n_level/512) <=
  * tpf_sparse_tree_max_slots() (16); otherwise use tpf_sparse_fpi_c128.
  *   workspace >= 256 device bytes                                          */
 int tpf_sparse_tree_max_slots(void);

@@ -172,7 +172,7 @@ TREE_MAX_SLOTS = 16     # TMEM slots per thread (include/tpf.h)
 TREE_LEVEL_SLOTS = 6    # slots of one depth level held in registers at a time
 TREE_MAX_ROOTS = 512    # root-level nodes (source injections kept in shared memory)
 TREE_CHUNK = 65536      # cases per compact chunk on long node-major batches (SparseOperator)
-TREE_MAX_NODES = 7800  # shared memory: sweep vector, child products, child ranges, parents: 44 B per node
+TREE_MAX_NODES = 220 * 1024 // 44  # 5,120: sweep vector, child products, child ranges, parents: 44 B per node
 
 
 @dataclass

@@ -194,3 +194,14 @@ def test_tree_chunked_long_batches_bitwise(golden, monkeypatch):
     r2 = torch.empty(tau, dtype=torch.float64, device="cuda:0")
     V2, it2 = op.solve(S, g.opts(), resid=r2)
     assert torch.equal(V1, V2) and torch.equal(it1, it2) and torch.equal(r1, r2)
+
+
+def test_feeder_beyond_tree_kernel_limits_uses_general_kernel():
+    """b > 5,120 does not fit the tree kernel's shared memory: the general CSR kernel runs instead."""
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios, batch_solve_sparse, SparseOperator
+    spec = GenSpec(n_buses=5301, seed=1)
+    model = build_network(spec)
+    assert SparseOperator(model, "cuda:0").tree is None
+    loads = gen_scenarios(model, 64, spec)
+    out = batch_solve_sparse(model, loads)
+    assert out.converged_mask.all() and 3 <= out.iterations <= 10
