@@ -227,3 +227,27 @@ def test_engine_dtype_validation():
     assert engine_dtype("complex64") == np.complex64
     with pytest.raises(ValueError):
         engine_dtype(np.float32)
+
+
+def test_reference_model_objects_are_accepted_as_is():
+    """A real tpflow.NetworkModel reduces to the same hot-path contract (skipped where the
+    reference is not importable, e.g. on the GPU box)."""
+    import os
+    import sys
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present")
+    sys.path.insert(0, ref)
+    try:
+        import tpflow
+    except Exception:  # pragma: no cover
+        pytest.skip("reference not importable")
+    finally:
+        sys.path.remove(ref)
+    from paper_2403_04578_b200._device import ModelContract
+    spec_r = tpflow.GenSpec(n_buses=30, seed=3)
+    mine = ModelContract.of(build_network(GenSpec(n_buses=30, seed=3)))
+    theirs = ModelContract.of(tpflow.build_network(spec_r))
+    assert (mine.y_dd != theirs.y_dd).nnz == 0
+    assert np.array_equal(mine.src, theirs.src) and mine.v_s == theirs.v_s
+    assert theirs.constant_power
