@@ -238,12 +238,15 @@ def test_reference_model_objects_are_accepted_as_is():
     if not os.path.isdir(ref):
         pytest.skip("reference not present")
     sys.path.insert(0, ref)
+    old = sys.dont_write_bytecode
+    sys.dont_write_bytecode = True  # never write into the read-only reference tree
     try:
         import tpflow
     except Exception:  # pragma: no cover
         pytest.skip("reference not importable")
     finally:
         sys.path.remove(ref)
+        sys.dont_write_bytecode = old
     from paper_2403_04578_b200._device import ModelContract
     spec_r = tpflow.GenSpec(n_buses=30, seed=3)
     mine = ModelContract.of(build_network(GenSpec(n_buses=30, seed=3)))
