@@ -186,13 +186,15 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     c = ModelContract.of(model)
     y = c.y_dd
     b = c.b
-    msg = "ZIP loads on the GPU need a radial feeder with a symmetric Y_dd"
     if (y != y.T).nnz != 0:
-        raise NotImplementedError(msg)
+        raise NotImplementedError("ZIP loads on the GPU need a radial feeder with a symmetric Y_dd")
     tree = tree_schedule(factorize_ydd(y, count=False), c.src)
     ell = tree_ell(tree, c) if tree is not None else None
     if tree is None or ell is None:
-        raise NotImplementedError(msg)
+        raise NotImplementedError(
+            "ZIP loads on the GPU need a radial feeder that fits the tree kernel (<= 5,120 nodes, "
+            "<= 64 depth levels, <= 16 slots of 512 nodes); meshed or deeper networks take the "
+            "reference's per-case route (tpflow.dense._batch_via_single)")
     dev = require_cuda(device)
     order = tree.node_info.reshape(b, 4)[:, 0]
     z = model.zip

@@ -74,7 +74,7 @@ class TestBoundaryErrors:
         y[i, j] = y[j, i] = -1.0 + 1.0j  # a second path: the network is no longer radial
         mesh = NetworkModel.from_admittance(sp.csc_matrix(y), m.admittance.y_ds, slack=m.slack,
                                             zip_coeffs=zm.zip)
-        with pytest.raises(NotImplementedError, match="radial"):
+        with pytest.raises(NotImplementedError, match="radial feeder"):
             batch_solve_dense(mesh, loads)
 
     def test_memory_guard(self):
