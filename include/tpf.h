@@ -189,6 +189,20 @@ int tpf_sparse_tree_max_ell_width(void);
  * stopped on the step test (or was a one-application case); *status = 1
  * if some case's B had a zero pivot (SingularSystemError in the reference).
  * workspace >= tpf_sparse_tree_zip_workspace_bytes(tau, b).              */
+/* The same ZIP route for radial feeders the tree kernel does not take (deep,
+ * wide or > 5,120 nodes): one thread per case, nodes in leaf-first order
+ * (orig = original node of position k, parent = position of k's parent or
+ * -1, e = Y[k, parent], ydiag, alpha [3][b], src all in that order); the
+ * residual sums Y v over the tree edges.  workspace >=
+ * tpf_sparse_zip_chain_workspace_bytes(tau, b) (64 B per node and case). */
+size_t tpf_sparse_zip_chain_workspace_bytes(int64_t tau, int32_t b);
+int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* orig, const int32_t* parent,
+                              const double* e, const double* ydiag, const double* alpha, const double* src,
+                              const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                              double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                              double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                              double* resid, uint8_t* step_met, int32_t* status,
+                              void* workspace, size_t workspace_bytes, void* stream);
 size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b);
 int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels,
                                  const int32_t* level_info, const int32_t* node_info, const double* node_coef,

@@ -175,3 +175,233 @@ extern "C" int tpf_sparse_fpi_c128(int64_t tau, int32_t b, const double* S, int6
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_fpi_kernel)", err);
   return TPF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// ZIP loads on radial feeders of any depth / size (the fallback of the tree
+// kernel's ZIP mode): one thread per case, nodes in leaf-first order.  Per
+// case the tree LU of B = Y_dd + diag(alpha_z s*) (no fill: U[k,k] = B[k,k] -
+// sum_c e_c^2 / U[c,c], g_k = e_k / U[k,k]) and fpi_solve's iteration
+// (fpi.py:107-206): B v' = -(alpha_p s*/conj(v) + src + alpha_i s*), one
+// application when alpha_p s = 0, stop on a non-finite iterate; the ZIP
+// residual (fpi.py:209-240) summed over the tree edges.  Scratch: four
+// node-major b x tau complex arrays (pivots/sweep, g, 1/U, Y v).
+namespace tpf {
+namespace {
+
+struct ZipChainArgs {
+  int64_t tau;
+  int b;
+  const double2* S;
+  int64_t s_node, s_case;   // original node order
+  const int32_t* orig;      // leaf-first position k -> original node
+  const int32_t* parent;    // position of k's parent, -1 at roots
+  const double2* e;         // Y[k, parent(k)] (symmetric)
+  const double2* ydiag;     // Y[k, k]
+  const double* alpha;      // [3][b] alpha_z, alpha_i, alpha_p (leaf-first order)
+  const double2* src;       // source injection (leaf-first order)
+  double2 v_flat;
+  double tol2;
+  int max_iter;
+  double2* V;
+  int64_t v_node, v_case;   // original node order
+  int32_t* iters;
+  double* resid;
+  uint8_t* met;
+  int32_t* status;
+  double2 *Z, *G, *UI, *A;  // scratch, [b][tau]
+};
+
+__device__ __forceinline__ double2 cmulz(double2 a, double2 x) {
+  return make_double2(__fma_rn(a.x, x.x, -(a.y * x.y)), __fma_rn(a.x, x.y, a.y * x.x));
+}
+
+__global__ void __launch_bounds__(128) sparse_zip_chain_kernel(const ZipChainArgs a) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= a.tau) return;
+  const int b = a.b;
+  const int64_t t = a.tau;
+  auto Sk = [&](int k) { return a.S[int64_t(__ldg(a.orig + k)) * a.s_node + j * a.s_case]; };
+  auto Vk = [&](int k) -> double2& { return a.V[int64_t(__ldg(a.orig + k)) * a.v_node + j * a.v_case]; };
+  // per-case factorization, leaf-first (children before parents)
+  bool any = false, bad = false;
+  for (int k = 0; k < b; ++k) {
+    const double2 s = Sk(k);
+    const double az = __ldg(a.alpha + k), ap = __ldg(a.alpha + 2 * b + k);
+    const double2 yd = __ldg(a.ydiag + k);
+    a.Z[k * t + j] = make_double2(__fma_rn(az, s.x, yd.x), __fma_rn(-az, s.y, yd.y));
+    if (ap != 0.0 && (s.x != 0.0 || s.y != 0.0)) any = true;
+  }
+  for (int k = 0; k < b; ++k) {
+    const double2 piv = a.Z[k * t + j];
+    const double n2 = __fma_rn(piv.x, piv.x, piv.y * piv.y);
+    if (!(n2 > 0.0) || !isfinite(n2)) bad = true;
+    const double rr = 1.0 / n2;
+    const double2 ui = make_double2(piv.x * rr, -piv.y * rr);
+    const double2 e = __ldg(a.e + k);
+    const double2 g = cmulz(e, ui);
+    a.UI[k * t + j] = ui;
+    a.G[k * t + j] = g;
+    const int p = __ldg(a.parent + k);
+    if (p >= 0) {
+      const double2 eg = cmulz(e, g);
+      double2 pp = a.Z[p * t + j];
+      pp.x -= eg.x;
+      pp.y -= eg.y;
+      a.Z[p * t + j] = pp;
+    }
+  }
+  if (bad) atomicExch(a.status, 1);
+  for (int k = 0; k < b; ++k) Vk(k) = a.v_flat;
+  int n = 0;
+  bool met = false;
+  while (n < a.max_iter) {
+    // right-hand sides, then the up-sweep (leaf-first): Z[p] -= g_k z_k
+    for (int k = 0; k < b; ++k) {
+      double2 v = Vk(k);
+      double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+      if (m2 < kZeroGuard2) {
+        v = make_double2(kZeroGuard, 0.0);
+        m2 = kZeroGuard * kZeroGuard;
+      }
+      const double r = 1.0 / m2;
+      const double2 s = Sk(k);
+      const double ai = __ldg(a.alpha + b + k), ap = __ldg(a.alpha + 2 * b + k);
+      const double2 c = __ldg(a.src + k);
+      const double ur = __fma_rn(s.x, v.x, s.y * v.y) * r, uim = __fma_rn(s.x, v.y, -(s.y * v.x)) * r;
+      a.Z[k * t + j] = any ? make_double2(-(ap * ur + c.x + ai * s.x), -(ap * uim + c.y - ai * s.y))
+                           : make_double2(-(c.x + ai * s.x), -(c.y - ai * s.y));
+    }
+    for (int k = 0; k < b; ++k) {
+      const int p = __ldg(a.parent + k);
+      if (p >= 0) {
+        const double2 gz = cmulz(a.G[k * t + j], a.Z[k * t + j]);
+        double2 zp = a.Z[p * t + j];
+        zp.x -= gz.x;
+        zp.y -= gz.y;
+        a.Z[p * t + j] = zp;
+      }
+    }
+    // down-sweep (parents first): w_k = z_k / U[k,k] - g_k w_parent; step test, update
+    bool small = true, fin = true;
+    for (int k = b - 1; k >= 0; --k) {
+      double2 w = cmulz(a.Z[k * t + j], a.UI[k * t + j]);
+      const int p = __ldg(a.parent + k);
+      if (p >= 0) {
+        const double2 gw = cmulz(a.G[k * t + j], a.Z[p * t + j]);
+        w.x -= gw.x;
+        w.y -= gw.y;
+      }
+      a.Z[k * t + j] = w;
+      double2& vk = Vk(k);
+      double2 v = vk;
+      if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+      const double dr = w.x - v.x, di = w.y - v.y;
+      if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;
+      if (!(isfinite(w.x) && isfinite(w.y))) fin = false;
+      vk = w;
+    }
+    ++n;
+    if (!any) {
+      met = true;
+      break;
+    }
+    if (!fin) break;
+    if (small) {
+      met = true;
+      break;
+    }
+  }
+  // ZIP residual: max_k |az s |v|^2 + ai s v + ap s + v conj(src + (Y v)_k)|
+  for (int k = 0; k < b; ++k) {
+    const double2 v = Vk(k);
+    a.A[k * t + j] = cmulz(__ldg(a.ydiag + k), v);
+  }
+  for (int k = 0; k < b; ++k) {
+    const int p = __ldg(a.parent + k);
+    if (p >= 0) {
+      const double2 e = __ldg(a.e + k);
+      const double2 ep = cmulz(e, Vk(p)), ek = cmulz(e, Vk(k));
+      double2 x = a.A[k * t + j];
+      x.x += ep.x;
+      x.y += ep.y;
+      a.A[k * t + j] = x;
+      double2 y = a.A[p * t + j];
+      y.x += ek.x;
+      y.y += ek.y;
+      a.A[p * t + j] = y;
+    }
+  }
+  double worst = 0.0;
+  for (int k = 0; k < b; ++k) {
+    const double2 v = Vk(k), s = Sk(k), c = __ldg(a.src + k), yv = a.A[k * t + j];
+    const double az = __ldg(a.alpha + k), zi = __ldg(a.alpha + b + k), zp = __ldg(a.alpha + 2 * b + k);
+    const double v2 = v.x * v.x + v.y * v.y;
+    const double2 sv = cmulz(s, v);
+    const double lr = az * s.x * v2 + zi * sv.x + zp * s.x, li = az * s.y * v2 + zi * sv.y + zp * s.y;
+    const double ar = c.x + yv.x, aim = c.y + yv.y;  // a = src + Y v
+    const double mr = lr + (v.x * ar + v.y * aim), mi = li + (v.y * ar - v.x * aim);
+    worst = nanmax(worst, hypot(mr, mi));
+  }
+  a.iters[j] = n;
+  a.resid[j] = worst;
+  a.met[j] = met ? 1 : 0;
+}
+
+}  // namespace
+}  // namespace tpf
+
+extern "C" size_t tpf_sparse_zip_chain_workspace_bytes(int64_t tau, int32_t b) {
+  return size_t(4) * size_t(tau) * size_t(b) * 16 + 256;
+}
+
+extern "C" int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* orig, const int32_t* parent,
+                                         const double* e, const double* ydiag, const double* alpha,
+                                         const double* src, const double* S, int64_t s_node_stride,
+                                         int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,
+                                         int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                         int32_t* iters, double* resid, uint8_t* step_met, int32_t* status,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_chain_c128: need tau >= 0, b >= 1");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!orig || !parent || !e || !ydiag || !alpha || !src || !S || !V || !iters || !resid || !step_met || !status ||
+      !workspace)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_chain_c128: null pointer");
+  if (workspace_bytes < tpf_sparse_zip_chain_workspace_bytes(tau, b))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_chain_c128: workspace too small");
+  ZipChainArgs a;
+  a.tau = tau;
+  a.b = b;
+  a.S = reinterpret_cast<const double2*>(S);
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.orig = orig;
+  a.parent = parent;
+  a.e = reinterpret_cast<const double2*>(e);
+  a.ydiag = reinterpret_cast<const double2*>(ydiag);
+  a.alpha = alpha;
+  a.src = reinterpret_cast<const double2*>(src);
+  a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = reinterpret_cast<double2*>(V);
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  a.resid = resid;
+  a.met = step_met;
+  a.status = status;
+  double2* w = static_cast<double2*>(workspace);
+  const size_t plane = size_t(tau) * size_t(b);
+  a.Z = w;
+  a.G = w + plane;
+  a.UI = w + 2 * plane;
+  a.A = w + 3 * plane;
+  const int threads = 128;
+  const int64_t blocks = (tau + threads - 1) / threads;
+  sparse_zip_chain_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(sparse_zip_chain_kernel)", err);
+  return TPF_OK;
+}

@@ -188,13 +188,10 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     b = c.b
     if (y != y.T).nnz != 0:
         raise NotImplementedError("ZIP loads on the GPU need a radial feeder with a symmetric Y_dd")
-    tree = tree_schedule(factorize_ydd(y, count=False), c.src)
+    tree = tree_schedule(factorize_ydd(y, count=False), c.src) if b <= 5120 else None
     ell = tree_ell(tree, c) if tree is not None else None
     if tree is None or ell is None:
-        raise NotImplementedError(
-            "ZIP loads on the GPU need a radial feeder that fits the tree kernel (<= 5,120 nodes, "
-            "<= 64 depth levels, <= 16 slots of 512 nodes); meshed or deeper networks take the "
-            "reference's per-case route (tpflow.dense._batch_via_single)")
+        return _solve_zip_chain(model, c, loads, opts, device, return_on_device)
     dev = require_cuda(device)
     order = tree.node_info.reshape(b, 4)[:, 0]
     z = model.zip
@@ -226,6 +223,61 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     if int(status.item()) != 0:  # assemble_fpi's splu failure (fpi.py:119-126)
         raise SingularSystemError("iteration matrix B is singular for some case (zero pivot)")
     # fpi_solve: converged = step_met and residual < residual_tolerance (fpi.py:197-198)
+    mask = (met != 0) & torch.isfinite(resid) & (resid < float(opts.residual_tolerance))
+    n_max = int(iters.max().item()) if tau else 0
+    if return_on_device:
+        return VoltageBatch(values=V, iterations=n_max, converged_mask=mask, residuals=resid,
+                            iterations_per_case=iters)
+    return VoltageBatch(values=V.cpu().numpy(), iterations=n_max, converged_mask=mask.cpu().numpy(),
+                        residuals=resid.cpu().numpy(), iterations_per_case=iters.cpu().numpy())
+
+
+def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
+    """ZIP loads on radial feeders beyond the tree kernel (deep, wide or large):
+    one thread per case with the same per-case tree LU and fpi_solve rules
+    (``tpf_sparse_zip_chain_c128``).  Meshed networks: NotImplementedError."""
+    from ._types import SingularSystemError
+    from .sparse import tree_parents
+    tp = tree_parents(c.y_dd)
+    if tp is None:
+        raise NotImplementedError(
+            "ZIP loads on the GPU need a radial feeder; meshed networks take the reference's per-case "
+            "route (tpflow.dense._batch_via_single)")
+    dev = require_cuda(device)
+    order, parent = tp
+    b = c.b
+    y = c.y_dd.tocsr()
+    e = np.zeros(b, dtype=np.complex128)
+    has = parent >= 0
+    e[has] = np.asarray(y[order[has], order[parent[has]]]).ravel()
+    z = model.zip
+    alpha = np.concatenate([np.asarray(z.alpha_z, float)[order], np.asarray(z.alpha_i, float)[order],
+                            np.asarray(z.alpha_p, float)[order]])
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    g = dict(orig=t(order.astype(np.int32)), parent=t(parent.astype(np.int32)), e=t(e),
+             ydiag=t(y.diagonal()[order].astype(np.complex128)), alpha=t(alpha), src=t(c.src[order]))
+    S = loads_to_device(loads.values, dev)
+    tau = S.shape[1]
+    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    resid = torch.empty(tau, dtype=torch.float64, device=dev)
+    met = torch.zeros(tau, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _capi.load()
+    chunk = max(1, min(tau, (1 << 30) // (64 * b)))  # scratch: 64 B per node and case, <= 1 GB
+    ws = torch.empty(int(lib.tpf_sparse_zip_chain_workspace_bytes(chunk, b)), dtype=torch.uint8, device=dev)
+    sn, sc = complex_strides(S)
+    v_flat = complex(abs(c.v_s))
+    for lo in range(0, tau, chunk):
+        hi = min(tau, lo + chunk)
+        _capi.call("tpf_sparse_zip_chain_c128", hi - lo, b, g["orig"].data_ptr(), g["parent"].data_ptr(),
+                   g["e"].data_ptr(), g["ydiag"].data_ptr(), g["alpha"].data_ptr(), g["src"].data_ptr(),
+                   S.data_ptr() + 16 * lo * sc, sn, sc, v_flat.real, v_flat.imag, float(opts.tolerance),
+                   int(opts.max_iterations), V.data_ptr() + 16 * lo, tau, 1, iters.data_ptr() + 4 * lo,
+                   resid.data_ptr() + 8 * lo, met.data_ptr() + lo, status.data_ptr(), ws.data_ptr(), ws.numel(),
+                   stream_ptr(dev))
+    if int(status.item()) != 0:
+        raise SingularSystemError("iteration matrix B is singular for some case (zero pivot)")
     mask = (met != 0) & torch.isfinite(resid) & (resid < float(opts.residual_tolerance))
     n_max = int(iters.max().item()) if tau else 0
     if return_on_device:

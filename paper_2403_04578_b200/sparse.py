@@ -86,6 +86,30 @@ def leaf_first_order(y: sparse.csr_matrix) -> np.ndarray | None:
     return np.argsort(-depth, kind="stable")
 
 
+def tree_parents(y) -> tuple[np.ndarray, np.ndarray] | None:
+    """Leaf-first order of a forest-shaped Y_dd and each position's parent
+    position (-1 at roots), or None if Y_dd has a cycle."""
+    y = sparse.csr_matrix(y)
+    order = leaf_first_order(y)
+    if order is None:
+        return None
+    b = y.shape[0]
+    g = sparse.csr_matrix(abs(y) + abs(y).T)
+    g.setdiag(0)
+    g.eliminate_zeros()
+    pos = np.empty(b, dtype=np.int64)
+    pos[order] = np.arange(b)
+    parent = np.full(b, -1, dtype=np.int64)
+    for k, v in enumerate(order):  # the neighbour eliminated after v is its parent (at most one: a forest)
+        nb = g.indices[g.indptr[v]:g.indptr[v + 1]]
+        later = [int(pos[u]) for u in nb if pos[u] > k]
+        if len(later) > 1:
+            return None
+        if later:
+            parent[k] = later[0]
+    return order, parent
+
+
 @dataclass
 class TreeLU:
     """Pr (Y_dd[o][:, o]) Pc = L U in the arrays libtpf's sparse kernel reads."""

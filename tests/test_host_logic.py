@@ -70,8 +70,11 @@ class TestBoundaryErrors:
         from scipy import sparse as sp
         y = m.admittance.y_dd.tolil()
         dense = m.admittance.y_dd.toarray()
-        i, j = next((i, j) for i in range(b) for j in range(i + 1, b) if dense[i, j] == 0)
-        y[i, j] = y[j, i] = -1.0 + 1.0j  # a second path: the network is no longer radial
+        # a node, a neighbour and that neighbour's other neighbour: closing the triangle
+        # makes a cycle among the demand nodes (Y_dd is no longer a forest)
+        i, j = next((i, j) for i in range(b) for k in range(b) for j in range(b)
+                    if len({i, j, k}) == 3 and dense[i, k] != 0 and dense[k, j] != 0 and dense[i, j] == 0)
+        y[i, j] = y[j, i] = -1.0 + 1.0j
         mesh = NetworkModel.from_admittance(sp.csc_matrix(y), m.admittance.y_ds, slack=m.slack,
                                             zip_coeffs=zm.zip)
         with pytest.raises(NotImplementedError, match="radial feeder"):

@@ -85,3 +85,28 @@ def test_zip_small_feeders_nan_and_empty(n_buses):
     S[0, 4] = np.nan
     with pytest.raises(SingularSystemError):
         batch_solve_dense(model, LoadMatrix(S), SolveOptions())
+
+
+@pytest.mark.parametrize("n_buses,kmax", [(40, 1), (300, 1), (60, 2)])
+def test_zip_deep_feeders_thread_per_case_kernel(n_buses, kmax):
+    """Radial feeders the tree kernel does not take (chains: > 64 depth levels) run
+    on tpf_sparse_zip_chain_c128 with the same semantics."""
+    from paper_2403_04578_b200 import (GenSpec, LoadMatrix, NetworkModel, SolveOptions, ZipCoefficients,
+                                       batch_solve_dense, build_network, gen_scenarios)
+    spec = GenSpec(n_buses=n_buses, k_max=kmax, seed=11)
+    base = build_network(spec)
+    b = base.n_demand
+    w = np.random.default_rng(b).dirichlet([1.0, 1.0, 1.0], size=b)
+    z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
+    model = NetworkModel.from_branches(base.branches, n_buses, slack=base.slack, zip_coeffs=z)
+    S = gen_scenarios(model, 150, spec).values.copy()
+    S[:, 3] = 0.0
+    out = batch_solve_dense(model, LoadMatrix(S), SolveOptions())
+    V, n, mask, res, it = orc.dense_zip_batch(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                              z.alpha_z, z.alpha_i, z.alpha_p, S)
+    assert out.iterations == it
+    assert np.array_equal(out.converged_mask, mask)
+    assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
+    assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
+    fin = np.isfinite(res) & mask
+    assert np.allclose(out.residuals[fin], res[fin], rtol=1e-3, atol=1e-12)

@@ -46,10 +46,7 @@ for trial in range(n_cases):
     w = rng.dirichlet([1.0, 1.0, 1.0], size=model.n_demand)
     z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
     zm = NetworkModel.from_branches(model.branches, nb, slack=model.slack, zip_coeffs=z)
-    try:
-        zo = batch_solve_dense(zm, loads, opts)
-    except NotImplementedError:  # deep chains (k_max = 1): beyond the tree kernel's levels
-        continue
+    zo = batch_solve_dense(zm, loads, opts)  # tree kernel, or the thread-per-case kernel for deep feeders
     ZV, zn, zmask, _, zit = orc.dense_zip_batch(zm.admittance.y_dd, zm.source_injection(), vs, z.alpha_z,
                                                 z.alpha_i, z.alpha_p, S)
     okz = np.array_equal(zo.iterations_per_case, zn) and np.array_equal(zo.converged_mask, zmask) and \
