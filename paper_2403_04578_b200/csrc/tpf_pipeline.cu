@@ -13,6 +13,8 @@
 // summary kernel and copy.  Pageable host buffers are page-locked in place for
 // the duration of the call (cudaHostRegister) so every copy is a DMA.
 #include <cstring>
+#include <map>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -204,6 +206,22 @@ struct Streams {
       if (x) cudaStreamDestroy(x);
   }
 };
+
+// Streams and events of the pipeline, created once per (thread, device) and
+// reused: creating 3 streams + 6 events per call costs ~0.1 ms, a visible
+// share of a small batch's end-to-end time.
+Streams* cached_streams(int device) {
+  thread_local std::map<int, std::unique_ptr<Streams>> cache;
+  std::unique_ptr<Streams>& p = cache[device];
+  if (!p) {
+    p.reset(new Streams);
+    if (p->init() != cudaSuccess) {
+      p.reset();
+      return nullptr;
+    }
+  }
+  return p.get();
+}
 
 #define TPF_CK(expr, where)                           \
   do {                                                \
@@ -497,8 +515,9 @@ extern "C" int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t l
   if (workspace && workspace_bytes < tpf_sparse_tree_solve_host_workspace_bytes(tau, b, chunk_cases, ydd_row_ptr[b]))
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_solve_host_c128: workspace too small");
   ArenaScope arena(workspace, workspace_bytes);
-  Streams ss;
-  TPF_CK(ss.init(), "cudaStreamCreate");
+  Streams* ssp = cached_streams(device);
+  if (!ssp) return set_cuda_error("cudaStreamCreate", cudaGetLastError());
+  const Streams& ss = *ssp;
   const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   cudaStream_t st = ss.s[1];
   DevBuf dl, di, dc, dws;
@@ -576,8 +595,9 @@ extern "C" int tpf_dense_solve_host_c128(int64_t tau, int32_t b, const double* S
   if (workspace && workspace_bytes < tpf_dense_solve_host_workspace_bytes(tau, b, chunk_cases, ydd_row_ptr[b]))
     return set_error(TPF_ERR_INVALID, "tpf_dense_solve_host_c128: workspace too small");
   ArenaScope arena(workspace, workspace_bytes);
-  Streams ss;
-  TPF_CK(ss.init(), "cudaStreamCreate");
+  Streams* ssp = cached_streams(device);
+  if (!ssp) return set_cuda_error("cudaStreamCreate", cudaGetLastError());
+  const Streams& ss = *ssp;
   const bool large = b > tpf_dense_max_nodes();
   const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   DevBuf dK, dW, dws;
@@ -627,8 +647,9 @@ extern "C" int tpf_sparse_solve_host_c128(int64_t tau, int32_t b, const double* 
                                                                             l_ptr[b], u_ptr[b]))
     return set_error(TPF_ERR_INVALID, "tpf_sparse_solve_host_c128: workspace too small");
   ArenaScope arena(workspace, workspace_bytes);
-  Streams ss;
-  TPF_CK(ss.init(), "cudaStreamCreate");
+  Streams* ssp = cached_streams(device);
+  if (!ssp) return set_cuda_error("cudaStreamCreate", cudaGetLastError());
+  const Streams& ss = *ssp;
   const int64_t chunk = pick_chunk(tau, b, chunk_cases);
   const int64_t lnnz = l_ptr[b], unnz = u_ptr[b];
   DevBuf dlp, dlc, dlv, dup, duc, duv, dud, dperm, dsrc, dws;
