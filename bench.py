@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", dest="graph", action="store_false",
+                   help="time eager launches instead of a CUDA-graph replay of the step")
     return p.parse_args()
 
 
@@ -294,8 +296,27 @@ def run_ours():
     for _ in range(ARGS.warmup):
         step()
     torch.cuda.synchronize(dev)
+    # kernel-only timing (roofline): eager steps with events around the solve
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(ARGS.steps)]
+    for k in range(ARGS.steps):
+        out = step(kev[k], k)
+    torch.cuda.synchronize(dev)
+    # the timed steps replay one CUDA graph of the whole step (solve + residual +
+    # summary: the same kernels on the same buffers, no per-launch host cost);
+    # several scenario batches (C4) or --no-graph: eager launches
+    graph = None
+    if ARGS.graph and len(S_list) == 1:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                out = step()
+            graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as exc:  # noqa: BLE001 -- report and fall back to eager
+            print(f"bench: graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            graph = None
+            torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         if world > 1:
@@ -303,7 +324,10 @@ def run_ours():
         torch.cuda.synchronize(dev)
         t0.record(stream)
         for k in range(ARGS.steps):
-            out = step(kev[k], k)
+            if graph is not None:
+                graph.replay()
+            else:
+                out = step(None, k)
         t1.record(stream)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -365,6 +389,7 @@ def run_ours():
                                 sum_iterations=sum_n, batch_iterations=int(summ[0]),
                                 converged=int(summ[1]),
                                 l2="inputs (S, V: %.0f MB each) larger than the 126 MB L2" % (b * tau * 16 / 1e6),
+                                step_launch="cuda graph replay" if graph is not None else "eager",
                                 parallelism=f"tau-sharded x{world} (independent scenario batches)",
                                 **({"c4_full_1000_scenarios_s_extrapolated": 1000 * tau / value} if scenarios else {})),
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
