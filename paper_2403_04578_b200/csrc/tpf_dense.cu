@@ -133,7 +133,38 @@ __device__ __forceinline__ void gemm_warp(double (&vr)[NBH][2], double (&vi)[NBH
   }
 }
 
-template <int NB>
+// 3M variant (Gauss, as the default ws kernel): P1 += ur kr, P2 += ui ki,
+// P3 += (ur + ui)(kr + ki), each accumulator over the k-steps in the same order
+// as the ws kernel, so the two kernels give the same bits.
+template <int NBH, int NBW>
+__device__ __forceinline__ void kstep3p(double (&p1)[NBH][2], double (&p2)[NBH][2], double (&p3)[NBH][2],
+                                        const double2& u, const double2 (&kf)[NBW]) {
+  const double us = u.x + u.y;
+#pragma unroll
+  for (int lb = 0; lb < NBW; ++lb) {
+    const double kss = kf[lb].x + kf[lb].y;
+    dmma884(p1[lb][0], p1[lb][1], u.x, kf[lb].x);
+    dmma884(p2[lb][0], p2[lb][1], u.y, kf[lb].y);
+    dmma884(p3[lb][0], p3[lb][1], us, kss);
+  }
+}
+
+template <int NBH, int NBW>
+__device__ __forceinline__ void gemm_warp3(double (&p1)[NBH][2], double (&p2)[NBH][2], double (&p3)[NBH][2],
+                                           const double2* kb, const double2* ub, int KS) {
+  double2 u0, u1, k0[NBW], k1[NBW];
+  load_frags<NBW>(u0, k0, kb, ub, 0, KS);
+#pragma unroll 1
+  for (int ks = 0; ks < KS; ks += 2) {
+    const bool odd = ks + 1 < KS;
+    if (odd) load_frags<NBW>(u1, k1, kb, ub, ks + 1, KS);
+    kstep3p<NBH, NBW>(p1, p2, p3, u0, k0);
+    if (ks + 2 < KS) load_frags<NBW>(u0, k0, kb, ub, ks + 2, KS);
+    if (odd) kstep3p<NBH, NBW>(p1, p2, p3, u1, k1);
+  }
+}
+
+template <int NB, bool M3>
 __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs a) {
   constexpr int NBH = (NB + 1) / 2;  // max node blocks per warp
   constexpr uint32_t kTmemCols = 256;  // 2 warps per lane quadrant x 128 columns
@@ -292,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
             xi2[e] = xi;
             // S*/conj(v) = S* v / |v|^2
             const double srr = sv[lb].get(e), sii = sv[lb].get(2 + e);
-            const double r = 1.0 / m2;
+            const double r = M3 ? rcp_nr(m2) : 1.0 / m2;
             const double ur = __fma_rn(srr, xr, -(sii * xi)) * r;
             const double ui = __fma_rn(srr, xi, sii * xr) * r;
             const int node = 8 * (nb0 + lb) + 2 * q + e;
@@ -313,19 +344,49 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
     }
 
     // ---------- GEMM: V' = W + U K^T on FP64 tensor cores ----------
+    if constexpr (M3) {
+      double p1[NBH][2], p2[NBH][2], p3[NBH][2];
 #pragma unroll
-    for (int lb = 0; lb < NBH; ++lb) {
-      if (lb < nbw) {
-        // (node 2q, 2q+1) pairs of each plane land directly in the DMMA register pairs
-        const double2 wr = w_sm[(8 * (nb0 + lb) + 2 * q) / 2];
-        const double2 wi = w_sm[(NB * 8 + 8 * (nb0 + lb) + 2 * q) / 2];
-        vr[lb][0] = wr.x;
-        vr[lb][1] = wr.y;
-        vi[lb][0] = wi.x;
-        vi[lb][1] = wi.y;
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          const double2 wr = w_sm[(8 * (nb0 + lb) + 2 * q) / 2];
+          const double2 wi = w_sm[(NB * 8 + 8 * (nb0 + lb) + 2 * q) / 2];
+          p1[lb][0] = wr.x;
+          p1[lb][1] = wr.y;
+          p2[lb][0] = p2[lb][1] = 0.0;
+          p3[lb][0] = wr.x + wi.x;
+          p3[lb][1] = wr.y + wi.y;
+        }
       }
-    }
-    {
+      const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
+      if (nbw == NBH) {
+        gemm_warp3<NBH, NBH>(p1, p2, p3, kb, u_sm + lane, KS);
+      } else {
+        if constexpr (NB - NBH > 0) gemm_warp3<NBH, NB - NBH>(p1, p2, p3, kb, u_sm + lane, KS);
+      }
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            vr[lb][e] = p1[lb][e] - p2[lb][e];
+            vi[lb][e] = (p3[lb][e] - p1[lb][e]) - p2[lb][e];
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int lb = 0; lb < NBH; ++lb) {
+        if (lb < nbw) {
+          // (node 2q, 2q+1) pairs of each plane land directly in the DMMA register pairs
+          const double2 wr = w_sm[(8 * (nb0 + lb) + 2 * q) / 2];
+          const double2 wi = w_sm[(NB * 8 + 8 * (nb0 + lb) + 2 * q) / 2];
+          vr[lb][0] = wr.x;
+          vr[lb][1] = wr.y;
+          vi[lb][0] = wi.x;
+          vi[lb][1] = wi.y;
+        }
+      }
       const double2* kb = k_sm + size_t(nb0) * KS * 32 + lane;
       if (nbw == NBH) {
         gemm_warp<NBH, NBH>(vr, vi, kb, u_sm + lane, KS);
@@ -437,11 +498,18 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
 
 template <int NB>
 static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
+  // 3M GEMM + Newton reciprocal (bitwise equal to the default ws kernel) unless
+  // TPF_WS_4M=1 selects the 4-DMMA arithmetic for both kernels
+  static const bool four = [] {
+    const char* e = getenv("TPF_WS_4M");
+    return e && e[0] == '1';
+  }();
+  auto kern = four ? dense_fpi_kernel<NB, false> : dense_fpi_kernel<NB, true>;
   const size_t smem = DenseSmem<NB>::total(a.ks_count);
-  cudaError_t err = cudaFuncSetAttribute(dense_fpi_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense)", err);
   int per_sm = 0;
-  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_fpi_kernel<NB>, kThreads, smem);
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (err != cudaSuccess) return set_cuda_error("occupancy(dense)", err);
   if (per_sm < 1) return set_error(TPF_ERR_UNSUPPORTED, "dense kernel does not fit on an SM");
   if (per_sm > 2) per_sm = 2;  // each CTA holds 256 of the SM's 512 TMEM columns
@@ -451,7 +519,7 @@ static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
   const int64_t need = (a.tau + slots_per_cta - 1) / slots_per_cta;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  dense_fpi_kernel<NB><<<unsigned(grid), kThreads, smem, stream>>>(a);
+  kern<<<unsigned(grid), kThreads, smem, stream>>>(a);
   err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense_fpi_kernel)", err);
   return TPF_OK;
@@ -486,14 +554,26 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
                                      int64_t v_case_stride, int32_t* iters, void* workspace, size_t workspace_bytes,
                                      void* stream);
 
-// Kernel selection for tpf_dense_fpi_c128: the warp-specialised kernel
-// (tpf_dense_ws.cu) unless TPF_DENSE_KERNEL=pairs selects the pair kernel below.
-static bool use_pairs_kernel() {
-  static const bool pairs = [] {
+// Kernel selection for tpf_dense_fpi_c128.  Both kernels compute the same
+// bits (3M GEMM, Newton reciprocal), so the choice is purely a speed one:
+// batches of at most two waves of the ws kernel's slots are latency-bound
+// (each case gets its own slot), and the pair kernel's shorter rounds (two
+// warps on each slot group's GEMM and elementwise work) win there (C1: 0.069
+// -> 0.046 ms; b=100, tau=8,760: 0.26 -> 0.16 ms); longer batches are
+// throughput-bound and the ws kernel wins.  TPF_DENSE_KERNEL=pairs|ws forces
+// one.
+static bool use_pairs_kernel(int64_t tau) {
+  static const int forced = [] {
     const char* e = getenv("TPF_DENSE_KERNEL");
-    return e && strcmp(e, "pairs") == 0;
+    if (e && strcmp(e, "pairs") == 0) return 1;
+    if (e && strcmp(e, "ws") == 0) return 0;
+    return -1;
   }();
-  return pairs;
+  if (forced >= 0) return forced == 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return tau <= int64_t(2) * sms * 64;
 }
 
 extern "C" int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
@@ -509,7 +589,7 @@ extern "C" int tpf_dense_fpi_c128(int64_t tau, int32_t b, const double* S, int64
                                   double* V, int64_t v_node_stride, int64_t v_case_stride,
                                   int32_t* iters, void* workspace, size_t workspace_bytes,
                                   void* stream) {
-  if (use_pairs_kernel())
+  if (use_pairs_kernel(tau))
     return tpf_dense_pairs_fpi_c128(tau, b, S, s_node_stride, s_case_stride, K, W, v_flat_re, v_flat_im, tol,
                                     max_iter, V, v_node_stride, v_case_stride, iters, workspace, workspace_bytes,
                                     stream);

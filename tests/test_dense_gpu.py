@@ -192,7 +192,8 @@ def test_large_b_permutation_invariance_bitwise(golden):
 @pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
                                   "nine_zero_batch"])
 def test_ws_and_pair_kernels_agree(golden, name, kernel):
-    """Warp-specialised (3M GEMM) vs the 4M pair/solo kernels: same counts, values to GEMM rounding."""
+    """Warp-specialised vs pair kernel (both 3M + Newton reciprocal): same bits; vs the 4M solo
+    kernel: same counts, values to GEMM rounding."""
     import torch
     from paper_2403_04578_b200 import DenseOperator
     g = golden(name)
@@ -202,6 +203,8 @@ def test_ws_and_pair_kernels_agree(golden, name, kernel):
     V1, it1 = op.solve(S, o, kernel="ws")
     V2, it2 = op.solve(S, o, kernel=kernel)
     assert torch.equal(it1, it2)
+    if kernel == "pairs":
+        assert torch.equal(V1, V2)
     fin = torch.isfinite(V2).all(dim=0)
     assert torch.equal(fin, torch.isfinite(V1).all(dim=0))
     if fin.any():
@@ -297,11 +300,13 @@ def _ws_variant_run(env_extra: dict, kernel: str = "ws"):
 
 
 def test_ws_4m_and_split_variants_bitwise_equal_pairs():
-    """TPF_WS_4M=1 (one DMMA warp, 4M GEMM) and TPF_WS_SPLIT=2 (two DMMA warps per
-    SMSP) issue the pair kernel's DMMAs in the same order per element: same bits."""
-    pairs = _ws_variant_run({}, kernel="pairs")
-    assert np.array_equal(_ws_variant_run({"TPF_WS_4M": "1"}), pairs)
-    assert np.array_equal(_ws_variant_run({"TPF_WS_SPLIT": "2"}), pairs)
+    """TPF_WS_4M=1 (both kernels on the 4-DMMA arithmetic) and TPF_WS_SPLIT=2 (two
+    4M DMMA warps per SMSP) issue the pair kernel's DMMAs in the same order per
+    element: same bits; by default ws and pairs are both 3M: same bits too."""
+    pairs4 = _ws_variant_run({"TPF_WS_4M": "1"}, kernel="pairs")
+    assert np.array_equal(_ws_variant_run({"TPF_WS_4M": "1"}), pairs4)
+    assert np.array_equal(_ws_variant_run({"TPF_WS_SPLIT": "2"}), pairs4)
+    assert np.array_equal(_ws_variant_run({}), _ws_variant_run({}, kernel="pairs"))
 
 
 @pytest.mark.parametrize("devs", [["cuda:0", "cuda:0"], ["cuda:0", "cuda:0", "cuda:0"]])
