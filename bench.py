@@ -353,8 +353,8 @@ def run_ours():
         achieved = alg / (kms * 1e-3) / 1e12
         roofline = dict(bound="tensor", pipe="FP64 DMMA (mma.sync m8n8k4)", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
                         frac=achieved / peak_tf if peak_tf else None,
-                        traffic=traffic_from_profiles("dense_ws_kernel", tau),
-                        kernel="dense_ws_kernel", kernel_ms=kms,
+                        traffic=traffic_from_profiles(dense_kernel_name(b, tau), tau),
+                        kernel=dense_kernel_name(b, tau), kernel_ms=kms,
                         peak_source="measured in-run: DMMA-only probe (tpf_probe_fp64_tflops); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                         algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch",
@@ -398,6 +398,15 @@ def run_ours():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dense_kernel_name(b, tau):
+    """The kernel tpf_dense_fpi_c128 / the large path runs for this shape (tpf_dense.cu dispatch)."""
+    if b > 104:
+        return "gemm_kernel (large-b active set)"
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return "dense_fpi_kernel" if tau <= 2 * sms * 64 else "dense_ws_kernel"
 
 
 def launches_per_step(method, op, tau):
