@@ -414,7 +414,9 @@ def launches_per_step(method, op, tau):
     one tree launch per compact chunk (SparseOperator) + summary, or the
     general kernel + residual + summary."""
     if method == "dense":
-        return 3
+        # b > 104: init + (prep, bulk GEMM, tail GEMM, compact) per iteration up to the
+        # cap (early-exit launches once every case froze), then residual + summary
+        return 1 + 4 * 100 + 2 if op.b > 104 else 3
     from paper_2403_04578_b200.sparse import TREE_CHUNK
     if op.tree is not None:
         return (-(-tau // TREE_CHUNK) if tau > TREE_CHUNK else 1) + 1
