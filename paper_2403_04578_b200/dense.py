@@ -174,6 +174,13 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
     return finish(V, iters, resid, mask, summ, return_on_device)
 
 
+# ZIP route by feeder size (tools/zip_route_probe.py, one B200): the thread-per-case
+# kernel wins up to ~b = 350 (b=100: 108 vs 210 ms at tau=525,600; b=300: 92 vs
+# 100 ms), the one-case-per-SM tree kernel above (b=500: 72 vs 84 ms; b=5000:
+# 149 vs 558 ms).
+ZIP_CHAIN_MAX_B = 384
+
+
 def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_on_device: bool = False):
     """ZIP loads: the reference's per-case route (dense.py:214-230 -> fpi_solve,
     fpi.py:107-206) as one GPU launch on radial feeders (include/tpf.h,
@@ -188,6 +195,8 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     b = c.b
     if (y != y.T).nnz != 0:
         raise NotImplementedError("ZIP loads on the GPU need a radial feeder with a symmetric Y_dd")
+    if b <= ZIP_CHAIN_MAX_B:  # small feeders: one thread per case beats one case per SM
+        return _solve_zip_chain(model, c, loads, opts, device, return_on_device)
     tree = tree_schedule(factorize_ydd(y, count=False), c.src) if b <= 5120 else None
     ell = tree_ell(tree, c) if tree is not None else None
     if tree is None or ell is None:
