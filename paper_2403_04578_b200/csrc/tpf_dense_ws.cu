@@ -910,18 +910,18 @@ static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   if constexpr (NB >= 2) {
     if (split == 2) return ws::launch<NB, KS, 2, false>(a, st, sms);
   }
-  // node blocks of the GEMM done by the elementwise warps (TPF_WS_NE: default 5 at 13 node blocks,
-  // otherwise min(4, blocks - 6) so the EW blocks lie past the 6 scratch blocks)
+  // node blocks of the GEMM done by the elementwise warps: 5 at 13 node blocks
+  // (tuned on C2: NE 2..7 measured 6.69 / 6.56 / 6.34 / 6.31 / 6.58 / 6.63 ms),
+  // otherwise min(4, blocks - 6) so the EW blocks lie past the 6 scratch
+  // blocks; TPF_WS_NE=0 disables the EW share, any other value keeps the
+  // generic min(4, blocks - 6)
   static const int ne = [] {
     const char* e = getenv("TPF_WS_NE");
     return e ? atoi(e) : 5;
   }();
   if (four) return ws::launch<NB, KS, 1, false>(a, st, sms);
   if constexpr (NB == 13) {
-    if (ne == 2) return ws::launch<NB, KS, 1, true, NB - 2>(a, st, sms);
-    if (ne == 3) return ws::launch<NB, KS, 1, true, NB - 3>(a, st, sms);
     if (ne == 5) return ws::launch<NB, KS, 1, true, NB - 5>(a, st, sms);
-
   }
   if constexpr (NB > ws::kM3Pass0) {
     // the EW blocks must lie past the scratch blocks: NM >= kM3Pass0
