@@ -203,6 +203,25 @@ int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* orig, const
                               double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                               double* resid, uint8_t* step_met, int32_t* status,
                               void* workspace, size_t workspace_bytes, void* stream);
+/* ZIP loads on meshed (or non-symmetric) networks, the reference's per-case
+ * SuperLU route (dense.py:214-230 -> fpi.py:107-206): one thread per case,
+ * per-case LU of B = Y_dd + diag(alpha_z s*) on a fixed fill pattern without
+ * pivoting.  Step k eliminates original node orig[k]; kinfo[k] = (m_k, off)
+ * with idx[off..] = the m_k later positions, their L slots, U slots and the
+ * m_k x m_k update targets; base = Y_dd at the nslot factor slots (slot k < b
+ * the pivot of step k).  alpha [3][b] and src in elimination order; the
+ * residual reads Y_dd in CSR (original order).  workspace >=
+ * tpf_sparse_zip_lu_workspace_bytes(tau, b, nslot) (16 B per slot, node and
+ * case).  *status = 1 on a zero pivot.                                   */
+size_t tpf_sparse_zip_lu_workspace_bytes(int64_t tau, int32_t b, int32_t nslot);
+int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, const int32_t* orig, const int32_t* kinfo,
+                           const int32_t* idx, const double* base, const double* alpha, const double* src,
+                           const int32_t* y_row_ptr, const int32_t* y_col, const double* y_val,
+                           const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                           double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                           double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
+                           double* resid, uint8_t* step_met, int32_t* status,
+                           void* workspace, size_t workspace_bytes, void* stream);
 size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b);
 int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels,
                                  const int32_t* level_info, const int32_t* node_info, const double* node_coef,

@@ -72,7 +72,11 @@ def complex_strides(t: torch.Tensor) -> tuple[int, int]:
 
 
 def loads_to_device(values: np.ndarray, device: torch.device, dtype=np.complex128) -> torch.Tensor:
-    """Copy a b x tau complex load matrix to the device keeping its C/F order."""
+    """Copy a b x tau complex load matrix to the device keeping its C/F order
+    (a tensor already there is used as is)."""
+    if isinstance(values, torch.Tensor):
+        tdt = torch.complex64 if np.dtype(dtype) == np.complex64 else torch.complex128
+        return values.to(device=device, dtype=tdt)
     arr = np.asarray(values, dtype=dtype)
     if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
         arr = np.ascontiguousarray(arr)

@@ -405,3 +405,232 @@ extern "C" int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* 
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_zip_chain_kernel)", err);
   return TPF_OK;
 }
+
+// ZIP loads on meshed networks (the reference's per-case SuperLU route,
+// dense.py:214-230 -> fpi.py:107-206): one thread per case, per-case LU of
+// B = Y_dd + diag(alpha_z s*) on a fixed fill pattern (minimum-degree order of
+// the symmetrised pattern, no pivoting; host schedule sparse.zip_lu_schedule)
+// and fpi_solve's iteration as in the chain kernel above; the ZIP residual
+// from Y_dd in CSR.  Scratch: the factor slots [nslot][tau] and one
+// right-hand side [b][tau], case-minor so every slot access is coalesced.
+namespace tpf {
+namespace {
+
+struct ZipLuArgs {
+  int64_t tau;
+  int b, nslot;
+  const double2* S;
+  int64_t s_node, s_case;  // original node order
+  const int32_t* orig;     // elimination position k -> original node
+  const int32_t* kinfo;    // [b][2]: later neighbours m_k, offset into idx
+  const int32_t* idx;      // per step: positions[m], L slots[m], U slots[m], targets[m*m]
+  const double2* base;     // [nslot] Y_dd at the factor slots
+  const double* alpha;     // [3][b] elimination order
+  const double2* src;      // elimination order
+  const int32_t* rp;       // CSR of Y_dd (original order), residual
+  const int32_t* ci;
+  const double2* yv;
+  double2 v_flat;
+  double tol2;
+  int max_iter;
+  double2* V;
+  int64_t v_node, v_case;  // original node order
+  int32_t* iters;
+  double* resid;
+  uint8_t* met;
+  int32_t* status;
+  double2 *F, *Z;
+};
+
+__global__ void __launch_bounds__(128) sparse_zip_lu_kernel(const ZipLuArgs a) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= a.tau) return;
+  const int b = a.b;
+  const int64_t t = a.tau;
+  double2* F = a.F + j;
+  double2* Z = a.Z + j;
+  auto Sk = [&](int k) { return a.S[int64_t(__ldg(a.orig + k)) * a.s_node + j * a.s_case]; };
+  auto Vn = [&](int node) -> double2& { return a.V[int64_t(node) * a.v_node + j * a.v_case]; };
+  for (int s = 0; s < a.nslot; ++s) F[s * t] = __ldg(a.base + s);
+  bool any = false, bad = false;
+  for (int k = 0; k < b; ++k) {
+    const double2 s = Sk(k);
+    const double az = __ldg(a.alpha + k), ap = __ldg(a.alpha + 2 * b + k);
+    const double2 yd = F[k * t];
+    F[k * t] = make_double2(__fma_rn(az, s.x, yd.x), __fma_rn(-az, s.y, yd.y));
+    if (ap != 0.0 && (s.x != 0.0 || s.y != 0.0)) any = true;
+  }
+  // right-looking elimination over the fixed pattern; slot k keeps 1 / U[k,k]
+  for (int k = 0; k < b; ++k) {
+    const double2 piv = F[k * t];
+    const double n2 = __fma_rn(piv.x, piv.x, piv.y * piv.y);
+    if (!(n2 > 0.0) || !isfinite(n2)) bad = true;
+    const double rr = 1.0 / n2;
+    const double2 ui = make_double2(piv.x * rr, -piv.y * rr);
+    F[k * t] = ui;
+    const int m = __ldg(a.kinfo + 2 * k), off = __ldg(a.kinfo + 2 * k + 1);
+    const int32_t* ls = a.idx + off + m;
+    const int32_t* us = ls + m;
+    const int32_t* tg = us + m;
+    for (int r = 0; r < m; ++r) {
+      const int lr = __ldg(ls + r);
+      const double2 l = cmulz(F[lr * t], ui);
+      F[lr * t] = l;
+      for (int c = 0; c < m; ++c) {
+        const int tt = __ldg(tg + r * m + c);
+        const double2 lu = cmulz(l, F[__ldg(us + c) * t]);
+        double2 x = F[tt * t];
+        x.x -= lu.x;
+        x.y -= lu.y;
+        F[tt * t] = x;
+      }
+    }
+  }
+  if (bad) atomicExch(a.status, 1);
+  for (int k = 0; k < b; ++k) Vn(__ldg(a.orig + k)) = a.v_flat;
+  int n = 0;
+  bool met = false;
+  while (n < a.max_iter) {
+    for (int k = 0; k < b; ++k) {
+      double2 v = Vn(__ldg(a.orig + k));
+      double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+      if (m2 < kZeroGuard2) {
+        v = make_double2(kZeroGuard, 0.0);
+        m2 = kZeroGuard * kZeroGuard;
+      }
+      const double r = 1.0 / m2;
+      const double2 s = Sk(k);
+      const double ai = __ldg(a.alpha + b + k), ap = __ldg(a.alpha + 2 * b + k);
+      const double2 c = __ldg(a.src + k);
+      const double ur = __fma_rn(s.x, v.x, s.y * v.y) * r, uim = __fma_rn(s.x, v.y, -(s.y * v.x)) * r;
+      Z[k * t] = any ? make_double2(-(ap * ur + c.x + ai * s.x), -(ap * uim + c.y - ai * s.y))
+                     : make_double2(-(c.x + ai * s.x), -(c.y - ai * s.y));
+    }
+    // forward (unit L), then backward (U) with the step test and the update
+    for (int k = 0; k < b; ++k) {
+      const int m = __ldg(a.kinfo + 2 * k), off = __ldg(a.kinfo + 2 * k + 1);
+      const double2 zk = Z[k * t];
+      for (int r = 0; r < m; ++r) {
+        const int p = __ldg(a.idx + off + r);
+        const double2 lz = cmulz(F[__ldg(a.idx + off + m + r) * t], zk);
+        double2 x = Z[p * t];
+        x.x -= lz.x;
+        x.y -= lz.y;
+        Z[p * t] = x;
+      }
+    }
+    bool small = true, fin = true;
+    for (int k = b - 1; k >= 0; --k) {
+      const int m = __ldg(a.kinfo + 2 * k), off = __ldg(a.kinfo + 2 * k + 1);
+      double2 acc = Z[k * t];
+      for (int c = 0; c < m; ++c) {
+        const double2 uz = cmulz(F[__ldg(a.idx + off + 2 * m + c) * t], Z[__ldg(a.idx + off + c) * t]);
+        acc.x -= uz.x;
+        acc.y -= uz.y;
+      }
+      const double2 w = cmulz(acc, F[k * t]);
+      Z[k * t] = w;
+      double2& vk = Vn(__ldg(a.orig + k));
+      double2 v = vk;
+      if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+      const double dr = w.x - v.x, di = w.y - v.y;
+      if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;
+      if (!(isfinite(w.x) && isfinite(w.y))) fin = false;
+      vk = w;
+    }
+    ++n;
+    if (!any) {
+      met = true;
+      break;
+    }
+    if (!fin) break;
+    if (small) {
+      met = true;
+      break;
+    }
+  }
+  // ZIP residual: max_k |az s |v|^2 + ai s v + ap s + v conj(src + (Y v)_k)|
+  double worst = 0.0;
+  for (int k = 0; k < b; ++k) {
+    const int node = __ldg(a.orig + k);
+    double2 yv = make_double2(0.0, 0.0);
+    for (int e = __ldg(a.rp + node); e < __ldg(a.rp + node + 1); ++e) {
+      const double2 x = cmulz(__ldg(a.yv + e), Vn(__ldg(a.ci + e)));
+      yv.x += x.x;
+      yv.y += x.y;
+    }
+    const double2 v = Vn(node), s = Sk(k), c = __ldg(a.src + k);
+    const double az = __ldg(a.alpha + k), zi = __ldg(a.alpha + b + k), zp = __ldg(a.alpha + 2 * b + k);
+    const double v2 = v.x * v.x + v.y * v.y;
+    const double2 sv = cmulz(s, v);
+    const double lr = az * s.x * v2 + zi * sv.x + zp * s.x, li = az * s.y * v2 + zi * sv.y + zp * s.y;
+    const double ar = c.x + yv.x, aim = c.y + yv.y;
+    const double mr = lr + (v.x * ar + v.y * aim), mi = li + (v.y * ar - v.x * aim);
+    worst = nanmax(worst, hypot(mr, mi));
+  }
+  a.iters[j] = n;
+  a.resid[j] = worst;
+  a.met[j] = met ? 1 : 0;
+}
+
+}  // namespace
+}  // namespace tpf
+
+extern "C" size_t tpf_sparse_zip_lu_workspace_bytes(int64_t tau, int32_t b, int32_t nslot) {
+  return (size_t(nslot) + size_t(b)) * size_t(tau) * 16 + 256;
+}
+
+extern "C" int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, const int32_t* orig,
+                                      const int32_t* kinfo, const int32_t* idx, const double* base,
+                                      const double* alpha, const double* src, const int32_t* y_row_ptr,
+                                      const int32_t* y_col, const double* y_val, const double* S,
+                                      int64_t s_node_stride, int64_t s_case_stride, double v_flat_re,
+                                      double v_flat_im, double tol, int32_t max_iter, double* V,
+                                      int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, double* resid,
+                                      uint8_t* step_met, int32_t* status, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  if (tau < 0 || b < 1 || nslot < b)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_lu_c128: need tau >= 0, b >= 1, nslot >= b");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!orig || !kinfo || !idx || !base || !alpha || !src || !y_row_ptr || !y_col || !y_val || !S || !V || !iters ||
+      !resid || !step_met || !status || !workspace)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_lu_c128: null pointer");
+  if (workspace_bytes < tpf_sparse_zip_lu_workspace_bytes(tau, b, nslot))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_lu_c128: workspace too small");
+  ZipLuArgs a;
+  a.tau = tau;
+  a.b = b;
+  a.nslot = nslot;
+  a.S = reinterpret_cast<const double2*>(S);
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.orig = orig;
+  a.kinfo = kinfo;
+  a.idx = idx;
+  a.base = reinterpret_cast<const double2*>(base);
+  a.alpha = alpha;
+  a.src = reinterpret_cast<const double2*>(src);
+  a.rp = y_row_ptr;
+  a.ci = y_col;
+  a.yv = reinterpret_cast<const double2*>(y_val);
+  a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = reinterpret_cast<double2*>(V);
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  a.resid = resid;
+  a.met = step_met;
+  a.status = status;
+  a.F = static_cast<double2*>(workspace);
+  a.Z = a.F + size_t(nslot) * size_t(tau);
+  const int threads = 128;
+  const int64_t blocks = (tau + threads - 1) / threads;
+  sparse_zip_lu_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(sparse_zip_lu_kernel)", err);
+  return TPF_OK;
+}

@@ -193,8 +193,8 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     c = ModelContract.of(model)
     y = c.y_dd
     b = c.b
-    if (y != y.T).nnz != 0:
-        raise NotImplementedError("ZIP loads on the GPU need a radial feeder with a symmetric Y_dd")
+    if (y != y.T).nnz != 0:  # non-symmetric values: the general per-case LU
+        return _solve_zip_lu(model, c, loads, opts, device, return_on_device)
     if b <= ZIP_CHAIN_MAX_B:  # small feeders: one thread per case beats one case per SM
         return _solve_zip_chain(model, c, loads, opts, device, return_on_device)
     tree = tree_schedule(factorize_ydd(y, count=False), c.src) if b <= 5120 else None
@@ -248,10 +248,8 @@ def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
     from ._types import SingularSystemError
     from .sparse import tree_parents
     tp = tree_parents(c.y_dd)
-    if tp is None:
-        raise NotImplementedError(
-            "ZIP loads on the GPU need a radial feeder; meshed networks take the reference's per-case "
-            "route (tpflow.dense._batch_via_single)")
+    if tp is None:  # meshed: per-case LU on a fixed fill pattern
+        return _solve_zip_lu(model, c, loads, opts, device, return_on_device)
     dev = require_cuda(device)
     order, parent = tp
     b = c.b
@@ -285,10 +283,59 @@ def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
                    int(opts.max_iterations), V.data_ptr() + 16 * lo, tau, 1, iters.data_ptr() + 4 * lo,
                    resid.data_ptr() + 8 * lo, met.data_ptr() + lo, status.data_ptr(), ws.data_ptr(), ws.numel(),
                    stream_ptr(dev))
-    if int(status.item()) != 0:
+    return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)
+
+
+def _solve_zip_lu(model, c, loads, opts, device, return_on_device):
+    """ZIP loads on meshed (or non-symmetric) networks: the reference's per-case
+    SuperLU route (dense.py:214-230 -> fpi.py:107-206) as one thread per case
+    factorizing B = Y_dd + diag(alpha_z s*) on a fixed minimum-degree fill
+    pattern without pivoting (``tpf_sparse_zip_lu_c128``).  A zero pivot raises
+    SingularSystemError, as splu does for a singular B."""
+    from .sparse import zip_lu_schedule
+    dev = require_cuda(device)
+    sch = zip_lu_schedule(c.y_dd)
+    order = sch.orig.astype(np.int64)
+    b = c.b
+    z = model.zip
+    alpha = np.concatenate([np.asarray(z.alpha_z, float)[order], np.asarray(z.alpha_i, float)[order],
+                            np.asarray(z.alpha_p, float)[order]])
+    rp, ci, yv = host_csr(c)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    g = dict(orig=t(sch.orig), kinfo=t(sch.kinfo), idx=t(sch.idx), base=t(sch.base), alpha=t(alpha),
+             src=t(np.asarray(c.src, np.complex128)[order]), rp=t(rp), ci=t(ci), yv=t(yv))
+    S = loads_to_device(loads.values, dev)
+    tau = S.shape[1]
+    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    resid = torch.empty(tau, dtype=torch.float64, device=dev)
+    met = torch.zeros(tau, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _capi.load()
+    per_case = 16 * (sch.nslot + b)
+    chunk = max(1, min(tau, (1 << 30) // per_case))  # scratch <= 1 GB
+    ws = torch.empty(int(lib.tpf_sparse_zip_lu_workspace_bytes(chunk, b, sch.nslot)), dtype=torch.uint8,
+                     device=dev)
+    sn, sc = complex_strides(S)
+    v_flat = complex(abs(c.v_s))
+    for lo in range(0, tau, chunk):
+        hi = min(tau, lo + chunk)
+        _capi.call("tpf_sparse_zip_lu_c128", hi - lo, b, sch.nslot, g["orig"].data_ptr(), g["kinfo"].data_ptr(),
+                   g["idx"].data_ptr(), g["base"].data_ptr(), g["alpha"].data_ptr(), g["src"].data_ptr(),
+                   g["rp"].data_ptr(), g["ci"].data_ptr(), g["yv"].data_ptr(), S.data_ptr() + 16 * lo * sc, sn,
+                   sc, v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                   V.data_ptr() + 16 * lo, tau, 1, iters.data_ptr() + 4 * lo, resid.data_ptr() + 8 * lo,
+                   met.data_ptr() + lo, status.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)
+
+
+def _zip_outputs(V, iters, resid, met, status, opts, return_on_device):
+    from ._types import SingularSystemError
+    if int(status.item()) != 0:  # assemble_fpi's splu failure (fpi.py:119-126)
         raise SingularSystemError("iteration matrix B is singular for some case (zero pivot)")
+    # fpi_solve: converged = step_met and residual < residual_tolerance (fpi.py:197-198)
     mask = (met != 0) & torch.isfinite(resid) & (resid < float(opts.residual_tolerance))
-    n_max = int(iters.max().item()) if tau else 0
+    n_max = int(iters.max().item()) if iters.numel() else 0
     if return_on_device:
         return VoltageBatch(values=V, iterations=n_max, converged_mask=mask, residuals=resid,
                             iterations_per_case=iters)

@@ -111,6 +111,107 @@ def tree_parents(y) -> tuple[np.ndarray, np.ndarray] | None:
 
 
 @dataclass
+class ZipLUSchedule:
+    """Fixed-pattern LU schedule of a meshed Y_dd for per-case factorization
+    (``tpf_sparse_zip_lu_c128``): minimum-degree elimination order over the
+    symmetrised pattern, no pivoting.  Step k eliminates node ``orig[k]``; its
+    later neighbours (fill included) sit at positions ``idx[off:off+m]``,
+    followed by their L slots, U slots and the m x m update targets; slot k
+    (< b) is the pivot of step k."""
+
+    b: int
+    nslot: int
+    orig: np.ndarray   # int32 [b]
+    kinfo: np.ndarray  # int32 [b, 2]: m_k, offset into idx
+    idx: np.ndarray    # int32
+    base: np.ndarray   # complex128 [nslot]: Y_dd at the factor slots (0 at fill)
+
+    @property
+    def fill(self) -> int:
+        return self.nslot - self.b
+
+
+def zip_lu_schedule(y) -> ZipLUSchedule:
+    """Greedy minimum-degree order (ties: lowest node index) and the symbolic
+    elimination of Y_dd's symmetrised pattern."""
+    import heapq
+    y = sparse.csr_matrix(y)
+    b = y.shape[0]
+    g = sparse.csr_matrix(abs(y) + abs(y).T)
+    g.setdiag(0)
+    g.eliminate_zeros()
+    adj = [set(g.indices[g.indptr[v]:g.indptr[v + 1]].tolist()) for v in range(b)]
+    heap = [(len(adj[v]), v) for v in range(b)]
+    heapq.heapify(heap)
+    done = np.zeros(b, dtype=bool)
+    order, nbrs = [], []
+    while heap:
+        d, v = heapq.heappop(heap)
+        if done[v] or d != len(adj[v]):
+            continue  # stale entry
+        done[v] = True
+        nb = adj[v]
+        order.append(v)
+        nbrs.append(list(nb))
+        for u in nb:
+            adj[u].discard(v)
+            adj[u] |= nb - {u}
+            heapq.heappush(heap, (len(adj[u]), u))
+        adj[v] = set()
+    order = np.asarray(order, dtype=np.int64)
+    pos = np.empty(b, dtype=np.int64)
+    pos[order] = np.arange(b)
+    later = [sorted(int(pos[u]) for u in nb) for nb in nbrs]
+    slot = {}
+    nslot = b
+    for k, lk in enumerate(later):
+        for q in lk:
+            slot[(q, k)] = nslot  # L
+            slot[(k, q)] = nslot + 1  # U
+            nslot += 2
+    kinfo = np.zeros((b, 2), dtype=np.int32)
+    idx = []
+    for k, lk in enumerate(later):
+        kinfo[k] = (len(lk), len(idx))
+        idx += lk
+        idx += [slot[(q, k)] for q in lk]
+        idx += [slot[(k, q)] for q in lk]
+        idx += [(q if q == r else slot[(q, r)]) for q in lk for r in lk]
+    base = np.zeros(nslot, dtype=np.complex128)
+    c = y.tocoo()
+    for r, col, v in zip(c.row, c.col, c.data):
+        pr, pc = int(pos[r]), int(pos[col])
+        base[pr if pr == pc else slot[(pr, pc)]] += v
+    return ZipLUSchedule(b=b, nslot=nslot, orig=order.astype(np.int32), kinfo=kinfo,
+                         idx=np.asarray(idx, dtype=np.int32), base=base)
+
+
+def zip_lu_solve_host(s: ZipLUSchedule, diag_add: np.ndarray, rhs: np.ndarray) -> np.ndarray:
+    """Host restatement of the kernel's factorization + solve (schedule tests):
+    (Y_dd + diag(diag_add)) x = rhs, original node order."""
+    F = s.base.copy()
+    F[:s.b] += np.asarray(diag_add)[s.orig]
+    for k in range(s.b):
+        m, off = s.kinfo[k]
+        pos, ls, us, tg = (s.idx[off:off + m], s.idx[off + m:off + 2 * m], s.idx[off + 2 * m:off + 3 * m],
+                           s.idx[off + 3 * m:off + 3 * m + m * m].reshape(m, m))
+        F[k] = 1.0 / F[k]
+        for i in range(m):
+            F[ls[i]] *= F[k]
+            F[tg[i]] -= F[ls[i]] * F[us]
+    z = np.asarray(rhs, dtype=np.complex128)[s.orig].copy()
+    for k in range(s.b):
+        m, off = s.kinfo[k]
+        z[s.idx[off:off + m]] -= F[s.idx[off + m:off + 2 * m]] * z[k]
+    for k in range(s.b - 1, -1, -1):
+        m, off = s.kinfo[k]
+        z[k] = (z[k] - np.dot(F[s.idx[off + 2 * m:off + 3 * m]], z[s.idx[off:off + m]])) * F[k]
+    out = np.empty_like(z)
+    out[s.orig] = z
+    return out
+
+
+@dataclass
 class TreeLU:
     """Pr (Y_dd[o][:, o]) Pc = L U in the arrays libtpf's sparse kernel reads."""
 

@@ -2,7 +2,8 @@
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_zip.py
 
-For each fixture: a radial feeder from the reference generator with mixed
+For each fixture: a radial feeder (``*_mesh``: plus tie branches closing loops
+among the demand buses, the reference's meshed per-case SuperLU route) from the reference generator with mixed
 Z/I/P fractions per node (seeded), a load batch (some zero-load cases and, for
 ``zip9_heavy``, an infeasible one), and the reference batch_solve_dense result
 (which loops fpi_solve per case) plus per-case iterations / step flags from
@@ -19,13 +20,25 @@ sys.dont_write_bytecode = True
 
 from tpflow import (GenSpec, LoadMatrix, NetworkModel, SolveOptions, batch_solve_dense,  # noqa: E402
                     build_network, fpi_solve, gen_scenarios)
-from tpflow.network import ZipCoefficients  # noqa: E402
+from tpflow.network import Branch, ZipCoefficients  # noqa: E402
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "zip")
 
 
-def zip_model(n_buses, seed, kind):
+def zip_model(n_buses, seed, kind, loops=0):
     base = build_network(GenSpec(n_buses=n_buses, seed=seed))
+    branches = list(base.branches)
+    if loops:  # tie branches between demand buses close loops: a meshed Y_dd
+        rng_l = np.random.default_rng(200 + seed)
+        linked = {frozenset((br.from_bus, br.to_bus)) for br in branches}
+        while loops:
+            i, j = (int(x) for x in rng_l.choice(np.arange(1, n_buses), 2, replace=False))
+            if frozenset((i, j)) in linked:
+                continue
+            linked.add(frozenset((i, j)))
+            loops -= 1
+            br = branches[int(rng_l.integers(len(branches)))]
+            branches.append(Branch(from_bus=i, to_bus=j, r=br.r * 2.0, x=br.x * 2.0))
     b = base.n_demand
     rng = np.random.default_rng(100 + seed)
     if kind == "mixed":
@@ -37,11 +50,11 @@ def zip_model(n_buses, seed, kind):
         raise ValueError(kind)
     w = w / w.sum(axis=1, keepdims=True)
     z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
-    return NetworkModel.from_branches(base.branches, n_buses, slack=base.slack, zip_coeffs=z), z
+    return NetworkModel.from_branches(branches, n_buses, slack=base.slack, zip_coeffs=z), z
 
 
-def save(name, n_buses, seed, tau, kind="mixed", scale=1.0, heavy=False, opts=SolveOptions()):
-    model, z = zip_model(n_buses, seed, kind)
+def save(name, n_buses, seed, tau, kind="mixed", scale=1.0, heavy=False, opts=SolveOptions(), loops=0):
+    model, z = zip_model(n_buses, seed, kind, loops)
     S = gen_scenarios(model, tau, GenSpec(n_buses=n_buses, seed=seed, load_scale=scale)).values.copy()
     S[:, 1] = 0.0  # a zero-load case
     if heavy:
@@ -66,3 +79,5 @@ save("zip9_mixed", 9, 0, 40)
 save("zip9_heavy", 9, 1, 20, heavy=True)
 save("zip9_pure_zi", 9, 2, 20, kind="pure_zi")
 save("zip101_mixed", 101, 0, 64, scale=3.0)
+save("zip9_mesh", 9, 3, 24, loops=4)
+save("zip101_mesh", 101, 4, 48, scale=2.0, loops=8)

@@ -66,7 +66,7 @@ class TestBoundaryErrors:
             batch_solve_dense(zm, loads)
         with pytest.raises(ValueError, match="constant-power"):
             batch_solve_sparse(zm, loads)
-        # a meshed network with ZIP loads stays on the reference's per-case route
+        # a meshed network with ZIP loads: the per-case LU kernel (tests/test_zip_gpu.py), no CPU fallback
         from scipy import sparse as sp
         y = m.admittance.y_dd.tolil()
         dense = m.admittance.y_dd.toarray()
@@ -77,8 +77,17 @@ class TestBoundaryErrors:
         y[i, j] = y[j, i] = -1.0 + 1.0j
         mesh = NetworkModel.from_admittance(sp.csc_matrix(y), m.admittance.y_ds, slack=m.slack,
                                             zip_coeffs=zm.zip)
-        with pytest.raises(NotImplementedError, match="radial feeder"):
+        with pytest.raises(RuntimeError, match="CUDA device"):
             batch_solve_dense(mesh, loads)
+        # its fixed-pattern schedule (sparse.zip_lu_schedule) solves B x = r like SuperLU
+        from paper_2403_04578_b200.sparse import zip_lu_schedule, zip_lu_solve_host
+        sch = zip_lu_schedule(mesh.admittance.y_dd)
+        assert sch.fill > 0 and sorted(sch.orig.tolist()) == list(range(b))
+        rng = np.random.default_rng(1)
+        d = 0.2 * rng.normal(size=b) - 0.1j
+        r = rng.normal(size=b) + 1j * rng.normal(size=b)
+        ref = sp.linalg.spsolve((mesh.admittance.y_dd + sp.diags(d)).tocsc(), r)
+        assert np.abs(zip_lu_solve_host(sch, d, r) - ref).max() <= 1e-12 * np.abs(ref).max()
 
     def test_memory_guard(self):
         m = build_network(GenSpec(n_buses=9, seed=42))

@@ -79,7 +79,8 @@ def test_c2_statistics_recorded(golden):
     assert int(g["c2_max_n"]) == 7
 
 
-@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed"])
+@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed", "zip9_mesh",
+                                  "zip101_mesh"])
 def test_zip_oracle_matches_reference(name):
     """The ZIP restatement (per-case fpi_solve) against the reference's own batch."""
     import os

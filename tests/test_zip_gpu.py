@@ -20,12 +20,21 @@ def fixture(name):
     d = np.load(os.path.join(DIR, name + ".npz"))
     base = build_network(GenSpec(n_buses=int(d["n_buses"]), seed=int(d["seed"])))
     z = ZipCoefficients(alpha_z=d["alpha_z"], alpha_i=d["alpha_i"], alpha_p=d["alpha_p"])
-    model = NetworkModel.from_branches(base.branches, int(d["n_buses"]), slack=base.slack, zip_coeffs=z)
+    if name.endswith("_mesh"):  # tie branches: the fixture's own Y_dd and source injection
+        from scipy import sparse as sp
+        b = d["S"].shape[0]
+        y = sp.csc_matrix((d["ydd_data"], d["ydd_indices"], d["ydd_indptr"]), shape=(b, b))
+        y_ds = sp.csc_matrix(np.asarray(d["src"]).reshape(b, 1) / base.slack.v_s)
+        model = NetworkModel.from_admittance(y, y_ds, slack=base.slack, zip_coeffs=z)
+        assert np.array_equal(model.source_injection(), d["src"])
+    else:
+        model = NetworkModel.from_branches(base.branches, int(d["n_buses"]), slack=base.slack, zip_coeffs=z)
     assert np.array_equal(model.admittance.y_dd.tocsc().data, d["ydd_data"])
     return model, d
 
 
-@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed"])
+@pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed", "zip9_mesh",
+                                  "zip101_mesh"])
 def test_zip_matches_reference(name):
     from paper_2403_04578_b200 import LoadMatrix, SolveOptions, batch_solve_dense
     model, d = fixture(name)
@@ -110,3 +119,38 @@ def test_zip_deep_feeders_thread_per_case_kernel(n_buses, kmax):
     assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
     fin = np.isfinite(res) & mask
     assert np.allclose(out.residuals[fin], res[fin], rtol=1e-3, atol=1e-12)
+
+
+@pytest.mark.parametrize("n_buses,loops", [(3, 1), (40, 6), (301, 30), (1001, 40)])
+def test_zip_meshed_vs_oracle(n_buses, loops):
+    """Meshed Y_dd (tie branches between demand buses): the per-case fixed-
+    pattern LU kernel (tpf_sparse_zip_lu_c128) against the oracle's per-case
+    splu route; zero-load and infeasible cases included."""
+    from paper_2403_04578_b200 import (Branch, GenSpec, LoadMatrix, NetworkModel, SolveOptions, ZipCoefficients,
+                                       batch_solve_dense, build_network, gen_scenarios)
+    from paper_2403_04578_b200.sparse import tree_parents
+    spec = GenSpec(n_buses=n_buses, seed=11, load_scale=2.0)
+    base = build_network(spec)
+    b = base.n_demand
+    rng = np.random.default_rng(n_buses)
+    branches = list(base.branches)
+    for _ in range(loops):
+        i, j = (int(x) for x in rng.choice(np.arange(1, n_buses), 2, replace=False))
+        branches.append(Branch(from_bus=i, to_bus=j, r=0.02, x=0.03))
+    w = rng.dirichlet([1.0, 1.0, 2.0], size=b)
+    z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
+    model = NetworkModel.from_branches(branches, n_buses, slack=base.slack, zip_coeffs=z)
+    if n_buses > 3:
+        assert tree_parents(model.admittance.y_dd) is None
+    tau = 150
+    S = gen_scenarios(model, tau, spec).values.copy()
+    S[:, 1] = 0.0
+    S[:, 2] *= 500.0
+    opts = SolveOptions(max_iterations=40)
+    out = batch_solve_dense(model, LoadMatrix(S), opts)
+    V, n, mask, res, it = orc.dense_zip_batch(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                              z.alpha_z, z.alpha_i, z.alpha_p, S, max_iter=40)
+    assert np.array_equal(out.converged_mask, mask)
+    assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
+    assert abs(out.iterations - it) <= 1
+    assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
