@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    p.add_argument("--dtype", choices=["c128", "c64"], default="c128",
+                   help="c64: the complex64 twin (FP32 SIMT, tol 1e-6), reported as its own line")
     p.add_argument("--tau", type=int, default=None, help="override tau (testing only)")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,7 +248,7 @@ def run_ours():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2403_04578_b200 import DenseOperator, SparseOperator, LoadMatrix, _capi
-    from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse
+    from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse, SolveOptions
     from paper_2403_04578_b200._device import residual_and_summary
 
     n_buses = CONFIGS[ARGS.config][0]
@@ -257,7 +259,14 @@ def run_ours():
     b = model.n_demand
     lib = _capi.load()
     peak_tf = ctypes_probe(lib)
-    op = DenseOperator(model, dev) if method == "dense" else SparseOperator(model, dev)
+    c64 = ARGS.dtype == "c64"
+    edt = np.complex64 if c64 else None
+    tdt = torch.complex64 if c64 else torch.complex128
+    if c64 and method == "dense" and b > 104:
+        raise SystemExit("bench: the dense complex64 twin covers b <= 104")
+    # c64: FP32 cannot resolve tol = 1e-10 (DESIGN 4.3b); the c64 bar is tol 1e-6, residual 1e-3
+    opts = SolveOptions(tolerance=1e-6, residual_tolerance=1e-3) if c64 else SolveOptions()
+    op = DenseOperator(model, dev, dtype=edt) if method == "dense" else SparseOperator(model, dev, dtype=edt)
     if scenarios:
         from paper_2403_04578_b200 import GenSpec
         from paper_2403_04578_b200.synth import gen_scenarios_device
@@ -270,8 +279,9 @@ def run_ours():
         S_list = [gen_scenarios_device(model, tau, lspec, device=dev)]
     else:
         S_list = [torch.from_numpy(loads.values).to(dev)]
+    S_list = [Sk.to(tdt) for Sk in S_list]
     S = S_list[0]
-    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    V = torch.empty((b, tau), dtype=tdt, device=dev)
     iters_list = [torch.empty(tau, dtype=torch.int32, device=dev) for _ in S_list]  # one per scenario batch
     iters = iters_list[0]
     stream = torch.cuda.current_stream(dev)
@@ -286,12 +296,13 @@ def run_ours():
         if ev:
             ev[0].record(stream)
         if fused:  # sparse: residual post-check fused into the solve kernel
-            op.solve(Sk, V=V, iters=itk, resid=post[0])
+            op.solve(Sk, opts, V=V, iters=itk, resid=post[0])
         else:
-            op.solve(Sk, V=V, iters=itk)
+            op.solve(Sk, opts, V=V, iters=itk)
         if ev:
             ev[1].record(stream)
-        return residual_and_summary(op.contract, Sk, V, itk, 1e-8, dev, csr=csr, out=post, have_resid=fused)
+        return residual_and_summary(op.contract, Sk, V, itk, opts.residual_tolerance, dev, csr=csr, out=post,
+                                    have_resid=fused)
 
     for _ in range(ARGS.warmup):
         step()
@@ -348,7 +359,16 @@ def run_ours():
         total_cases = tau
     value = total_cases * ARGS.steps / (ms * 1e-3)
 
-    if method == "dense":
+    if c64 and method == "dense":
+        alg = 8.0 * b * b * sum_n
+        achieved = alg / (kms * 1e-3) / 1e12
+        peak32 = fp32_peak(local)
+        roofline = dict(bound="fp32", pipe="FP32 FFMA (SIMT; no FP32-exact tensor-core path on sm_100a)",
+                        achieved=achieved, peak=peak32, unit="TFLOP/s", frac=achieved / peak32, traffic=None,
+                        kernel="dense_c64_kernel", kernel_ms=kms,
+                        peak_source="nominal: SMs x 128 FP32 lanes x 2 flop x max SM clock",
+                        algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch")
+    elif method == "dense":
         alg = 8.0 * b * b * sum_n  # FLOP_alg = 8 b^2 sum_j n_j
         achieved = alg / (kms * 1e-3) / 1e12
         roofline = dict(bound="tensor", pipe="FP64 DMMA (mma.sync m8n8k4)", achieved=achieved, peak=peak_tf, unit="TFLOP/s",
@@ -363,8 +383,11 @@ def run_ours():
         alg = 48.0 * b * sum_n  # BYTES_alg = 48 b sum_j n_j
         achieved = alg / (kms * 1e-3) / 1e9
         peak = measured_hbm()
-        roofline = dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                        traffic=traffic_from_profiles(op.kernel, tau), kernel=op.kernel,
+        if c64:
+            alg /= 2.0  # 8-byte complex64 elements
+        roofline = dict(bound="hbm", achieved=achieved * (0.5 if c64 else 1.0), peak=peak, unit="GB/s",
+                        frac=achieved * (0.5 if c64 else 1.0) / peak,
+                        traffic=None if c64 else traffic_from_profiles(op.kernel, tau), kernel=op.kernel,
                         kernel_ms=kms, peak_source="MEASURED_PEAKS.json hbm_gbs",
                         algorithmic=f"48*b*sum(n_j) = {alg:.4e} bytes per launch",
                         compulsory=dict(bytes=32.0 * b * tau, gbs=32.0 * b * tau / (kms * 1e-3) / 1e9,
@@ -373,7 +396,8 @@ def run_ours():
 
     e2e = None
     if not ARGS.no_e2e:
-        e2e = run_e2e(model, loads, method, dev, batch_solve_dense, batch_solve_sparse, LoadMatrix, world)
+        e2e = run_e2e(model, loads, method, dev, batch_solve_dense, batch_solve_sparse, LoadMatrix, world,
+                      dtype=edt, opts=opts)
 
     cpu = None
     if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
@@ -382,8 +406,8 @@ def run_ours():
     if rank == 0:
         line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=ARGS.steps,
                     warmup=ARGS.warmup, ms_per_step=ms / ARGS.steps, higher_is_better=True,
-                    scaling="weak", vs_baseline=None, dtype="c128", data="synthetic",
-                    config=dict(workload=desc, b=b, tau_per_gpu=tau, method=method,
+                    scaling="weak", vs_baseline=None, dtype=ARGS.dtype, data="synthetic",
+                    config=dict(workload=desc + (" [complex64 twin, tol 1e-6]" if c64 else ""), b=b, tau_per_gpu=tau, method=method,
                                 loads="device generator (synth.gen_scenarios_device)" if device_gen
                                 else "host generator, bit-identical to tpflow.gen_scenarios",
                                 sum_iterations=sum_n, batch_iterations=int(summ[0]),
@@ -452,23 +476,38 @@ def measured_hbm():
         return 6650.0  # B200_PROFILING.md fallback
 
 
-def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world):
+def fp32_peak(local):
+    """Nominal FP32 FFMA peak (TFLOP/s) at the GPU's max SM clock."""
+    import torch
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    try:
+        mhz = float(subprocess.check_output(["nvidia-smi", "-i", str(local), "--query-gpu=clocks.max.sm",
+                                             "--format=csv,noheader,nounits"], text=True).split()[0])
+    except (OSError, subprocess.CalledProcessError, ValueError, IndexError):
+        mhz = 1965.0
+    return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world, dtype=None, opts=None):
     """Public API from pinned host memory; H2D/D2H inside the timed region."""
     import torch
     import torch.distributed as dist
-    pinned = torch.from_numpy(loads.values).pin_memory()
-    host = LoadMatrix(pinned.numpy())
+    vals = loads.values if dtype is None else np.ascontiguousarray(loads.values, dtype=dtype)  # caller's c64 data
+    pinned = torch.from_numpy(vals).pin_memory()
+    # complex64: the caller's complex64 array goes in as is (batch_solve_*(..., dtype=complex64))
+    host = LoadMatrix(pinned.numpy()) if dtype is None else pinned.numpy()
     solver = bsd if method == "dense" else bss
     out = None
+    kw = {} if dtype is None else dict(dtype=dtype, opts=opts)
     for _ in range(3):  # populate torch's pinned-host cache exactly as the timed loop uses it
-        out = solver(model, host, device=dev)
+        out = solver(model, host, device=dev, **kw)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     ts = []
     for _ in range(max(1, ARGS.steps)):
         t0 = time.perf_counter()
-        out = solver(model, host, device=dev)
+        out = solver(model, host, device=dev, **kw)
         torch.cuda.synchronize(dev)
         ts.append(time.perf_counter() - t0)
     t = float(np.mean(ts))
@@ -477,8 +516,9 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
     b, tau = loads.values.shape
-    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * 16), cases_per_step=tau,
-                d2h_bytes_per_step=int(b * tau * 16 + tau * (4 + 8 + 1)),
+    esz = 8 if dtype is not None and np.dtype(dtype) == np.complex64 else 16
+    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * esz), cases_per_step=tau,
+                d2h_bytes_per_step=int(b * tau * esz + tau * (4 + 8 + 1)),
                 ms_per_step=t * 1e3, api=f"paper_2403_04578_b200.batch_solve_{method}(model, LoadMatrix)",
                 iterations=int(out.iterations))
 

@@ -19,6 +19,7 @@
 // The residual post-check of a c64 solution is evaluated in FP64
 // (tpf_residual_c64).
 #include <climits>
+#include <cstdlib>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -66,7 +67,7 @@ __device__ __forceinline__ float2 recip32(float2 s, float2 v) {
 // nodes, loads and iterate), so 8 warps per SM hide the shared-memory latency
 // of the FFMA loop; only U is exchanged (shared memory, __syncwarp).
 template <int BP>
-__global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const DenseC64Args a) {
+__global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_halves_kernel(const DenseC64Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = a.b;
   constexpr int bp = BP;
@@ -171,6 +172,176 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
         cid = c;
         n_it = 0;
         load_case(cid);
+      }
+    }
+  }
+}
+
+// Default dense c64 kernel: 256 threads = 2 groups of 4 warps; a group owns
+// 64 slot pairs (slots p and p + 64, p = lane of the group's warps) and warp q
+// of the group owns node quarter q (NC nodes).  Every K^T read of a warp is
+// then one broadcast address (one wavefront for two complex entries) and is
+// reused by two slots, so each LDS.128 of K feeds 16 FFMAs instead of 8, and
+// the U reads are contiguous.  The four quarters of a slot meet at a named
+// barrier of their group (bar 1 + group, 128 threads) after U is formed and
+// after the step test; the refill ids go through shared memory.  Same
+// arithmetic per case as dense_c64_halves_kernel (bitwise the same V').
+template <int NC>
+__global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const DenseC64Args a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_cid[kC64Threads];
+  __shared__ unsigned char s_small[4][kC64Threads];
+  const int b = a.b;
+  constexpr int bp = 4 * NC;
+  float2* kt = reinterpret_cast<float2*>(smem_raw);  // [b][bp]: kt[k][n] = K[n][k]
+  float2* w = kt + size_t(b) * bp;                   // [bp]
+  float2* us = w + bp;                               // [b][128]: U of each slot
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int q = warp & 3, grp = warp >> 2;
+  const int sA = grp * 32 + lane, sB = sA + 64;
+  for (int idx = t; idx < b * bp; idx += 2 * kC64Threads) {
+    const int k = idx / bp, n = idx % bp;
+    kt[idx] = n < b ? a.K[size_t(n) * b + k] : make_float2(0.f, 0.f);
+  }
+  for (int n = t; n < bp; n += 2 * kC64Threads) w[n] = n < b ? a.W[n] : make_float2(0.f, 0.f);
+  __syncthreads();
+
+  const int64_t slots = int64_t(gridDim.x) * kC64Threads;
+  const int64_t gA = int64_t(blockIdx.x) * kC64Threads + sA;
+  float2* vsA = a.scratch + gA;               // iterate, slot-major
+  float2* ssA = a.scratch + slots * b + gA;   // loads
+  float2* vsB = vsA + 64;
+  float2* ssB = ssA + 64;
+  const int n0 = q * NC;
+  const int k0 = min(b, n0), k1 = min(b, n0 + NC);
+  auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(4 * 32) : "memory"); };
+  // quarter 0 claims the next case ids of the group's retiring slots; the
+  // other quarters read them after the group barrier
+  auto claim = [&](bool wantA, bool wantB, int& cA, int& cB) {
+    if (q == 0) {
+      if (wantA) {
+        const unsigned long long x = atomicAdd(a.counter, 1ull);
+        s_cid[sA] = x < (unsigned long long)a.tau ? int(x) : INT_MAX;
+      }
+      if (wantB) {
+        const unsigned long long x = atomicAdd(a.counter, 1ull);
+        s_cid[sB] = x < (unsigned long long)a.tau ? int(x) : INT_MAX;
+      }
+    }
+    gbar();
+    if (wantA) cA = s_cid[sA];
+    if (wantB) cB = s_cid[sB];
+  };
+  auto load_case = [&](int cid, float2* ss, float2* vs) {
+    if (cid == INT_MAX) return;
+    const int64_t sb = int64_t(cid) * a.s_case;
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      ss[k * slots] = a.S[k * a.s_node + sb];
+      vs[k * slots] = a.v_flat;
+    }
+  };
+  auto retire = [&](int cid, int n_it, const float2* vs) {
+    const int64_t vb = int64_t(cid) * a.v_case;
+#pragma unroll 4
+    for (int n = k0; n < k1; ++n) a.V[n * a.v_node + vb] = vs[n * slots];
+    if (q == 0) a.iters[cid] = n_it;
+  };
+  // U is formed with every load of a half-quarter issued before the first
+  // dependent store (one memory round trip per half, not one per node)
+  constexpr int kH = (NC + 1) / 2;  // U formed in two halves of the quarter (register budget)
+  auto form_u = [&](const float2* ss, const float2* vs, int slot) {
+#pragma unroll
+    for (int c0 = 0; c0 < NC; c0 += kH) {
+      float2 sv[kH], vv[kH];
+#pragma unroll
+      for (int c = 0; c < kH; ++c)
+        if (c0 + c < NC && n0 + c0 + c < b) {
+          sv[c] = ss[(n0 + c0 + c) * slots];
+          vv[c] = vs[(n0 + c0 + c) * slots];
+        }
+#pragma unroll
+      for (int c = 0; c < kH; ++c)
+        if (c0 + c < NC && n0 + c0 + c < b) us[(n0 + c0 + c) * kC64Threads + slot] = recip32(sv[c], guard32(vv[c]));
+    }
+  };
+  int cA = INT_MAX, cB = INT_MAX;
+  claim(true, true, cA, cB);
+  load_case(cA, ssA, vsA);
+  load_case(cB, ssB, vsB);
+  int itA = 0, itB = 0;
+  while (__any_sync(0xffffffffu, cA != INT_MAX || cB != INT_MAX)) {  // uniform over the group
+    // ---- U = S* / conj(guarded v) on this quarter's nodes of both slots ----
+    form_u(ssA, vsA, sA);
+    form_u(ssB, vsB, sB);
+    gbar();
+    // ---- V' = W + K U on this quarter's nodes, two slots per K read ----
+    float arA[NC], aiA[NC], arB[NC], aiB[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const float2 wc = w[n0 + c];
+      arA[c] = wc.x;
+      aiA[c] = wc.y;
+      arB[c] = wc.x;
+      aiB[c] = wc.y;
+    }
+#pragma unroll 2
+    for (int k = 0; k < b; ++k) {
+      const float2 uA = us[k * kC64Threads + sA];
+      const float2 uB = us[k * kC64Threads + sB];
+      const float4* kr = reinterpret_cast<const float4*>(kt + size_t(k) * bp + n0);
+#pragma unroll
+      for (int c = 0; c < NC; c += 2) {
+        const float4 kk = kr[c / 2];  // K[n0+c][k], K[n0+c+1][k] (one broadcast address per warp)
+        arA[c] = fmaf(kk.x, uA.x, fmaf(-kk.y, uA.y, arA[c]));
+        aiA[c] = fmaf(kk.x, uA.y, fmaf(kk.y, uA.x, aiA[c]));
+        arA[c + 1] = fmaf(kk.z, uA.x, fmaf(-kk.w, uA.y, arA[c + 1]));
+        aiA[c + 1] = fmaf(kk.z, uA.y, fmaf(kk.w, uA.x, aiA[c + 1]));
+        arB[c] = fmaf(kk.x, uB.x, fmaf(-kk.y, uB.y, arB[c]));
+        aiB[c] = fmaf(kk.x, uB.y, fmaf(kk.y, uB.x, aiB[c]));
+        arB[c + 1] = fmaf(kk.z, uB.x, fmaf(-kk.w, uB.y, arB[c + 1]));
+        aiB[c + 1] = fmaf(kk.z, uB.y, fmaf(kk.w, uB.x, aiB[c + 1]));
+      }
+    }
+    // ---- step test against the old iterate, new iterate out ----
+    bool smA = true, smB = true;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int n = n0 + c;
+      if (n < b) {
+        const float2 va = guard32(vsA[n * slots]);
+        const float dra = arA[c] - va.x, dia = aiA[c] - va.y;
+        if (!(fmaf(dra, dra, dia * dia) < a.tol2)) smA = false;  // NaN never passes
+        vsA[n * slots] = make_float2(arA[c], aiA[c]);
+        const float2 vb = guard32(vsB[n * slots]);
+        const float drb = arB[c] - vb.x, dib = aiB[c] - vb.y;
+        if (!(fmaf(drb, drb, dib * dib) < a.tol2)) smB = false;
+        vsB[n * slots] = make_float2(arB[c], aiB[c]);
+      }
+    }
+    s_small[q][sA] = smA;
+    s_small[q][sB] = smB;
+    gbar();  // also: every quarter has finished reading U
+    smA = s_small[0][sA] & s_small[1][sA] & s_small[2][sA] & s_small[3][sA];
+    smB = s_small[0][sB] & s_small[1][sB] & s_small[2][sB] & s_small[3][sB];
+    ++itA;
+    ++itB;
+    const bool doneA = cA != INT_MAX && (smA || itA >= a.max_iter);
+    const bool doneB = cB != INT_MAX && (smB || itB >= a.max_iter);
+    if (doneA) retire(cA, itA, vsA);
+    if (doneB) retire(cB, itB, vsB);
+    if (__any_sync(0xffffffffu, doneA || doneB)) {  // same answer in the group's 4 warps
+      int nA = cA, nB = cB;
+      claim(doneA, doneB, nA, nB);
+      if (doneA) {
+        cA = nA;
+        itA = 0;
+        load_case(cA, ssA, vsA);
+      }
+      if (doneB) {
+        cB = nB;
+        itB = 0;
+        load_case(cB, ssB, vsB);
       }
     }
   }
@@ -310,10 +481,25 @@ extern "C" int tpf_dense_fpi_c64(int64_t tau, int32_t b, const float* S, int64_t
   const int64_t grid = c64_grid(tau);
   cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
   if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
-  const int bp = (b + kC64Chunk - 1) / kC64Chunk * kC64Chunk;
+  // default: quarter kernel (two slots per thread); TPF_C64_HALVES=1 runs the
+  // previous one-slot-per-thread kernel (A/B only)
+  static const bool halves = [] {
+    const char* e = getenv("TPF_C64_HALVES");
+    return e && e[0] == '1';
+  }();
+  int bp;
+  void (*kern)(const DenseC64Args);
+  if (halves) {
+    bp = (b + kC64Chunk - 1) / kC64Chunk * kC64Chunk;
+    kern = bp == 26 ? dense_c64_halves_kernel<26> : bp == 52 ? dense_c64_halves_kernel<52>
+         : bp == 78 ? dense_c64_halves_kernel<78> : dense_c64_halves_kernel<104>;
+  } else {  // nodes per quarter
+    const int nc = b <= 32 ? 8 : b <= 40 ? 10 : b <= 56 ? 14 : b <= 80 ? 20 : 26;
+    bp = 4 * nc;
+    kern = nc == 8 ? dense_c64_kernel<8> : nc == 10 ? dense_c64_kernel<10> : nc == 14 ? dense_c64_kernel<14>
+         : nc == 20 ? dense_c64_kernel<20> : dense_c64_kernel<26>;
+  }
   const size_t smem = (size_t(b) * bp + bp + size_t(b) * kC64Threads) * sizeof(float2);
-  auto kern = bp == 26 ? dense_c64_kernel<26> : bp == 52 ? dense_c64_kernel<52>
-            : bp == 78 ? dense_c64_kernel<78> : dense_c64_kernel<104>;
   err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_c64)", err);
   DenseC64Args a;

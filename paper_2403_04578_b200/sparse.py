@@ -37,7 +37,7 @@ from ._device import (ModelContract, complex_strides, engine_dtype, host_csr, ho
                       loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
                       stream_ptr)
 from ._types import LoadMatrix, MemoryGuardError, SingularSystemError, SolveOptions, VoltageBatch
-from .dense import finish
+from .dense import as_load_matrix, finish
 
 __all__ = ["batch_solve_sparse", "factorization_count", "factorize_ydd", "TreeLU",
            "TreeSchedule", "tree_schedule", "SparseOperator", "DEFAULT_MAX_BLOCK_NNZ"]
@@ -607,8 +607,7 @@ def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptio
     result as one device).  ``dtype=numpy.complex64`` runs the c64 twin (FP32
     general CSR kernel, one device; pass a tolerance >= ~1e-6).
     """
-    if not isinstance(loads, LoadMatrix):
-        loads = LoadMatrix(np.asarray(getattr(loads, "values", loads)))
+    loads = as_load_matrix(loads, dtype)
     if not model.zip.is_constant_power:
         raise ValueError("the sparse batch path supports constant-power loads only")
     if loads.n_demand != model.n_demand:

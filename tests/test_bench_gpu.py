@@ -44,3 +44,16 @@ def test_bench_two_ranks_plumbing():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+
+
+def test_bench_c64_line():
+    """The complex64 twin is reported as its own line (north_star: "a complex64 mode reported separately")."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "c1", "--dtype", "c64", "--steps", "3",
+                        "--warmup", "3", "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["dtype"] == "c64" and d["value"] > 0
+    assert d["roofline"]["kernel"] == "dense_c64_kernel" and 0 < d["roofline"]["frac"] < 1
+    assert d["config"]["converged"] == d["config"]["tau_per_gpu"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 34 * 8760 * 8

@@ -69,3 +69,31 @@ def test_c64_dense_large_b_is_unsupported():
     model, loads = _case(106, 20)
     with pytest.raises(NotImplementedError):
         batch_solve_dense(model, loads, _opts(), dtype=np.complex64)
+
+
+@pytest.mark.parametrize("method", ["dense", "sparse"])
+def test_c64_array_passthrough_same_bits(method):
+    """A complex64 array handed to the c64 twin is used as is; same bits as the
+    LoadMatrix (complex128) route, whose values round to the same complex64."""
+    from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse, LoadMatrix
+    solver = batch_solve_dense if method == "dense" else batch_solve_sparse
+    model, loads = _case(101, 900)
+    a = solver(model, LoadMatrix(loads.values), _opts(), dtype=np.complex64)
+    b = solver(model, loads.values.astype(np.complex64), _opts(), dtype=np.complex64)
+    assert a.values.dtype == b.values.dtype == np.complex64
+    assert np.array_equal(a.values, b.values) and np.array_equal(a.iterations_per_case, b.iterations_per_case)
+    assert np.array_equal(a.converged_mask, b.converged_mask) and a.iterations == b.iterations
+
+
+def test_c64_quarter_kernel_node_counts():
+    """Every quarter width of the default c64 kernel (b <= 32, 40, 56, 80, 104) and
+    an empty last quarter (b = 5: quarters of 8 nodes)."""
+    from paper_2403_04578_b200 import solve_batch
+    for n_buses in (6, 33, 41, 57, 81, 105):
+        model, loads = _case(n_buses, 300, seed=n_buses)
+        out = solve_batch("dense", model, loads, _opts(), dtype=np.complex64)
+        V, n, mask, _ = orc.dense_per_case(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                           loads.values, tol=TOL, residual_tol=RTOL)
+        assert out.converged_mask.all()
+        assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
+        assert np.abs(out.values.astype(np.complex128) - V).max() < 2e-5
