@@ -364,7 +364,8 @@ def run_ours():
         achieved = alg / (kms * 1e-3) / 1e12
         peak32 = fp32_peak(local)
         roofline = dict(bound="fp32", pipe="FP32 FFMA (SIMT; no FP32-exact tensor-core path on sm_100a)",
-                        achieved=achieved, peak=peak32, unit="TFLOP/s", frac=achieved / peak32, traffic=None,
+                        achieved=achieved, peak=peak32, unit="TFLOP/s", frac=achieved / peak32,
+                        traffic=traffic_from_profiles("dense_c64_kernel", tau),
                         kernel="dense_c64_kernel", kernel_ms=kms,
                         peak_source="nominal: SMs x 128 FP32 lanes x 2 flop x max SM clock",
                         algorithmic=f"8*b^2*sum(n_j) = {alg:.4e} flop per launch")
