@@ -209,9 +209,7 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
   const int64_t slots = int64_t(gridDim.x) * kC64Threads;
   const int64_t gA = int64_t(blockIdx.x) * kC64Threads + sA;
   float2* vsA = a.scratch + gA;               // iterate, slot-major
-  float2* ssA = a.scratch + slots * b + gA;   // loads
   float2* vsB = vsA + 64;
-  float2* ssB = ssA + 64;
   const int n0 = q * NC;
   const int k0 = min(b, n0), k1 = min(b, n0 + NC);
   auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(4 * 32) : "memory"); };
@@ -232,32 +230,28 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
     if (wantA) cA = s_cid[sA];
     if (wantB) cB = s_cid[sB];
   };
-  auto load_case = [&](int cid, float2* ss, float2* vs) {
+  // refill = flat start only: S is read in place by form_u (L2-resident
+  // while the case is active) and V' is written by the step test of the
+  // iteration that may retire the slot, so neither end copies through the
+  // scratch (such a copy waits one memory round trip per node)
+  auto load_case = [&](int cid, float2* vs) {
     if (cid == INT_MAX) return;
-    const int64_t sb = int64_t(cid) * a.s_case;
 #pragma unroll 4
-    for (int k = k0; k < k1; ++k) {
-      ss[k * slots] = a.S[k * a.s_node + sb];
-      vs[k * slots] = a.v_flat;
-    }
-  };
-  auto retire = [&](int cid, int n_it, const float2* vs) {
-    const int64_t vb = int64_t(cid) * a.v_case;
-#pragma unroll 4
-    for (int n = k0; n < k1; ++n) a.V[n * a.v_node + vb] = vs[n * slots];
-    if (q == 0) a.iters[cid] = n_it;
+    for (int k = k0; k < k1; ++k) vs[k * slots] = a.v_flat;
   };
   // U is formed with every load of a half-quarter issued before the first
   // dependent store (one memory round trip per half, not one per node)
   constexpr int kH = (NC + 1) / 2;  // U formed in two halves of the quarter (register budget)
-  auto form_u = [&](const float2* ss, const float2* vs, int slot) {
+  auto form_u = [&](int cid, const float2* vs, int slot) {
+    const bool live = cid != INT_MAX;
+    const int64_t sb = int64_t(live ? cid : 0) * a.s_case;
 #pragma unroll
     for (int c0 = 0; c0 < NC; c0 += kH) {
       float2 sv[kH], vv[kH];
 #pragma unroll
       for (int c = 0; c < kH; ++c)
         if (c0 + c < NC && n0 + c0 + c < b) {
-          sv[c] = ss[(n0 + c0 + c) * slots];
+          sv[c] = live ? __ldg(a.S + (n0 + c0 + c) * a.s_node + sb) : make_float2(0.f, 0.f);
           vv[c] = vs[(n0 + c0 + c) * slots];
         }
 #pragma unroll
@@ -267,13 +261,13 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
   };
   int cA = INT_MAX, cB = INT_MAX;
   claim(true, true, cA, cB);
-  load_case(cA, ssA, vsA);
-  load_case(cB, ssB, vsB);
+  load_case(cA, vsA);
+  load_case(cB, vsB);
   int itA = 0, itB = 0;
   while (__any_sync(0xffffffffu, cA != INT_MAX || cB != INT_MAX)) {  // uniform over the group
     // ---- U = S* / conj(guarded v) on this quarter's nodes of both slots ----
-    form_u(ssA, vsA, sA);
-    form_u(ssB, vsB, sB);
+    form_u(cA, vsA, sA);
+    form_u(cB, vsB, sB);
     gbar();
     // ---- V' = W + K U on this quarter's nodes, two slots per K read ----
     float arA[NC], aiA[NC], arB[NC], aiB[NC];
@@ -319,6 +313,20 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
         vsB[n * slots] = make_float2(arB[c], aiB[c]);
       }
     }
+    // V' out when this iteration can retire the slot (this quarter passed the
+    // test, or the cap is reached); a quarter whose slot goes on rewrites it later
+    if (cA != INT_MAX && (smA || itA + 1 >= a.max_iter)) {
+      const int64_t vb = int64_t(cA) * a.v_case;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (n0 + c < b) a.V[(n0 + c) * a.v_node + vb] = make_float2(arA[c], aiA[c]);
+    }
+    if (cB != INT_MAX && (smB || itB + 1 >= a.max_iter)) {
+      const int64_t vb = int64_t(cB) * a.v_case;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (n0 + c < b) a.V[(n0 + c) * a.v_node + vb] = make_float2(arB[c], aiB[c]);
+    }
     s_small[q][sA] = smA;
     s_small[q][sB] = smB;
     gbar();  // also: every quarter has finished reading U
@@ -328,20 +336,22 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_kernel(const Den
     ++itB;
     const bool doneA = cA != INT_MAX && (smA || itA >= a.max_iter);
     const bool doneB = cB != INT_MAX && (smB || itB >= a.max_iter);
-    if (doneA) retire(cA, itA, vsA);
-    if (doneB) retire(cB, itB, vsB);
+    if (q == 0) {  // retire: V' is already out
+      if (doneA) a.iters[cA] = itA;
+      if (doneB) a.iters[cB] = itB;
+    }
     if (__any_sync(0xffffffffu, doneA || doneB)) {  // same answer in the group's 4 warps
       int nA = cA, nB = cB;
       claim(doneA, doneB, nA, nB);
       if (doneA) {
         cA = nA;
         itA = 0;
-        load_case(cA, ssA, vsA);
+        load_case(cA, vsA);
       }
       if (doneB) {
         cB = nB;
         itB = 0;
-        load_case(cB, ssB, vsB);
+        load_case(cB, vsB);
       }
     }
   }
