@@ -266,3 +266,18 @@ def test_reference_model_objects_are_accepted_as_is():
     assert (mine.y_dd != theirs.y_dd).nnz == 0
     assert np.array_equal(mine.src, theirs.src) and mine.v_s == theirs.v_s
     assert theirs.constant_power
+
+
+def test_as_load_matrix_complex64_passthrough():
+    """complex64 arrays reach the c64 twin as is; everything else becomes the
+    reference's complex128 LoadMatrix (dense.py:57-78)."""
+    import numpy as np
+    from paper_2403_04578_b200 import LoadMatrix
+    from paper_2403_04578_b200.dense import as_load_matrix
+    a64 = (np.arange(12, dtype=np.float32).reshape(3, 4) * (1 + 1j)).astype(np.complex64)
+    lm = as_load_matrix(a64, np.complex64)
+    assert lm.values is a64 and lm.n_demand == 3 and lm.tau == 4 and lm.dims == (4,)
+    assert as_load_matrix(a64).values.dtype == np.complex128  # c128 engine: the reference's conversion
+    assert as_load_matrix(a64.astype(np.complex128), np.complex64).values.dtype == np.complex128
+    ref = LoadMatrix(a64)
+    assert as_load_matrix(ref, np.complex64) is ref
