@@ -12,6 +12,8 @@
 // outputs (iters, residuals, mask) stay device-resident until one final
 // summary kernel and copy.  Pageable host buffers are page-locked in place for
 // the duration of the call (cudaHostRegister) so every copy is a DMA.
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -296,11 +298,28 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
   // device chunk strides mirror the host layout so each chunk copy is one 2-D DMA
   const int64_t dsn_S = LS.case_contig ? chunk : 1, dsc_S = LS.case_contig ? 1 : b;
   const int64_t dsn_V = LV.case_contig ? chunk : 1, dsc_V = LV.case_contig ? 1 : b;
-  const int64_t nchunks = (tau + chunk - 1) / chunk;
+  // chunk boundaries: with more than 4 chunks the first and the last are a
+  // quarter chunk, which shortens the pipeline fill (first H2D, nothing to
+  // overlap it with) and drain (last D2H); the rest are full chunks
+  std::vector<int64_t> bnd{0};
+  {
+    static const bool no_ramp = [] {  // TPF_PIPE_NORAMP=1: equal chunks (A/B only)
+      const char* e = getenv("TPF_PIPE_NORAMP");
+      return e && e[0] == '1';
+    }();
+    const int64_t small =
+        tau > 4 * chunk && !no_ramp ? std::max<int64_t>(chunk / 4 / 256 * 256, 256) : chunk;
+    int64_t at = 0;
+    if (small < chunk) bnd.push_back(at = small);
+    while (tau - at > chunk + (small < chunk ? small : 0)) bnd.push_back(at += chunk);
+    if (small < chunk && tau - at > small) bnd.push_back(at = tau - small);
+    if (at < tau) bnd.push_back(tau);
+  }
+  const int64_t nchunks = int64_t(bnd.size()) - 1;
   int rc = TPF_OK;
   for (int64_t c = 0; c < nchunks && rc == TPF_OK; ++c) {
     const int k = int(c & 1);
-    const int64_t lo = c * chunk, n = (tau - lo < chunk) ? tau - lo : chunk;
+    const int64_t lo = bnd[c], n = bnd[c + 1] - bnd[c];
     if (c >= 2) cudaStreamWaitEvent(sin, ss.comp_done[k], 0);
     if (stage_s) {
       // staging slot k was last read by the H2D of chunk c - 2
