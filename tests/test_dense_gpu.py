@@ -340,3 +340,27 @@ def test_pageable_staging_matches_pinned(golden, order):
     assert np.array_equal(a.values, b.values)
     assert np.array_equal(a.iterations_per_case, b.iterations_per_case)
     assert np.array_equal(a.residuals, b.residuals)
+
+
+@pytest.mark.parametrize("method", ["dense", "sparse"])
+@pytest.mark.parametrize("layout", ["node_major", "case_major"])
+@pytest.mark.parametrize("tau,chunk", [(2000, 300), (1201, 300), (4097, 1024)])
+def test_host_pipeline_ragged_ramp_chunks_bitwise(tau, chunk, layout, method):
+    """Quarter-size first/last chunks (tau > 4*chunk) and a ragged tail, staged from pageable
+    host memory in both host layouts, == one device-resident solve, bit for bit."""
+    import torch
+    from paper_2403_04578_b200 import (GenSpec, LoadMatrix, build_network, gen_scenarios,
+                                       batch_solve_dense, batch_solve_sparse)
+    solver = batch_solve_dense if method == "dense" else batch_solve_sparse
+    spec = GenSpec(n_buses=101, seed=0)
+    model = build_network(spec)
+    S = gen_scenarios(model, tau, GenSpec(n_buses=101, seed=7)).values
+    if layout == "case_major":
+        S = np.asfortranarray(S)
+    host = solver(model, LoadMatrix(S), chunk_cases=chunk)
+    dev = solver(model, LoadMatrix(np.ascontiguousarray(S)), return_on_device=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.values, dev.values.cpu().numpy())
+    assert np.array_equal(host.iterations_per_case, dev.iterations_per_case.cpu().numpy())
+    assert np.array_equal(host.converged_mask, dev.converged_mask.cpu().numpy())
+    assert host.iterations == dev.iterations
