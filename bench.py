@@ -59,6 +59,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--chunk-cases", type=int, default=0, help="e2e host-pipeline chunk (0 = library default)")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="time eager launches instead of a CUDA-graph replay of the step")
     return p.parse_args()
@@ -500,6 +501,8 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world, dtype=None, 
     solver = bsd if method == "dense" else bss
     out = None
     kw = {} if dtype is None else dict(dtype=dtype, opts=opts)
+    if ARGS.chunk_cases:
+        kw["chunk_cases"] = ARGS.chunk_cases
     for _ in range(3):  # populate torch's pinned-host cache exactly as the timed loop uses it
         out = solver(model, host, device=dev, **kw)
     torch.cuda.synchronize(dev)
@@ -518,10 +521,38 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world, dtype=None, 
         t = float(tt[0])
     b, tau = loads.values.shape
     esz = 8 if dtype is not None and np.dtype(dtype) == np.complex64 else 16
-    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=int(b * tau * esz), cases_per_step=tau,
-                d2h_bytes_per_step=int(b * tau * esz + tau * (4 + 8 + 1)),
+    h2d, d2h = int(b * tau * esz), int(b * tau * esz + tau * (4 + 8 + 1))
+    floor_ms = pcie_floor_ms(h2d, d2h, dev)
+    return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=h2d, cases_per_step=tau,
+                d2h_bytes_per_step=d2h,
                 ms_per_step=t * 1e3, api=f"paper_2403_04578_b200.batch_solve_{method}(model, LoadMatrix)",
-                iterations=int(out.iterations))
+                iterations=int(out.iterations),
+                pcie_floor=dict(ms=floor_ms, frac=floor_ms / (t * 1e3),
+                                how="copy-only: same H2D and D2H bytes, pinned host, one copy stream per "
+                                    "direction running concurrently, no compute; frac = floor / e2e"))
+
+
+def pcie_floor_ms(h2d: int, d2h: int, dev) -> float:
+    """The e2e roofline: the step's H2D and D2H bytes moved concurrently with nothing else."""
+    import torch
+    hi = torch.empty(h2d, dtype=torch.uint8, pin_memory=True)
+    ho = torch.empty(d2h, dtype=torch.uint8, pin_memory=True)
+    di = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    do = torch.empty(d2h, dtype=torch.uint8, device=dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ts = []
+    for i in range(4):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            di.copy_(hi, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            ho.copy_(do, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        if i:
+            ts.append(time.perf_counter() - t0)
+    del hi, ho, di, do
+    return float(np.min(ts)) * 1e3
 
 
 if __name__ == "__main__":

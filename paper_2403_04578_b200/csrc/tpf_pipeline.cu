@@ -307,8 +307,13 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
       const char* e = getenv("TPF_PIPE_NORAMP");
       return e && e[0] == '1';
     }();
+    static const int64_t div = [] {  // TPF_PIPE_RAMP_DIV: ramp chunk = chunk / div (A/B only)
+      const char* e = getenv("TPF_PIPE_RAMP_DIV");
+      const long v = e ? atol(e) : 0;
+      return int64_t(v >= 2 && v <= 64 ? v : 4);
+    }();
     const int64_t small =
-        tau > 4 * chunk && !no_ramp ? std::max<int64_t>(chunk / 4 / 256 * 256, 256) : chunk;
+        tau > 4 * chunk && !no_ramp ? std::max<int64_t>(chunk / div / 256 * 256, 256) : chunk;
     int64_t at = 0;
     if (small < chunk) bnd.push_back(at = small);
     while (tau - at > chunk + (small < chunk ? small : 0)) bnd.push_back(at += chunk);
