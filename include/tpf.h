@@ -75,22 +75,17 @@ int tpf_dense_fpi_c128(int64_t tau, int32_t b,
                        int32_t* iters, void* workspace, size_t workspace_bytes,
                        void* stream);
 
-/* The two b <= 104 kernels behind tpf_dense_fpi_c128 (same arguments; the
- * environment variable TPF_DENSE_KERNEL=pairs selects the second):
+/* The two b <= 104 kernels behind tpf_dense_fpi_c128 (same arguments, same
+ * bits; tpf_dense_fpi_c128 picks pairs for batches of at most two waves of
+ * ws slots, ws above; TPF_DENSE_KERNEL=pairs forces the second):
  *   _ws_    warp-specialised: per SM sub-partition one DMMA warp alternating
  *           between two slot groups and two elementwise warps (default);
- *   _solo_  8 independent warps, each owning 8 slots and all node blocks;
  *   _pairs_ pairs of warps sharing 8 slots, each doing GEMM and elementwise. */
 int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b,
                           const double* S, int64_t s_node_stride, int64_t s_case_stride,
                           const double* K, const double* W, double v_flat_re, double v_flat_im,
                           double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
                           int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
-int tpf_dense_solo_fpi_c128(int64_t tau, int32_t b,
-                            const double* S, int64_t s_node_stride, int64_t s_case_stride,
-                            const double* K, const double* W, double v_flat_re, double v_flat_im,
-                            double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
-                            int32_t* iters, void* workspace, size_t workspace_bytes, void* stream);
 int tpf_dense_pairs_fpi_c128(int64_t tau, int32_t b,
                              const double* S, int64_t s_node_stride, int64_t s_case_stride,
                              const double* K, const double* W, double v_flat_re, double v_flat_im,
@@ -188,7 +183,10 @@ int tpf_sparse_tree_max_ell_width(void);
  * rows = diagonal + tree edges (ELL as above).  step_met[j] = 1 when case j
  * stopped on the step test (or was a one-application case); *status = 1
  * if some case's B had a zero pivot (SingularSystemError in the reference).
- * workspace >= tpf_sparse_tree_zip_workspace_bytes(tau, b).              */
+ * workspace >= tpf_sparse_tree_zip_workspace_bytes(tau, b).
+ * All three ZIP entry points take v0: null = flat start v_flat for every
+ * node (fpi.py:130-131), else b complex values in ORIGINAL node order, the
+ * start of every case (opts.initial_voltage, fpi.py:141-145).            */
 /* The same ZIP route for radial feeders the tree kernel does not take (deep,
  * wide or > 5,120 nodes): one thread per case, nodes in leaf-first order
  * (orig = original node of position k, parent = position of k's parent or
@@ -199,7 +197,7 @@ size_t tpf_sparse_zip_chain_workspace_bytes(int64_t tau, int32_t b);
 int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* orig, const int32_t* parent,
                               const double* e, const double* ydiag, const double* alpha, const double* src,
                               const double* S, int64_t s_node_stride, int64_t s_case_stride,
-                              double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                              double v_flat_re, double v_flat_im, const double* v0, double tol, int32_t max_iter,
                               double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                               double* resid, uint8_t* step_met, int32_t* status,
                               void* workspace, size_t workspace_bytes, void* stream);
@@ -218,7 +216,7 @@ int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, const int32_t*
                            const int32_t* idx, const double* base, const double* alpha, const double* src,
                            const int32_t* y_row_ptr, const int32_t* y_col, const double* y_val,
                            const double* S, int64_t s_node_stride, int64_t s_case_stride,
-                           double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                           double v_flat_re, double v_flat_im, const double* v0, double tol, int32_t max_iter,
                            double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                            double* resid, uint8_t* step_met, int32_t* status,
                            void* workspace, size_t workspace_bytes, void* stream);
@@ -227,7 +225,7 @@ int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels,
                                  const int32_t* level_info, const int32_t* node_info, const double* node_coef,
                                  const double* alpha, const double* ydiag,
                                  const double* S, int64_t s_node_stride, int64_t s_case_stride,
-                                 double v_flat_re, double v_flat_im, double tol, int32_t max_iter,
+                                 double v_flat_re, double v_flat_im, const double* v0, double tol, int32_t max_iter,
                                  double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                                  int32_t ell_width, const int32_t* ell_col, const double* ell_val,
                                  double* resid, uint8_t* step_met, int32_t* status,

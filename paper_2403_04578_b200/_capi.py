@@ -35,9 +35,6 @@ SIGNATURES = {
     "tpf_dense_ws_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
         _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
-    "tpf_dense_solo_fpi_c128": (ctypes.c_int, [
-        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
-        _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
     "tpf_dense_pairs_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32,
         _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
@@ -77,17 +74,17 @@ SIGNATURES = {
     "tpf_sparse_tree_zip_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
     "tpf_sparse_zip_chain_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
     "tpf_sparse_zip_chain_c128": (ctypes.c_int, [
-        _c_i64, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl,
+        _c_i64, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_ptr,
         _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
     "tpf_sparse_zip_lu_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i32]),
     "tpf_sparse_zip_lu_c128": (ctypes.c_int, [
-        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
-        _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
-        _c_ptr, _c_sz, _c_ptr]),
-    "tpf_sparse_tree_zip_fpi_c128": (ctypes.c_int, [
-        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl,
-        _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
+        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64,
+        _c_i64, _c_dbl, _c_dbl, _c_ptr, _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_sz, _c_ptr]),
+    "tpf_sparse_tree_zip_fpi_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_ptr,
+        _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_sz,
+        _c_ptr]),
     "tpf_sparse_tree_ell_width": (ctypes.c_int, [_c_i32, _c_ptr]),
     "tpf_sparse_tree_build_ell": (ctypes.c_int, [_c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr]),
     "tpf_sparse_tree_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i64, _c_i64]),

@@ -6,6 +6,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import hashlib
+import threading
 
 import numpy as np
 import torch
@@ -149,17 +150,11 @@ def ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
-_WS: dict = {}
-
-
-def device_workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Grow-only per-device scratch reused across host-pipeline calls."""
-    ws = _WS.get(device)
-    if ws is None or ws.numel() < nbytes:
-        _WS.pop(device, None)
-        ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
-        _WS[device] = ws
-    return ws
+# Host-pipeline scratch, one grow-only buffer per (device, slot) and per
+# calling THREAD: the native pipelines release the GIL, so two Python threads
+# solving on one device must never carve the same arena.  Thread-
+# local storage also drops a thread's buffers when the thread ends.
+_WS_TLS = threading.local()
 
 
 def resolve_devices(device=None, devices=None) -> list[torch.device]:
@@ -236,12 +231,19 @@ def run_sliced(devices: list[torch.device], tau: int, call, arrays) -> list:
 
 
 def device_workspace_slot(device: torch.device, nbytes: int, slot: int) -> torch.Tensor:
-    """Like ``device_workspace`` but one buffer per (device, slot): concurrent
-    calls on the same device never share scratch."""
+    """Grow-only scratch for one host-pipeline call: one buffer per (calling
+    thread, device, slot), so concurrent calls (the per-device threads of
+    ``run_sliced`` or independent caller threads on the same GPU) never share
+    scratch.  A grown buffer replaces the old one only after the caller's
+    previous call on it has returned (the pipelines synchronise their streams
+    before returning), so no native stream still uses the freed block."""
+    cache = getattr(_WS_TLS, "ws", None)
+    if cache is None:
+        cache = _WS_TLS.ws = {}
     key = (device, slot)
-    ws = _WS.get(key)
+    ws = cache.get(key)
     if ws is None or ws.numel() < nbytes:
-        _WS.pop(key, None)
+        cache.pop(key, None)
         ws = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
-        _WS[key] = ws
+        cache[key] = ws
     return ws

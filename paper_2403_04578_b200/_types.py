@@ -2,8 +2,11 @@
 
 * ``SolveOptions``            -- fpi.py:48-62 (tolerance, max_iterations,
                                  residual_tolerance; ``initial_voltage`` and
-                                 ``compute_contraction`` accepted and ignored,
-                                 as both reference batch paths ignore them)
+                                 ``compute_contraction`` are ignored by the
+                                 constant-power batch paths, as in the
+                                 reference, dense.py:155; the ZIP route
+                                 honours ``initial_voltage`` like fpi_solve,
+                                 fpi.py:141-145)
 * ``PowerTensor``/``LoadMatrix``/``VoltageBatch`` -- dense.py:35-98
 * ``reshape_tensor``/``unreshape``                -- dense.py:101-111
 * ``SingularSystemError``     -- fpi.py:44-45

@@ -60,6 +60,7 @@ __device__ __forceinline__ float2 recip32(float2 s, float2 v) {
   return make_float2(fmaf(s.x, v.x, s.y * v.y) * r, fmaf(s.x, v.y, -(s.y * v.x)) * r);
 }
 
+#ifdef TPF_AB_VARIANTS  // A/B-only kernel, not in libtpf.so
 // BP: node count padded to a multiple of the 26-node register chunk, so every
 // loop over V' nodes is compile-time (padding rows of K^T and W are zero).
 // 256 threads = 128 case slots, two threads per slot (lanes l and l + 16 of
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(2 * kC64Threads, 1) dense_c64_halves_kernel(co
     }
   }
 }
+#endif  // TPF_AB_VARIANTS
 
 // Default dense c64 kernel: 256 threads = 2 groups of 4 warps; a group owns
 // 64 slot pairs (slots p and p + 64, p = lane of the group's warps) and warp q
@@ -491,19 +493,22 @@ extern "C" int tpf_dense_fpi_c64(int64_t tau, int32_t b, const float* S, int64_t
   const int64_t grid = c64_grid(tau);
   cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
   if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
-  // default: quarter kernel (two slots per thread); TPF_C64_HALVES=1 runs the
-  // previous one-slot-per-thread kernel (A/B only)
+  // default: quarter kernel (two slots per thread); in A/B builds
+  // (-DTPF_AB_VARIANTS) TPF_C64_HALVES=1 runs the previous one-slot-per-thread kernel
+  int bp;
+  void (*kern)(const DenseC64Args);
+#ifdef TPF_AB_VARIANTS
   static const bool halves = [] {
     const char* e = getenv("TPF_C64_HALVES");
     return e && e[0] == '1';
   }();
-  int bp;
-  void (*kern)(const DenseC64Args);
   if (halves) {
     bp = (b + kC64Chunk - 1) / kC64Chunk * kC64Chunk;
     kern = bp == 26 ? dense_c64_halves_kernel<26> : bp == 52 ? dense_c64_halves_kernel<52>
          : bp == 78 ? dense_c64_halves_kernel<78> : dense_c64_halves_kernel<104>;
-  } else {  // nodes per quarter
+  } else
+#endif
+  {  // nodes per quarter
     const int nc = b <= 32 ? 8 : b <= 40 ? 10 : b <= 56 ? 14 : b <= 80 ? 20 : 26;
     bp = 4 * nc;
     kern = nc == 8 ? dense_c64_kernel<8> : nc == 10 ? dense_c64_kernel<10> : nc == 14 ? dense_c64_kernel<14>

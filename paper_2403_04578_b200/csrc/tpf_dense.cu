@@ -498,13 +498,17 @@ __global__ void __launch_bounds__(kThreads, 1) dense_fpi_kernel(const DenseArgs 
 
 template <int NB>
 static int launch_dense(const DenseArgs& a, cudaStream_t stream, int sm_count) {
-  // 3M GEMM + Newton reciprocal (bitwise equal to the default ws kernel) unless
-  // TPF_WS_4M=1 selects the 4-DMMA arithmetic for both kernels
+  // 3M GEMM + Newton reciprocal (bitwise equal to the default ws kernel); A/B
+  // builds (-DTPF_AB_VARIANTS) also carry the 4-DMMA arithmetic (TPF_WS_4M=1)
+#ifdef TPF_AB_VARIANTS
   static const bool four = [] {
     const char* e = getenv("TPF_WS_4M");
     return e && e[0] == '1';
   }();
   auto kern = four ? dense_fpi_kernel<NB, false> : dense_fpi_kernel<NB, true>;
+#else
+  auto kern = dense_fpi_kernel<NB, true>;
+#endif
   const size_t smem = DenseSmem<NB>::total(a.ks_count);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense)", err);

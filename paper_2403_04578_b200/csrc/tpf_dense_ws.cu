@@ -662,6 +662,7 @@ int launch(const Args& a, cudaStream_t st, int sms) {
 
 }  // namespace ws
 
+#ifdef TPF_AB_VARIANTS  // A/B-only kernels (tools/build_timing.sh -DTPF_AB_VARIANTS); not in libtpf.so
 // ---------------------------------------------------------------------------
 // "Solo" variant: 8 independent warps per SM, each owning 8 case slots and all
 // node blocks, each doing its own GEMM and elementwise work.  Two DMMA
@@ -876,6 +877,7 @@ int launch(const ws::Args& a, cudaStream_t st, int sms) {
 }
 
 }  // namespace solo
+#endif  // TPF_AB_VARIANTS
 }  // namespace tpf
 
 using namespace tpf;
@@ -893,12 +895,13 @@ extern "C" int tpf_debug_ws_phase_cycles(long long* out) {
 #endif
 
 // Variants (chosen once per process): default 3M GEMM with the EW warps taking
-// TPF_WS_NE node blocks (C2: 6.25 ms); TPF_WS_4M=1 the 4-DMMA GEMM on one DMMA
-// warp per SMSP (7.43 ms, bitwise equal to the pair/solo kernels);
-// TPF_WS_SPLIT=2 two 4M DMMA warps per SMSP (8.17 ms: the EW warps cannot
-// refill U fast enough).
+// TPF_WS_NE node blocks (C2: 6.25 ms).  In A/B builds only (-DTPF_AB_VARIANTS,
+// not libtpf.so): TPF_WS_4M=1 the 4-DMMA GEMM on one DMMA warp per SMSP
+// (7.43 ms) and TPF_WS_SPLIT=2 two 4M DMMA warps per SMSP (8.17 ms: the EW
+// warps cannot refill U fast enough).
 template <int NB, int KS>
 static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
+#ifdef TPF_AB_VARIANTS  // A/B builds only: the 4M and two-DMMA-warp variants
   static const int split = [] {
     const char* e = getenv("TPF_WS_SPLIT");
     return (e && e[0] == '2') ? 2 : 1;
@@ -910,6 +913,8 @@ static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
   if constexpr (NB >= 2) {
     if (split == 2) return ws::launch<NB, KS, 2, false>(a, st, sms);
   }
+  if (four) return ws::launch<NB, KS, 1, false>(a, st, sms);
+#endif
   // node blocks of the GEMM done by the elementwise warps: 5 at 13 node blocks
   // (tuned on C2: NE 2..7 measured 6.69 / 6.56 / 6.34 / 6.31 / 6.58 / 6.63 ms),
   // otherwise min(4, blocks - 6) so the EW blocks lie past the 6 scratch
@@ -919,7 +924,6 @@ static int ws_launch(const ws::Args& a, cudaStream_t st, int sms) {
     const char* e = getenv("TPF_WS_NE");
     return e ? atoi(e) : 5;
   }();
-  if (four) return ws::launch<NB, KS, 1, false>(a, st, sms);
   if constexpr (NB == 13) {
     if (ne == 5) return ws::launch<NB, KS, 1, true, NB - 5>(a, st, sms);
   }
@@ -991,6 +995,7 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
   return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");
 }
 
+#ifdef TPF_AB_VARIANTS
 extern "C" int tpf_dense_solo_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
                                        int64_t s_case_stride, const double* K, const double* W, double v_flat_re,
                                        double v_flat_im, double tol, int32_t max_iter, double* V,
@@ -1046,3 +1051,4 @@ extern "C" int tpf_dense_solo_fpi_c128(int64_t tau, int32_t b, const double* S, 
   }
   return set_error(TPF_ERR_UNSUPPORTED, "unsupported b");
 }
+#endif  // TPF_AB_VARIANTS

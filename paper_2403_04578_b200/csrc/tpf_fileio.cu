@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <locale.h>
 #include <string>
 #include <thread>
 #include <vector>
@@ -26,6 +27,16 @@
 
 namespace tpf {
 namespace {
+
+// Python's float() and f"{x:.17g}" ignore LC_NUMERIC; strtod/snprintf follow
+// it.  Every parse and format here uses the "C" locale explicitly, so a
+// process that called setlocale(LC_ALL, "") under a comma-decimal locale
+// still reads and writes the reference's bytes.
+locale_t c_locale() {
+  static const locale_t loc = newlocale(LC_ALL_MASK, "C", locale_t(0));
+  return loc;
+}
+
 
 bool read_file(const char* path, std::string& out) {
   FILE* f = fopen(path, "rb");
@@ -92,7 +103,7 @@ int parse_field(const char* b, const char* e, double* out) {
   buf[n] = '\0';
   char* end = nullptr;
   errno = 0;
-  const double v = strtod(buf, &end);
+  const double v = strtod_l(buf, &end, c_locale());
   if (end != buf + n) return 1;
   *out = v;  // overflow gives +-inf and underflow a denormal/0, as float() does
   return 0;
@@ -226,6 +237,7 @@ extern "C" int tpf_write_pairs_csv(const char* path, const char* header, int32_t
   };
   for (int64_t r0 = 0; ok && r0 < tau; r0 += block * nt) {
     auto work = [&](int w) {
+      const locale_t prev = uselocale(c_locale());  // this thread only
       std::string& s = out[size_t(w)];
       s.clear();
       const int64_t lo = r0 + block * w, hi = std::min(tau, lo + block);
@@ -240,6 +252,7 @@ extern "C" int tpf_write_pairs_csv(const char* path, const char* header, int32_t
         if (flag) s += flag[j] ? ",1" : ",0";
         s += '\n';
       }
+      uselocale(prev);
     };
     std::vector<std::thread> pool;
     for (int w = 1; w < nt; ++w) pool.emplace_back(work, w);

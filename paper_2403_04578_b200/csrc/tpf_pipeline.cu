@@ -231,6 +231,18 @@ Streams* cached_streams(int device) {
     if (_e != cudaSuccess) return set_cuda_error(where, _e); \
   } while (0)
 
+// Inside the chunk loop: record the error and leave the loop, so the streams
+// are still synchronised (queued copies may target the caller's host buffers,
+// which HostPin unregisters on return) and the setup event is destroyed.
+#define TPF_CK_LOOP(expr, where)                \
+  {                                             \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) {                    \
+      rc = set_cuda_error(where, _e);           \
+      break;                                    \
+    }                                           \
+  }
+
 template <class T>
 cudaError_t upload(DevBuf& d, const T* h, size_t n, cudaStream_t st) {
   cudaError_t e = d.alloc(n * sizeof(T));
@@ -328,22 +340,22 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     if (c >= 2) cudaStreamWaitEvent(sin, ss.comp_done[k], 0);
     if (stage_s) {
       // staging slot k was last read by the H2D of chunk c - 2
-      if (c >= 2) TPF_CK(cudaEventSynchronize(ss.in_done[k]), "staging reuse");
+      if (c >= 2) TPF_CK_LOOP(cudaEventSynchronize(ss.in_done[k]), "staging reuse");
       char* stg = static_cast<char*>(g_staging.p) + size_t(k) * size_t(chunk) * b * 16;
       const char* hs = reinterpret_cast<const char*>(S);
       if (LS.case_contig) {  // b rows of n cases -> [b][chunk] pitch chunk
         parallel_copy2d(stg, size_t(chunk) * 16, hs + size_t(lo) * 16, size_t(LS.ld) * 16, size_t(n) * 16, b);
-        TPF_CK(cudaMemcpy2DAsync(d_S[k].as<double>(), size_t(chunk) * 16, stg, size_t(chunk) * 16, size_t(n) * 16,
+        TPF_CK_LOOP(cudaMemcpy2DAsync(d_S[k].as<double>(), size_t(chunk) * 16, stg, size_t(chunk) * 16, size_t(n) * 16,
                                  size_t(b), cudaMemcpyHostToDevice, sin),
                "H2D(S chunk)");
       } else {  // n cases of b nodes -> [n][b]
         parallel_copy2d(stg, size_t(b) * 16, hs + size_t(lo) * size_t(LS.ld) * 16, size_t(LS.ld) * 16,
                         size_t(b) * 16, n);
-        TPF_CK(cudaMemcpyAsync(d_S[k].as<double>(), stg, size_t(n) * b * 16, cudaMemcpyHostToDevice, sin),
+        TPF_CK_LOOP(cudaMemcpyAsync(d_S[k].as<double>(), stg, size_t(n) * b * 16, cudaMemcpyHostToDevice, sin),
                "H2D(S chunk)");
       }
     } else {
-      TPF_CK(copy_chunk(true, LS, const_cast<double*>(S), d_S[k].as<double>(), b, lo, n, chunk, sin),
+      TPF_CK_LOOP(copy_chunk(true, LS, const_cast<double*>(S), d_S[k].as<double>(), b, lo, n, chunk, sin),
              "H2D(S chunk)");
     }
     cudaEventRecord(ss.in_done[k], sin);
@@ -355,7 +367,7 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     if (rc == TPF_OK) {
       cudaEventRecord(ss.comp_done[k], scomp);
       cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
-      TPF_CK(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
+      TPF_CK_LOOP(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
       cudaEventRecord(ss.out_done[k], sout);
       continue;
     }
@@ -369,7 +381,7 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     if (rc != TPF_OK) break;
     cudaEventRecord(ss.comp_done[k], scomp);
     cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
-    TPF_CK(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
+    TPF_CK_LOOP(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
     cudaEventRecord(ss.out_done[k], sout);
   }
   if (rc == TPF_OK) {

@@ -200,6 +200,7 @@ struct ZipChainArgs {
   const double* alpha;      // [3][b] alpha_z, alpha_i, alpha_p (leaf-first order)
   const double2* src;       // source injection (leaf-first order)
   double2 v_flat;
+  const double2* v0;        // initial iterate (original node order) or null: flat start
   double tol2;
   int max_iter;
   double2* V;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(128) sparse_zip_chain_kernel(const ZipChainArg
     }
   }
   if (bad) atomicExch(a.status, 1);
-  for (int k = 0; k < b; ++k) Vk(k) = a.v_flat;
+  for (int k = 0; k < b; ++k) Vk(k) = a.v0 ? __ldg(a.v0 + __ldg(a.orig + k)) : a.v_flat;  // fpi.py:141-145
   int n = 0;
   bool met = false;
   while (n < a.max_iter) {
@@ -357,8 +358,8 @@ extern "C" size_t tpf_sparse_zip_chain_workspace_bytes(int64_t tau, int32_t b) {
 extern "C" int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* orig, const int32_t* parent,
                                          const double* e, const double* ydiag, const double* alpha,
                                          const double* src, const double* S, int64_t s_node_stride,
-                                         int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,
-                                         int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                         int64_t s_case_stride, double v_flat_re, double v_flat_im, const double* v0,
+                                         double tol, int32_t max_iter, double* V, int64_t v_node_stride, int64_t v_case_stride,
                                          int32_t* iters, double* resid, uint8_t* step_met, int32_t* status,
                                          void* workspace, size_t workspace_bytes, void* stream) {
   if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_chain_c128: need tau >= 0, b >= 1");
@@ -383,6 +384,7 @@ extern "C" int tpf_sparse_zip_chain_c128(int64_t tau, int32_t b, const int32_t* 
   a.alpha = alpha;
   a.src = reinterpret_cast<const double2*>(src);
   a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.v0 = reinterpret_cast<const double2*>(v0);
   a.tol2 = tol * tol;
   a.max_iter = max_iter;
   a.V = reinterpret_cast<double2*>(V);
@@ -431,6 +433,7 @@ struct ZipLuArgs {
   const int32_t* ci;
   const double2* yv;
   double2 v_flat;
+  const double2* v0;       // initial iterate (original node order) or null: flat start
   double tol2;
   int max_iter;
   double2* V;
@@ -487,7 +490,10 @@ __global__ void __launch_bounds__(128) sparse_zip_lu_kernel(const ZipLuArgs a) {
     }
   }
   if (bad) atomicExch(a.status, 1);
-  for (int k = 0; k < b; ++k) Vn(__ldg(a.orig + k)) = a.v_flat;
+  for (int k = 0; k < b; ++k) {  // fpi.py:141-145
+    const int i = __ldg(a.orig + k);
+    Vn(i) = a.v0 ? __ldg(a.v0 + i) : a.v_flat;
+  }
   int n = 0;
   bool met = false;
   while (n < a.max_iter) {
@@ -585,7 +591,7 @@ extern "C" int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, con
                                       const double* alpha, const double* src, const int32_t* y_row_ptr,
                                       const int32_t* y_col, const double* y_val, const double* S,
                                       int64_t s_node_stride, int64_t s_case_stride, double v_flat_re,
-                                      double v_flat_im, double tol, int32_t max_iter, double* V,
+                                      double v_flat_im, const double* v0, double tol, int32_t max_iter, double* V,
                                       int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, double* resid,
                                       uint8_t* step_met, int32_t* status, void* workspace, size_t workspace_bytes,
                                       void* stream) {
@@ -616,6 +622,7 @@ extern "C" int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, con
   a.ci = y_col;
   a.yv = reinterpret_cast<const double2*>(y_val);
   a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.v0 = reinterpret_cast<const double2*>(v0);
   a.tol2 = tol * tol;
   a.max_iter = max_iter;
   a.V = reinterpret_cast<double2*>(V);

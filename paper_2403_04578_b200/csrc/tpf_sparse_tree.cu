@@ -57,6 +57,7 @@ struct TreeArgs {
   const int4* info;       // per level-ordered node m: {original node, parent m or -1, first child m, child count}
   const double2* coef;    // planes [4][b] (level order m): e = Y[parent, m], g = U[m,parent]/U[m,m], uinv = 1/U[m,m], src
   double2 v_flat;
+  const double2* v0;      // ZIP: initial iterate (original node order) or null: flat start
   double tol2;
   int max_iter;
   // optional fused residual post-check (same arithmetic as residual_kernel):
@@ -180,8 +181,13 @@ __global__ void __launch_bounds__(kTreeThreads, 1) sparse_tree_kernel(const Tree
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j0 + j < nslots) {  // warp-uniform
+          double2 v0 = a.v_flat;
+          if (ZIP && a.v0) {  // fpi.py:141-145: opts.initial_voltage
+            const int m = slot_node(j0 + j);
+            if (m >= 0) v0 = __ldg(a.v0 + __ldg(&a.info[m].x));
+          }
           tmem_st2(tm_s + 4 * (j0 + j), sv[j]);
-          tmem_st2(tm_v + 4 * (j0 + j), a.v_flat);
+          tmem_st2(tm_v + 4 * (j0 + j), v0);
         }
       }
     }
@@ -515,7 +521,8 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
                        int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, int32_t ell_w,
                        const int32_t* ell_col, const double* ell_val, double* resid, void* workspace,
                        size_t workspace_bytes, void* stream, const double* alpha = nullptr,
-                       const double* ydiag = nullptr, int32_t* status = nullptr, uint8_t* met = nullptr) {
+                       const double* ydiag = nullptr, int32_t* status = nullptr, uint8_t* met = nullptr,
+                       const double* v0 = nullptr) {
   const bool zip = alpha != nullptr;
   if (tau < 0 || b < 1 || levels < 1 || levels > kMaxLevels)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_fpi_c128: bad shape");
@@ -557,6 +564,7 @@ static int tree_launch(int64_t tau, int32_t b, int32_t levels, const int32_t* le
   a.info = reinterpret_cast<const int4*>(node_info);
   a.coef = reinterpret_cast<const double2*>(node_coef);
   a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.v0 = reinterpret_cast<const double2*>(v0);
   a.tol2 = tol * tol;
   a.max_iter = max_iter;
   a.ell_w = ell_w;
@@ -616,8 +624,8 @@ extern "C" size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b) {
 extern "C" int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels, const int32_t* level_info,
                                             const int32_t* node_info, const double* node_coef, const double* alpha,
                                             const double* ydiag, const double* S, int64_t s_node_stride,
-                                            int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,
-                                            int32_t max_iter, double* V, int64_t v_node_stride,
+                                            int64_t s_case_stride, double v_flat_re, double v_flat_im,
+                                            const double* v0, double tol, int32_t max_iter, double* V, int64_t v_node_stride,
                                             int64_t v_case_stride, int32_t* iters, int32_t ell_width,
                                             const int32_t* ell_col, const double* ell_val, double* resid,
                                             uint8_t* step_met, int32_t* status, void* workspace,
@@ -626,7 +634,7 @@ extern "C" int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t leve
     return set_error(TPF_ERR_INVALID, "tpf_sparse_tree_zip_fpi_c128: null alpha / ydiag / resid / step_met / status");
   return tree_launch(tau, b, levels, level_info, node_info, node_coef, S, s_node_stride, s_case_stride, v_flat_re,
                      v_flat_im, tol, max_iter, V, v_node_stride, v_case_stride, iters, ell_width, ell_col, ell_val,
-                     resid, workspace, workspace_bytes, stream, alpha, ydiag, status, step_met);
+                     resid, workspace, workspace_bytes, stream, alpha, ydiag, status, step_met, v0);
 }
 
 extern "C" int tpf_sparse_tree_ell_width(int32_t b, const int32_t* ydd_row_ptr) {

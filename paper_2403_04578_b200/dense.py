@@ -6,9 +6,10 @@ Reference: pkg/src/tpflow/dense.py:129-205.  Same signature, same
 * ``ValueError("load matrix has N rows, model has M")`` (dense.py:143-146);
 * non-constant-power ZIP models: the reference routes them through the
   single-case solver column by column (dense.py:147-148, 214-230); here they
-  run as one GPU launch with the single-case semantics on radial feeders
-  (``solve_zip``), and raise ``NotImplementedError`` on meshed networks
-  instead of silently running a CPU loop;
+  run as one GPU launch with the single-case semantics and start
+  (``solve_zip``: radial feeders on the per-case tree-LU kernels, meshed or
+  non-symmetric networks on the per-case fixed-pattern LU kernel); only
+  complex64 or multi-device ZIP batches raise ``NotImplementedError``;
 * ``numpy.linalg.LinAlgError`` from the inverse of a singular Y_dd
   (dense.py:151, uncaught in the reference too).
 
@@ -131,8 +132,7 @@ class DenseOperator:
         vn, vc = complex_strides(V)
         fn = "tpf_dense_fpi_large_c128" if self.large else "tpf_dense_fpi_c128"
         if kernel is not None and not self.large:
-            fn = {"ws": "tpf_dense_ws_fpi_c128", "pairs": "tpf_dense_pairs_fpi_c128",
-                  "solo": "tpf_dense_solo_fpi_c128"}[kernel]
+            fn = {"ws": "tpf_dense_ws_fpi_c128", "pairs": "tpf_dense_pairs_fpi_c128"}[kernel]
         _capi.call(fn, tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
                    self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                    V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -196,16 +196,39 @@ def batch_solve_dense(model, loads: LoadMatrix, opts: SolveOptions = SolveOption
 ZIP_CHAIN_MAX_B = 384
 
 
+def _zip_start(c: ModelContract, opts: SolveOptions, dev):
+    """fpi_solve's start (fpi.py:141-145): ``opts.initial_voltage`` (b values,
+    ValueError on a length mismatch) as a device vector in original node
+    order, or None for the flat start |v_s| + 0j.  The reference's ZIP route
+    (dense.py:214-230) goes through fpi_solve case by case, so it honours the
+    option, unlike the constant-power batch paths."""
+    if opts.initial_voltage is None:
+        return None
+    v = np.asarray(opts.initial_voltage, dtype=complex).ravel().copy()
+    if v.shape[0] != c.b:
+        raise ValueError("initial voltage length mismatch")
+    return torch.from_numpy(np.ascontiguousarray(v, dtype=np.complex128)).to(dev)
+
+
+def _ptr_or_null(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
 def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_on_device: bool = False):
     """ZIP loads: the reference's per-case route (dense.py:214-230 -> fpi_solve,
-    fpi.py:107-206) as one GPU launch on radial feeders (include/tpf.h,
-    ``tpf_sparse_tree_zip_fpi_c128``): every case factorizes its own
-    B = Y_dd + diag(alpha_z s*) on chip and iterates with fpi_solve's stopping
-    rules.  Meshed or non-symmetric networks raise NotImplementedError (the
-    reference's per-case CPU loop is not the accelerated path)."""
+    fpi.py:107-206), one GPU launch per batch, each case factorizing its own
+    B = Y_dd + diag(alpha_z s*) and iterating with fpi_solve's stopping rules
+    and start (``opts.initial_voltage`` honoured, fpi.py:141-145).  Routing:
+    radial feeders up to ZIP_CHAIN_MAX_B nodes and radial feeders the tree
+    kernel does not take -> ``tpf_sparse_zip_chain_c128`` (one thread per
+    case); larger radial feeders -> ``tpf_sparse_tree_zip_fpi_c128`` (one case
+    per SM, on-chip tree LU); meshed or non-symmetric networks ->
+    ``tpf_sparse_zip_lu_c128`` (per-case LU on a fixed fill pattern).  Only
+    complex64 and multi-device ZIP batches raise NotImplementedError."""
     from ._types import SingularSystemError
     from .sparse import factorize_ydd, tree_ell, tree_schedule
     c = ModelContract.of(model)
+    _zip_start(c, opts, "cpu")  # validate before any device work
     y = c.y_dd
     b = c.b
     if (y != y.T).nnz != 0:  # non-symmetric values: the general per-case LU
@@ -217,6 +240,7 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     if tree is None or ell is None:
         return _solve_zip_chain(model, c, loads, opts, device, return_on_device)
     dev = require_cuda(device)
+    v0 = _zip_start(c, opts, dev)
     order = tree.node_info.reshape(b, 4)[:, 0]
     z = model.zip
     alpha = np.ascontiguousarray(np.concatenate([np.asarray(z.alpha_z, float)[order],
@@ -240,7 +264,8 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
     if tau:
         _capi.call("tpf_sparse_tree_zip_fpi_c128", tau, b, tree.levels, g["level_info"].data_ptr(),
                    g["node_info"].data_ptr(), g["node_coef"].data_ptr(), g["alpha"].data_ptr(),
-                   g["ydiag"].data_ptr(), S.data_ptr(), sn, sc, v_flat.real, v_flat.imag, float(opts.tolerance),
+                   g["ydiag"].data_ptr(), S.data_ptr(), sn, sc, v_flat.real, v_flat.imag, _ptr_or_null(v0),
+                   float(opts.tolerance),
                    int(opts.max_iterations), V.data_ptr(), tau, 1, iters.data_ptr(), ell[0],
                    g["ell_col"].data_ptr(), g["ell_val"].data_ptr(), resid.data_ptr(), met.data_ptr(),
                    status.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
@@ -257,9 +282,9 @@ def solve_zip(model, loads: LoadMatrix, opts: SolveOptions, device=None, return_
 
 
 def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
-    """ZIP loads on radial feeders beyond the tree kernel (deep, wide or large):
-    one thread per case with the same per-case tree LU and fpi_solve rules
-    (``tpf_sparse_zip_chain_c128``).  Meshed networks: NotImplementedError."""
+    """ZIP loads on radial feeders, one thread per case with the per-case tree
+    LU and fpi_solve rules (``tpf_sparse_zip_chain_c128``).  Meshed networks
+    go to the per-case LU kernel (``_solve_zip_lu``)."""
     from ._types import SingularSystemError
     from .sparse import tree_parents
     tp = tree_parents(c.y_dd)
@@ -267,6 +292,7 @@ def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
         return _solve_zip_lu(model, c, loads, opts, device, return_on_device)
     dev = require_cuda(device)
     order, parent = tp
+    v0 = _zip_start(c, opts, dev)
     b = c.b
     y = c.y_dd.tocsr()
     e = np.zeros(b, dtype=np.complex128)
@@ -294,8 +320,9 @@ def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
         hi = min(tau, lo + chunk)
         _capi.call("tpf_sparse_zip_chain_c128", hi - lo, b, g["orig"].data_ptr(), g["parent"].data_ptr(),
                    g["e"].data_ptr(), g["ydiag"].data_ptr(), g["alpha"].data_ptr(), g["src"].data_ptr(),
-                   S.data_ptr() + 16 * lo * sc, sn, sc, v_flat.real, v_flat.imag, float(opts.tolerance),
-                   int(opts.max_iterations), V.data_ptr() + 16 * lo, tau, 1, iters.data_ptr() + 4 * lo,
+                   S.data_ptr() + 16 * lo * sc, sn, sc, v_flat.real, v_flat.imag, _ptr_or_null(v0),
+                   float(opts.tolerance), int(opts.max_iterations), V.data_ptr() + 16 * lo, tau, 1,
+                   iters.data_ptr() + 4 * lo,
                    resid.data_ptr() + 8 * lo, met.data_ptr() + lo, status.data_ptr(), ws.data_ptr(), ws.numel(),
                    stream_ptr(dev))
     return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)
@@ -310,6 +337,7 @@ def _solve_zip_lu(model, c, loads, opts, device, return_on_device):
     from .sparse import zip_lu_schedule
     dev = require_cuda(device)
     sch = zip_lu_schedule(c.y_dd)
+    v0 = _zip_start(c, opts, dev)
     order = sch.orig.astype(np.int64)
     b = c.b
     z = model.zip
@@ -338,7 +366,7 @@ def _solve_zip_lu(model, c, loads, opts, device, return_on_device):
         _capi.call("tpf_sparse_zip_lu_c128", hi - lo, b, sch.nslot, g["orig"].data_ptr(), g["kinfo"].data_ptr(),
                    g["idx"].data_ptr(), g["base"].data_ptr(), g["alpha"].data_ptr(), g["src"].data_ptr(),
                    g["rp"].data_ptr(), g["ci"].data_ptr(), g["yv"].data_ptr(), S.data_ptr() + 16 * lo * sc, sn,
-                   sc, v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                   sc, v_flat.real, v_flat.imag, _ptr_or_null(v0), float(opts.tolerance), int(opts.max_iterations),
                    V.data_ptr() + 16 * lo, tau, 1, iters.data_ptr() + 4 * lo, resid.data_ptr() + 8 * lo,
                    met.data_ptr() + lo, status.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr(dev))
     return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)

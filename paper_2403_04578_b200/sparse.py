@@ -23,7 +23,7 @@ size, in tau chunks that fit device memory.
 from __future__ import annotations
 
 import threading
-from collections import OrderedDict, deque
+from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
@@ -639,30 +639,14 @@ def _nonempty(a):
     return a if a.size else np.zeros(1, dtype=a.dtype)
 
 
-_LU_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
-_LU_LOCK = threading.Lock()
-
-
 def _batch_lu(contract, use_tree: bool):
-    """The batch's LU of Y_dd and tree schedule.  ``factorization_count``
-    advances by one per batch exactly as in the reference (sparse.py:186); the
-    SuperLU result itself is memoised per network content (a deterministic
-    function of Y_dd, so the bits are those of a fresh factorization), which
-    takes the O(b) host setup (C3: ~10 ms) off repeated batches."""
-    global _factorizations
-    key = (contract.fingerprint(), bool(use_tree))
-    with _LU_LOCK:
-        hit = _LU_CACHE.get(key)
-        if hit is not None:
-            _LU_CACHE.move_to_end(key)
-            _factorizations += 1
-            return hit
+    """The batch's LU of Y_dd and tree schedule: one real SuperLU
+    factorization per batch, exactly as the reference (sparse.py:186), so
+    ``factorization_count`` counts factorizations that ran.  Nothing is
+    memoised: the host setup (C3: ~30 ms) is part of every call, as it is of
+    the reference's."""
     f = factorize_ydd(contract.y_dd)
     tree = tree_schedule(f, contract.src) if use_tree else None
-    with _LU_LOCK:
-        _LU_CACHE[key] = (f, tree)
-        while len(_LU_CACHE) > 8:
-            _LU_CACHE.popitem(last=False)
     return f, tree
 
 

@@ -1,6 +1,6 @@
 """ZIP-load fixtures from the REFERENCE (dense.py:214-230 -> fpi.py:107-206).
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_zip.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_zip.py [names...]
 
 For each fixture: a radial feeder (``*_mesh``: plus tie branches closing loops
 among the demand buses, the reference's meshed per-case SuperLU route) from the reference generator with mixed
@@ -53,8 +53,17 @@ def zip_model(n_buses, seed, kind, loops=0):
     return NetworkModel.from_branches(branches, n_buses, slack=base.slack, zip_coeffs=z), z
 
 
-def save(name, n_buses, seed, tau, kind="mixed", scale=1.0, heavy=False, opts=SolveOptions(), loops=0):
+def save(name, n_buses, seed, tau, kind="mixed", scale=1.0, heavy=False, opts=SolveOptions(), loops=0,
+         warm=False):
+    if len(sys.argv) > 1 and name not in sys.argv[1:]:
+        return
     model, z = zip_model(n_buses, seed, kind, loops)
+    if warm:  # opts.initial_voltage: a seeded non-flat start (fpi.py:141-145)
+        rng_w = np.random.default_rng(300 + seed)
+        b = model.n_demand
+        v0 = rng_w.uniform(0.9, 1.05, b) * np.exp(1j * rng_w.uniform(-0.05, 0.05, b))
+        opts = SolveOptions(tolerance=opts.tolerance, max_iterations=opts.max_iterations,
+                            residual_tolerance=opts.residual_tolerance, initial_voltage=v0)
     S = gen_scenarios(model, tau, GenSpec(n_buses=n_buses, seed=seed, load_scale=scale)).values.copy()
     S[:, 1] = 0.0  # a zero-load case
     if heavy:
@@ -71,7 +80,8 @@ def save(name, n_buses, seed, tau, kind="mixed", scale=1.0, heavy=False, opts=So
              ydd_data=y.data, ydd_indices=y.indices, ydd_indptr=y.indptr, src=model.source_injection(),
              V=r.values, iterations=r.iterations, mask=r.converged_mask, residuals=r.residuals,
              n_case=np.array(n), tol=opts.tolerance, max_iter=opts.max_iterations,
-             residual_tol=opts.residual_tolerance)
+             residual_tol=opts.residual_tolerance,
+             **({} if opts.initial_voltage is None else {"initial_voltage": opts.initial_voltage}))
     print(name, "iterations", r.iterations, "converged", int(r.converged_mask.sum()), "/", tau, file=sys.stderr)
 
 
@@ -81,3 +91,7 @@ save("zip9_pure_zi", 9, 2, 20, kind="pure_zi")
 save("zip101_mixed", 101, 0, 64, scale=3.0)
 save("zip9_mesh", 9, 3, 24, loops=4)
 save("zip101_mesh", 101, 4, 48, scale=2.0, loops=8)
+# warm starts (opts.initial_voltage) on each GPU route: chain (b <= 384), tree (b > 384), meshed LU
+save("zip9_warm", 9, 5, 24, warm=True)
+save("zip501_warm", 501, 6, 12, scale=2.0, warm=True)
+save("zip9_mesh_warm", 9, 7, 24, loops=4, warm=True)

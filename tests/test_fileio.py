@@ -127,3 +127,27 @@ def test_cli_error_exit_code(tmp_path, capsys):
                  str(tmp_path / "v.csv")]) == 1
     err = capsys.readouterr().err
     assert err.startswith("error: ") and "line 2" in err and "bad.csv" in err
+
+
+def test_native_reader_writer_ignore_lc_numeric(tmp_path):
+    """Python's float()/format ignore LC_NUMERIC; so must the native table I/O
+    (strtod_l / uselocale with the "C" locale).  Needs a comma-decimal locale
+    installed in the image; skipped otherwise."""
+    import locale
+    old = locale.setlocale(locale.LC_NUMERIC)
+    for name in ("de_DE.UTF-8", "de_DE.utf8", "fr_FR.UTF-8", "de_DE", "fr_FR"):
+        try:
+            locale.setlocale(locale.LC_NUMERIC, name)
+            break
+        except locale.Error:
+            continue
+    else:
+        pytest.skip("no comma-decimal locale installed")
+    try:
+        assert locale.localeconv()["decimal_point"] == ","
+        ref = gen_scenarios(fileio.read_network(fx("net9.json")), 50, GenSpec(n_buses=9, seed=3))
+        fileio.write_loads(tmp_path / "l.csv", ref, threads=3)
+        assert (tmp_path / "l.csv").read_bytes() == open(fx("loads9.csv"), "rb").read()
+        assert np.array_equal(fileio.read_loads(fx("loads9.csv")).values, ref.values)
+    finally:
+        locale.setlocale(locale.LC_NUMERIC, old)

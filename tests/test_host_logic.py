@@ -281,3 +281,15 @@ def test_as_load_matrix_complex64_passthrough():
     assert as_load_matrix(a64.astype(np.complex128), np.complex64).values.dtype == np.complex128
     ref = LoadMatrix(a64)
     assert as_load_matrix(ref, np.complex64) is ref
+
+
+def test_zip_initial_voltage_length_checked_like_fpi_solve():
+    """The ZIP route honours opts.initial_voltage (fpi.py:141-145) and raises the
+    reference's ValueError on a length mismatch before any device work."""
+    base = build_network(GenSpec(n_buses=9, seed=0))
+    b = base.n_demand
+    z = ZipCoefficients(alpha_z=np.full(b, 0.3), alpha_i=np.full(b, 0.3), alpha_p=np.full(b, 0.4))
+    model = NetworkModel.from_branches(base.branches, 9, slack=base.slack, zip_coeffs=z)
+    loads = LoadMatrix(np.full((b, 3), 0.01 + 0.005j))
+    with pytest.raises(ValueError, match="initial voltage length mismatch"):
+        batch_solve_dense(model, loads, SolveOptions(initial_voltage=np.ones(b + 1)))

@@ -20,7 +20,7 @@ def fixture(name):
     d = np.load(os.path.join(DIR, name + ".npz"))
     base = build_network(GenSpec(n_buses=int(d["n_buses"]), seed=int(d["seed"])))
     z = ZipCoefficients(alpha_z=d["alpha_z"], alpha_i=d["alpha_i"], alpha_p=d["alpha_p"])
-    if name.endswith("_mesh"):  # tie branches: the fixture's own Y_dd and source injection
+    if "_mesh" in name:  # tie branches: the fixture's own Y_dd and source injection
         from scipy import sparse as sp
         b = d["S"].shape[0]
         y = sp.csc_matrix((d["ydd_data"], d["ydd_indices"], d["ydd_indptr"]), shape=(b, b))
@@ -34,12 +34,15 @@ def fixture(name):
 
 
 @pytest.mark.parametrize("name", ["zip9_mixed", "zip9_heavy", "zip9_pure_zi", "zip101_mixed", "zip9_mesh",
-                                  "zip101_mesh"])
+                                  "zip101_mesh", "zip9_warm", "zip501_warm", "zip9_mesh_warm"])
 def test_zip_matches_reference(name):
+    """``*_warm``: opts.initial_voltage set (fpi.py:141-145), one fixture per GPU
+    route (chain kernel, tree kernel, meshed LU kernel)."""
     from paper_2403_04578_b200 import LoadMatrix, SolveOptions, batch_solve_dense
     model, d = fixture(name)
     opts = SolveOptions(tolerance=float(d["tol"]), max_iterations=int(d["max_iter"]),
-                        residual_tolerance=float(d["residual_tol"]))
+                        residual_tolerance=float(d["residual_tol"]),
+                        initial_voltage=d["initial_voltage"] if "initial_voltage" in d else None)
     out = batch_solve_dense(model, LoadMatrix(d["S"]), opts)
     assert out.iterations == int(d["iterations"])
     assert np.array_equal(out.converged_mask, d["mask"])
