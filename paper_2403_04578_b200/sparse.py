@@ -298,6 +298,19 @@ TREE_LEVEL_SLOTS = 6    # slots of one depth level held in registers at a time
 TREE_MAX_ROOTS = 512    # root-level nodes (source injections kept in shared memory)
 TREE_CHUNK = 65536      # cases per compact chunk on long node-major batches (SparseOperator)
 TREE_MAX_NODES = 220 * 1024 // 44  # 5,120: sweep vector, child products, child ranges, parents: 44 B per node
+SUBTREE_MIN_B = 0       # radial feeders from this size run the warp-per-subtree kernel (tpf_sparse_subtree_fpi_c128)
+
+
+def _subtree_layout_ok(S: torch.Tensor, V: torch.Tensor) -> bool:
+    """The subtree kernel moves whole case columns by TMA: node-major (case
+    stride 1) or case-major (node stride 1) S and V, 16-byte aligned."""
+    b, tau = S.shape
+    sn, sc = S.stride()
+    vn, vc = V.stride()
+    aligned = S.data_ptr() % 16 == 0 and V.data_ptr() % 16 == 0
+    node_major = sc == 1 and vc == 1 and sn >= tau and vn >= tau
+    case_major = sn == 1 and vn == 1 and sc >= b and vc >= b
+    return aligned and (node_major or case_major) and tau < (1 << 30)
 
 
 @dataclass
@@ -320,10 +333,13 @@ class TreeSchedule:
     slots: int
 
 
-def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
-    """Build the level schedule if the LU is a zero-fill tree elimination, else None."""
+def tree_levels(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
+    """Depth-level layout of a zero-fill tree elimination of a symmetric Y_dd,
+    or None.  No kernel limits: ``tree_schedule`` (one-case-per-SM level
+    kernel) and ``subtree_schedule`` (warp-per-subtree kernel) apply theirs.
+    ``level_info``'s slot starts are those of the level kernel's 512 threads."""
     b = f.b
-    if f.ordering != "leaf-first" or b > TREE_MAX_NODES:
+    if f.ordering != "leaf-first":
         return None
     row_src = f.perm[:b].astype(np.int64)
     col_dst = f.perm[b:].astype(np.int64)
@@ -351,21 +367,15 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
         if parent[k] >= 0:
             depth[k] = depth[parent[k]] + 1
     levels = int(depth.max(initial=0)) + 1
-    order = []
     pos_in_level = np.zeros(b, dtype=np.int64)
     level_nodes = [np.nonzero(depth == 0)[0]]
+    pos_in_level[level_nodes[0]] = np.arange(level_nodes[0].size)
+    # level by level (level 0 first) so children sort by parent position, then by k
     for d in range(1, levels):
         cand = np.nonzero(depth == d)[0]
         key = pos_in_level[parent[cand]]
         level_nodes.append(cand[np.lexsort((cand, key))])
-        pos_in_level[level_nodes[-1]] = np.arange(level_nodes[-1].size)
-    pos_in_level[level_nodes[0]] = np.arange(level_nodes[0].size)
-    # recompute positions level by level (level 0 first) so children sort by parent position
-    for d in range(1, levels):
-        cand = level_nodes[d]
-        key = pos_in_level[parent[cand]]
-        level_nodes[d] = cand[np.lexsort((cand, key))]
-        pos_in_level[level_nodes[d]] = np.arange(cand.size)
+        pos_in_level[level_nodes[-1]] = np.arange(cand.size)
     order = np.concatenate(level_nodes)
     m_of_k = np.empty(b, dtype=np.int64)
     m_of_k[order] = np.arange(b)
@@ -373,10 +383,7 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
     offs = np.concatenate([[0], np.cumsum(sizes)])
     slots_per = -(-sizes // TREE_THREADS)
     j0 = np.concatenate([[0], np.cumsum(slots_per)])
-    if j0[-1] > TREE_MAX_SLOTS:
-        return None
     pm = np.where(parent[order] >= 0, m_of_k[np.maximum(parent[order], 0)], -1)
-    first = np.zeros(b, dtype=np.int64)
     cnt = np.zeros(b, dtype=np.int64)
     kids = pm >= 0
     np.add.at(cnt, pm[kids], 1)
@@ -397,13 +404,26 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
     if np.any(src_o[offs[1]:] != 0):
         return None  # source injection only at the root level (nodes next to the slack)
     g = upar[order] * f.u_diag_inv[order]  # U[m, parent] / U[m, m] = L[parent, m] for symmetric Y
-    if np.any(-(-sizes // TREE_THREADS) > TREE_LEVEL_SLOTS) or sizes[0] > TREE_MAX_ROOTS:
-        return None
     coef = np.stack([e, g, f.u_diag_inv[order], src_o], axis=1).astype(complex)
     return TreeSchedule(b=b, levels=levels,
                         level_info=np.concatenate([offs, j0]).astype(np.int32),
                         node_info=np.ascontiguousarray(info.ravel()),
                         node_coef=np.ascontiguousarray(coef.T.ravel()), slots=int(j0[-1]))
+
+
+def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
+    """``tree_levels`` within the level kernel's limits (tpf_sparse_tree_fpi_c128), else None."""
+    if f.b > TREE_MAX_NODES:
+        return None
+    t = tree_levels(f, src)
+    if t is None:
+        return None
+    offs = t.level_info[:t.levels + 1]
+    sizes = np.diff(offs)
+    if t.slots > TREE_MAX_SLOTS or np.any(-(-sizes // TREE_THREADS) > TREE_LEVEL_SLOTS) \
+            or sizes[0] > TREE_MAX_ROOTS:
+        return None
+    return t
 
 
 def tree_ell(t: TreeSchedule, contract) -> tuple[int, np.ndarray, np.ndarray] | None:
@@ -464,7 +484,11 @@ def lu_solve_host(f: TreeLU, rhs: np.ndarray) -> np.ndarray:
 class SparseOperator:
     """One factorization of Y_dd resident on a device; ``solve`` iterates."""
 
-    def __init__(self, model, device=None, use_tree: bool = True, dtype=None):
+    def __init__(self, model, device=None, use_tree: bool = True, dtype=None, kernel: str = "auto"):
+        """``kernel``: "auto" (warp-per-subtree kernel where its schedule fits and
+        b >= SUBTREE_MIN_B, else the level kernel on radial feeders, else the
+        general CSR kernel), or "subtree" / "tree" / "general" to force one
+        (A/B tests; a forced radial kernel that does not fit falls back)."""
         self.device = require_cuda(device)
         self.contract = ModelContract.of(model)
         self.dtype = engine_dtype(dtype)
@@ -481,12 +505,28 @@ class SparseOperator:
         self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(cx(f.l_val)), u_ptr=t(f.u_ptr),
                         u_col=t(f.u_col), u_val=t(cx(f.u_val)), u_diag_inv=t(cx(f.u_diag_inv)),
                         perm=t(f.perm), src=t(cx(self.contract.src)))
-        use_tree = use_tree and not c64  # the c64 twin is the general CSR kernel
+        use_tree = use_tree and not c64 and kernel != "general"  # the c64 twin is the general CSR kernel
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
         self._csr = None
         self._chunk = None
-        self.tree = tree_schedule(f, self.contract.src) if use_tree else None
+        levels = tree_levels(f, self.contract.src) if use_tree else None
+        self.tree = None
+        self.sub = None
+        if levels is not None and kernel in ("auto", "subtree") and \
+                (kernel == "subtree" or self.contract.b >= SUBTREE_MIN_B):
+            from .subtree import subtree_schedule
+            rp, ci, yv = host_csr(self.contract)
+            self.sub = subtree_schedule(levels, rp, ci, yv)
+        if self.sub is not None:
+            sb = self.sub
+            self.sub_dev = dict(pinfo=t(sb.pinfo), kids=torch.from_numpy(sb.kids.view(np.int16).copy()).to(d),
+                                coef=t(sb.coef), ell_col=t(sb.ell_col), ell_val=t(sb.ell_val),
+                                meta=np.ascontiguousarray(sb.meta, dtype=np.int32))
+        if levels is not None:
+            # the level kernel: radial feeders without a subtree schedule, and
+            # the fallback for S / V layouts the subtree kernel's TMA cannot move
+            self.tree = tree_schedule(f, self.contract.src)
         if self.tree is not None:
             self.tree_dev = dict(level_info=t(self.tree.level_info), node_info=t(self.tree.node_info),
                                  node_coef=t(self.tree.node_coef))
@@ -500,6 +540,8 @@ class SparseOperator:
 
     @property
     def kernel(self) -> str:
+        if self.sub is not None:
+            return "sparse_subtree_kernel"
         return "sparse_tree_kernel" if self.tree is not None else "sparse_fpi_kernel"
 
     def csr(self):
@@ -525,6 +567,19 @@ class SparseOperator:
             V = torch.empty((b, tau), dtype=tdt, device=self.device)
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
+        if self.sub is not None and _subtree_layout_ok(S, V):
+            if self._ws is None:
+                self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+            sb, g = self.sub, self.sub_dev
+            sn, sc = complex_strides(S)
+            vn, vc = complex_strides(V)
+            _capi.call("tpf_sparse_subtree_fpi_c128", tau, b, g["meta"].ctypes.data, sb.NSL, sb.NS, sb.RMAX, sb.RW,
+                       int(sb.kids.size), g["pinfo"].data_ptr(), g["kids"].data_ptr(), g["coef"].data_ptr(),
+                       g["ell_col"].data_ptr(), g["ell_val"].data_ptr(), S.data_ptr(), sn, sc,
+                       self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                       V.data_ptr(), vn, vc, iters.data_ptr(), 0 if resid is None else resid.data_ptr(),
+                       self._ws.data_ptr(), self._ws.numel(), stream_ptr(self.device))
+            return V, iters
         if self.tree is not None:
             if self._ws is None:
                 self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
