@@ -133,26 +133,29 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
 
 /* Radial-feeder sparse solver, warp-per-subtree (default for radial feeders
  * whose schedule fits; paper_2403_04578_b200.subtree.subtree_schedule): the
- * tree LU is cut at depth D, subtrees are packed onto 12 warps and swept with
- * __syncwarp only, the top (depth < D) is swept by every warp on a private
- * copy; one CTA barrier per iteration.  One case per SM; per case the loads
- * come in by TMA (one column of node-major S, cp.async.bulk.tensor, or one
- * case-major column, cp.async.bulk), the next case's column is prefetched
- * into L2, V goes out by TMA, and the residual post-check (fpi.py:221-240)
- * is fused when resid != null.  Same arithmetic and bits as
- * tpf_sparse_tree_fpi_c128.
- *   meta        HOST int32[24]: per warp the first depth-D slot (12), then the
- *               __syncwarp mask (12)
- *   nsl, ns     slots per thread (6, 9, 12, 15, 18 or 21) and subtree slots
- *   rmax, rw    root slots per warp, residual row width (<= 16)
- *   pinfo       int32[2 * P] (P = 12 * nsl * 32 positions), kids uint16[nkids],
- *   coef        complex[3 * P] (g, 1/U[m,m], src), ell_col int32[rw * P],
- *   ell_val     complex[rw * P]: device arrays of the schedule
+ * tree LU is cut at depth D, the subtrees are packed onto 12 warps and
+ * list-scheduled into slots of 32 independent nodes swept with __syncwarp
+ * only (two slots at a time where independent), the top (depth < D) is swept
+ * by every warp on a private copy; one CTA barrier per iteration.  One case
+ * per SM; per thread and slot the iterate, the load and z / U_mm live in
+ * Tensor Memory.  Per case the loads come in by TMA (one column of
+ * node-major S, cp.async.bulk.tensor, or one case-major column,
+ * cp.async.bulk), the next case's column is prefetched into L2, V goes out
+ * by TMA, and the residual post-check (fpi.py:221-240) is fused when
+ * resid != null.  Same arithmetic and bits as tpf_sparse_tree_fpi_c128.
+ *   ns, nt      subtree slots (8 * ns + 4 * y-slots <= 168) and top slots
+ *   rmax, rw    root slots per warp, residual row width (<= 8)
+ *   pinfo       int32[2 * P] (P = 12 * (ns + nt) * 32 positions),
+ *   slotinfo    int32[12 * ns], kids uint16[nkids], coef complex[3 * P]
+ *               (g, 1/U[m,m], src), ell_col int32[rw * P], ell_val
+ *               complex[rw * P]: device arrays of the schedule
  *   S, V        node-major (case stride 1) or case-major (node stride 1), 16-B aligned
- *   workspace  >= 256 device bytes                                          */
+ *   workspace  >= 256 device bytes
+ * tpf_sparse_subtree_smem_bytes: the kernel's shared memory for a schedule. */
 int tpf_sparse_subtree_warps(void);
-int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t* meta, int32_t nsl, int32_t ns,
-                                int32_t rmax, int32_t rw, int32_t nkids, const int32_t* pinfo,
+size_t tpf_sparse_subtree_smem_bytes(int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t nkids);
+int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t rw,
+                                int32_t nkids, const int32_t* pinfo, const int32_t* slotinfo,
                                 const uint16_t* kids, const double* coef, const int32_t* ell_col,
                                 const double* ell_val, const double* S, int64_t s_node_stride,
                                 int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,

@@ -45,30 +45,30 @@ namespace {
 constexpr int kSubWarps = 12;
 constexpr int kSubThreads = 32 * kSubWarps;
 constexpr int kParentNone = -32768;
-constexpr int kMaxRW = 16;
+constexpr int kMaxRW = 8;   // residual row width (diagonal + parent + children)
+constexpr int kSubKmax = 8;  // children per node (paper_2403_04578_b200/subtree.py SUB_KMAX)
 
 struct SubArgs {
   int64_t tau;
-  int b, NS, RMAX, RW, P, xcap, nkids;
+  int b, NS, NT, NSL, RMAX, RW, P, xcap, nkids;
   int mode;      // 0: node-major S / V (2-D TMA), 1: case-major (1-D bulk)
   int nbox, boxrows;
   const double2* S;
   int64_t s_case;  // mode 1: case stride (complex elements)
   double2* V;
   int64_t v_case;
-  const int2* pinfo;      // [P]
-  const uint16_t* kids;   // [nkids]
-  const double2* coef;    // [3][P]: g, 1/U[m,m], src
-  const int32_t* ell_col; // [RW][P]
-  const double2* ell_val; // [RW][P]
+  const int2* pinfo;       // [P]
+  const int32_t* slotinfo; // [W][NS]
+  const uint16_t* kids;    // [nkids]
+  const double2* coef;     // [3][P]: g, 1/U[m,m], src
+  const int32_t* ell_col;  // [RW][P]
+  const double2* ell_val;  // [RW][P]
   int32_t* iters;
-  double* resid;          // or null
+  double* resid;           // or null
   unsigned long long* counter;
   double2 v_flat;
   double tol2;
   int max_iter;
-  int jD[kSubWarps];
-  unsigned sync[kSubWarps];
 };
 
 // ---- TMA / bulk-copy helpers (sm_90+ async proxy) ----
@@ -119,24 +119,78 @@ __device__ __forceinline__ double2 cfma_sub_s(double2 acc, double2 a, double2 x)
   return make_double2(__fma_rn(-a.x, x.x, __fma_rn(a.y, x.y, acc.x)), __fma_rn(-a.x, x.y, __fma_rn(-a.y, x.x, acc.y)));
 }
 
-template <int NSL>
+// TMEM access without a compiler memory clobber: Tensor Memory is not
+// addressable by ordinary loads/stores, so independent global / shared loads
+// may be scheduled across these (program order among the volatile asm
+// statements themselves is kept).
+__device__ __forceinline__ void tld2(uint32_t taddr, D2& o) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(o.r[0]), "=r"(o.r[1]), "=r"(o.r[2]), "=r"(o.r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tst2(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)), "r"(__double2hiint(v.y)));
+}
+__device__ __forceinline__ void twait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;"); }
+__device__ __forceinline__ void twait_st() { asm volatile("tcgen05.wait::st.sync.aligned;"); }
+
+// shared memory through 32-bit addresses (no generic-to-shared conversion per access)
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int2 lds_i2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double2 rhs_of(double2 v, const double2 sl, const double2 src) {
+  // r_m = -(s*/conj(v) + src) on the guarded v (fpi.py:39-41), s*/conj(v) = conj(s) v / |v|^2
+  double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+  if (m2 < kZeroGuard2) {
+    v = make_double2(kZeroGuard, 0.0);
+    m2 = kZeroGuard * kZeroGuard;
+  }
+  const double r = rcp_nr(m2);
+  return make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
+                      -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
+}
+
 __global__ void __launch_bounds__(kSubThreads, 1)
     sparse_subtree_kernel(const __grid_constant__ SubArgs a, const __grid_constant__ CUtensorMap tmS,
                           const __grid_constant__ CUtensorMap tmV) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  double2* X = reinterpret_cast<double2*>(smem_raw);                 // [xcap]
-  int2* PI = reinterpret_cast<int2*>(X + a.xcap);                    // [P]
-  double2* PR = reinterpret_cast<double2*>(PI + a.P);                // [2][W * RMAX * 32]
-  uint16_t* KD = reinterpret_cast<uint16_t*>(PR + 2 * kSubWarps * a.RMAX * 32);  // [nkids]
+  const int RR = kSubWarps * a.RMAX * 32;
+  const int P = a.P, NS = a.NS, NT = a.NT, xcap = a.xcap;
+  const int NTOP = kSubWarps * NT * 32;
+  double2* X = reinterpret_cast<double2*>(smem_raw);  // [xcap | Proot parity 0 | parity 1 | zero]
+  double2* TV = X + xcap + 2 * RR + 1;                 // top copies: iterate, load, z / U_mm
+  double2* TS = TV + NTOP;
+  double2* TY = TS + NTOP;
+  int2* PI = reinterpret_cast<int2*>(TY + NTOP);       // [P]
+  int32_t* SI = reinterpret_cast<int32_t*>(PI + P);   // [W][NS]
+  uint16_t* KD = reinterpret_cast<uint16_t*>(SI + kSubWarps * NS);  // [nkids]
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ int s_case, s_next;
   __shared__ double s_red[kSubWarps];
   __shared__ uint32_t s_tmem;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int P = a.P, NS = a.NS;
   for (int i = tid; i < P; i += kSubThreads) PI[i] = __ldg(a.pinfo + i);
+  for (int i = tid; i < kSubWarps * NS; i += kSubThreads) SI[i] = __ldg(a.slotinfo + i);
   for (int i = tid; i < a.nkids; i += kSubThreads) KD[i] = __ldg(a.kids + i);
+  if (tid == 0) X[xcap + 2 * RR] = make_double2(0.0, 0.0);
   if (warp == 0) tmem_alloc(&s_tmem, 512);
   if (tid == 0) {
     mbar_init(&s_bar, 1);
@@ -145,32 +199,25 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  // TMEM: lane quadrant warp % 4, column group warp / 4 (3 groups of 8 * NSL <= 168 columns)
-  const uint32_t tm = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 8 * NSL);
-  const uint32_t tm_v = tm, tm_s = tm + 4 * NSL;
-  const int base = warp * NSL * 32 + lane;  // position of slot j: base + 32 j
-  const int topbase = (warp * NSL + NS) * 32;
-  const int jD = a.jD[warp];
-  const unsigned syncm = a.sync[warp];
-  const int RR = kSubWarps * a.RMAX * 32;
-  unsigned vmask = 0;  // slots holding a node for this thread
-#pragma unroll
-  for (int j = 0; j < NSL; ++j)
-    if ((uint32_t(PI[base + 32 * j].y) >> 16) != 0xFFFFu) vmask |= 1u << j;
+  // TMEM per warp (lane quadrant warp % 4, column group warp / 4 of 168 columns):
+  // iterate V at 4 j, load S at 4 (NS + j), z / U_mm of y-slot y at 4 (2 NS + y)
+  const uint32_t tm = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 168);
+  const uint32_t tV = tm, tS = tm + 4 * NS, tY = tm + 8 * NS;
+  const int base = warp * a.NSL * 32 + lane;  // position of slot j: base + 32 j
+  const int topbase = (warp * a.NSL + NS) * 32;
+  const int tpriv = warp * NT * 32 + lane;    // top copy of slot t: tpriv + 32 t
+  const int32_t* si_w = SI + warp * NS;
   const double2* cg = a.coef;
   const double2* cu = a.coef + P;
-  const double2* cs_src = a.coef + 2 * P;
+  const double2* csrc = a.coef + 2 * P;
   const uint32_t in_bytes =
       a.mode == 0 ? uint32_t(a.nbox) * uint32_t(a.boxrows) * 16u : uint32_t(a.b) * 16u;
+  const uint32_t xs = smem_u32(X), pi_s = smem_u32(PI), kd_s = smem_u32(KD);
+  const uint32_t zero_idx = uint32_t(xcap + 2 * RR);
 
   auto claim = [&]() {
     const unsigned long long c = atomicAdd(a.counter, 1ull);
     return c < (unsigned long long)a.tau ? int(c) : -1;
-  };
-  auto child_val = [&](unsigned code, int par) -> double2 {
-    if (code >= 0xC000u) return PR[par * RR + int(code - 0xC000u)];
-    if (code >= 0x8000u) return X[topbase + int(code - 0x8000u)];
-    return X[code];
   };
   if (tid == 0) {
     s_case = claim();
@@ -178,7 +225,6 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   }
   __syncthreads();
   uint32_t phase = 0;
-  double2 zr[NSL];
 
   for (;;) {
     const int cs = s_case, nx = s_next;
@@ -197,102 +243,211 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     }
     mbar_wait(&s_bar, phase);
     phase ^= 1u;
-#pragma unroll
-    for (int j = 0; j < NSL; ++j) {
-      double2 s = make_double2(0.0, 0.0);
-      if (vmask >> j & 1u) s = X[uint32_t(PI[base + 32 * j].y) >> 16];
-      tmem_st2(tm_s + 4 * j, s);
-      tmem_st2(tm_v + 4 * j, a.v_flat);  // flat start (dense.py:155)
+    for (int j = 0; j < NS; ++j) {
+      const uint32_t o = uint32_t(PI[base + 32 * j].y) >> 16;
+      tst2(tS + 4 * j, o != 0xFFFFu ? X[o] : make_double2(0.0, 0.0));
+      tst2(tV + 4 * j, a.v_flat);  // flat start (dense.py:155)
     }
-    tmem_wait_st();
+    for (int t = 0; t < NT; ++t) {
+      const uint32_t o = uint32_t(PI[topbase + 32 * t + lane].y) >> 16;
+      TS[tpriv + 32 * t] = o != 0xFFFFu ? X[o] : make_double2(0.0, 0.0);
+      TV[tpriv + 32 * t] = a.v_flat;
+    }
+    twait_st();
     __syncthreads();  // X is free for the sweeps
 
     int it = 0;
     bool small = false;
     for (;;) {
-      const int par = it & 1;
-      // ---- up-sweep: slots 0..NS-1 (subtrees), barrier, NS..NSL-1 (top) ----
-#pragma unroll
-      for (int j = 0; j < NSL; ++j) {
-        if (j == NS) {
-          // the previous iteration's step test, AND over the CTA (false at it = 0)
-          if (__syncthreads_and(small)) goto converged;
-        }
-        {
-          D2 vv, ss;
-          tmem_ld2(tm_v + 4 * j, vv);
-          tmem_ld2(tm_s + 4 * j, ss);
-          tmem_wait_ld();
-          if (vmask >> j & 1u) {
-            const int p = base + 32 * j;
-            const int2 pi = PI[p];
-            const int pc = int(int16_t(pi.x & 0xFFFF));
-            double2 v = vv.get();
-            const double2 sl = ss.get();
-            double m2 = __fma_rn(v.x, v.x, v.y * v.y);
-            if (m2 < kZeroGuard2) {  // fpi.py:39-41
-              v = make_double2(kZeroGuard, 0.0);
-              m2 = kZeroGuard * kZeroGuard;
-            }
-            const double r = rcp_nr(m2);
-            const double2 src = pc == kParentNone ? __ldg(cs_src + p) : make_double2(0.0, 0.0);
-            // r_m = -(s*/conj(v) + src),  s*/conj(v) = conj(s) v / |v|^2
-            double2 z = make_double2(-(__fma_rn(sl.x, v.x, sl.y * v.y) * r + src.x),
-                                     -(__fma_rn(sl.x, v.y, -(sl.y * v.x)) * r + src.y));
-            const int kf = int(uint32_t(pi.x) >> 16), kc = pi.y & 0xFF;
-            for (int k = 0; k < kc; ++k) {
-              const double2 pcv = child_val(KD[kf + k], par);
-              z.x -= pcv.x;
-              z.y -= pcv.y;
-            }
-            zr[j] = z;
-            const double2 P_m = cmul_s(__ldg(cg + p), z);
-            X[p] = P_m;
-            if (j < NS && j >= jD && pc < 0 && pc != kParentNone)
-              PR[par * RR + (warp * a.RMAX + j - jD) * 32 + lane] = P_m;
+      const int shift = (it & 1) ? RR : 0;  // Proot parity
+      // ---- subtree up-sweep: z_m = r_m - sum_c X[c], X[m] = g_m z_m, y_m = z_m / U_mm ----
+      {
+        auto up_one = [&](const int j, const D2& vv, const D2& ss, const int2 pi, const int si, const double2 g,
+                          const double2 u) {
+          double2 z = rhs_of(vv.get(), ss.get(), make_double2(0.0, 0.0));
+          const int km = si & 0xF;
+          const uint32_t kf = uint32_t(pi.x) >> 16, kc = uint32_t(pi.y) & 0xF;
+#pragma unroll 4
+          for (int k = 0; k < km; ++k) {  // branch-free: lanes past their own count read the zero slot
+            const uint32_t e = lds_u16(kd_s + 2 * (kf + k));
+            const double2 c = lds2(xs + 16 * (uint32_t(k) < kc ? e : zero_idx));
+            z.x -= c.x;
+            z.y -= c.y;
           }
+          const double2 P_m = cmul_s(g, z);
+          sts2(xs + 16 * (base + 32 * j), P_m);
+          const int root = (pi.y >> 4) & 0xFFF;
+          if (root) sts2(xs + 16 * (xcap + shift + root - 1), P_m);  // subtree root: to the top via Proot
+          const int ys = si >> 5;
+          if (ys) tst2(tY + 4 * (ys - 1), cmul_s(z, u));  // leaf-only slots recompute it later
+        };
+        // one step = one slot, or two independent slots; the coefficients of the
+        // next step are loaded one step ahead (two register sets, loop body
+        // unrolled twice so the sets alternate without moves)
+        auto up_step = [&](int& j, double2& g0, double2& u0, double2& g1, double2& u1, double2& gn0, double2& un0,
+                           double2& gn1, double2& un1) {
+          const int p0 = base + 32 * j;
+          const int si0 = si_w[j];
+          const bool pair = (si0 >> 4 & 1) && j + 1 < NS;
+          const int jn = j + (pair ? 2 : 1);
+          if (jn < NS) {
+            gn0 = __ldg(cg + base + 32 * jn);
+            un0 = __ldg(cu + base + 32 * jn);
+            gn1 = __ldg(cg + base + 32 * (jn + 1));
+            un1 = __ldg(cu + base + 32 * (jn + 1));
+          }
+          if (pair) {
+            D2 v0, s0, v1, s1;
+            tld2(tV + 4 * j, v0);
+            tld2(tS + 4 * j, s0);
+            tld2(tV + 4 * (j + 1), v1);
+            tld2(tS + 4 * (j + 1), s1);
+            const int2 pi0 = lds_i2(pi_s + 8 * p0), pi1 = lds_i2(pi_s + 8 * (p0 + 32));
+            const int si1 = si_w[j + 1];
+            twait_ld();
+            up_one(j, v0, s0, pi0, si0, g0, u0);
+            up_one(j + 1, v1, s1, pi1, si1, g1, u1);
+          } else {
+            D2 v0, s0;
+            tld2(tV + 4 * j, v0);
+            tld2(tS + 4 * j, s0);
+            const int2 pi0 = lds_i2(pi_s + 8 * p0);
+            twait_ld();
+            up_one(j, v0, s0, pi0, si0, g0, u0);
+          }
+          __syncwarp();
+          j = jn;
+        };
+        double2 ga0 = __ldg(cg + base), ua0 = __ldg(cu + base), ga1 = __ldg(cg + base + 32), ua1 = __ldg(cu + base + 32);
+        double2 gb0, ub0, gb1, ub1;
+        int j = 0;
+        while (j < NS) {
+          up_step(j, ga0, ua0, ga1, ua1, gb0, ub0, gb1, ub1);
+          if (j >= NS) break;
+          up_step(j, gb0, ub0, gb1, ub1, ga0, ua0, ga1, ua1);
         }
-        if (syncm >> j & 1u) __syncwarp();
       }
-      // ---- down-sweep: top slots (root level first), then subtrees, leaves last ----
+      // the previous iteration's step test, AND over the CTA (false at it = 0); the
+      // subtree roots' products are visible after this barrier
+      if (__syncthreads_and(small)) break;
+      // ---- top (every warp on its own copy): up-sweep, then down-sweep ----
       small = true;
-#pragma unroll
-      for (int j = NSL - 1; j >= 0; --j) {
-        if (j < NSL - 1 && (syncm >> j & 1u)) __syncwarp();
-        if (j == NS - 1) __syncwarp();
-        D2 vv;
-        tmem_ld2(tm_v + 4 * j, vv);
-        tmem_wait_ld();
-        double2 v = vv.get();
-        double2 w = v;
-        if (vmask >> j & 1u) {
-          const int p = base + 32 * j;
-          const int pc = int(int16_t(PI[p].x & 0xFFFF));
-          w = cmul_s(zr[j], __ldg(cu + p));
-          if (pc != kParentNone) {
-            const double2 wp = pc < 0 ? X[topbase + (-1 - pc)] : X[pc];
-            w = cfma_sub_s(w, __ldg(cg + p), wp);
+      for (int t = 0; t < NT; ++t) {
+        const int p = topbase + 32 * t + lane, q = tpriv + 32 * t;
+        const int2 pi = PI[p];
+        if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
+          const int pc = pi.x & 0xFFFF;
+          const double2 src = pc == 0xFFFF ? __ldg(csrc + p) : make_double2(0.0, 0.0);  // next to the slack
+          double2 z = rhs_of(TV[q], TS[q], src);
+          const int kf = int(uint32_t(pi.x) >> 16), kc = pi.y & 0xF;
+          for (int k = 0; k < kc; ++k) {
+            int idx = KD[kf + k];
+            if (idx >= xcap) idx += shift;  // a subtree root: Proot
+            const double2 c = X[idx];
+            z.x -= c.x;
+            z.y -= c.y;
           }
+          X[p] = cmul_s(__ldg(cg + p), z);
+          TY[q] = cmul_s(z, __ldg(cu + p));
+        }
+        __syncwarp();
+      }
+      for (int t = NT - 1; t >= 0; --t) {
+        const int p = topbase + 32 * t + lane, q = tpriv + 32 * t;
+        const int2 pi = PI[p];
+        if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
+          const int pc = pi.x & 0xFFFF;
+          double2 w = TY[q];
+          if (pc != 0xFFFF) w = cfma_sub_s(w, __ldg(cg + p), X[pc]);
           X[p] = w;
+          double2 v = TV[q];
           if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
           const double dr = w.x - v.x, di = w.y - v.y;
           if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
+          TV[q] = w;
         }
-        tmem_st2(tm_v + 4 * j, w);
+        __syncwarp();
       }
-      tmem_wait_st();
+      // ---- subtree down-sweep: w_m = y_m - g_m w_parent, step test |w - v|^2 < tol^2 ----
+      {
+        auto down_one = [&](const int j, const D2& vv, const D2& ys_or_s, const int2 pi, const int si,
+                            const double2 g, const double2 u) {
+          double2 v = vv.get();
+          // y_m from TMEM, or (leaf-only slot) recomputed: same operations, same bits
+          double2 w = (si >> 5) ? ys_or_s.get() : cmul_s(rhs_of(v, ys_or_s.get(), make_double2(0.0, 0.0)), u);
+          const uint32_t pc = uint32_t(pi.x) & 0xFFFF;
+          if (pc != 0xFFFF) w = cfma_sub_s(w, g, lds2(xs + 16 * pc));
+          sts2(xs + 16 * (base + 32 * j), w);
+          if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+          const double dr = w.x - v.x, di = w.y - v.y;
+          if ((uint32_t(pi.y) >> 16) != 0xFFFFu && !(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;
+          tst2(tV + 4 * j, w);
+        };
+        auto down_step = [&](int& j, double2& g0, double2& u0, double2& g1, double2& u1, double2& gn0,
+                             double2& un0, double2& gn1, double2& un1) {
+          const int p0 = base + 32 * j;
+          const int si0 = si_w[j];
+          const bool pair = j >= 1 && (si_w[j - 1] >> 4 & 1);
+          const int jn = j - (pair ? 2 : 1);
+          if (jn >= 0) {
+            gn0 = __ldg(cg + base + 32 * jn);
+            un0 = __ldg(cu + base + 32 * jn);
+            if (jn >= 1) {
+              gn1 = __ldg(cg + base + 32 * (jn - 1));
+              un1 = __ldg(cu + base + 32 * (jn - 1));
+            }
+          }
+          if (pair) {
+            const int si1 = si_w[j - 1];
+            D2 v0, y0, v1, y1;
+            tld2(tV + 4 * j, v0);
+            tld2((si0 >> 5) ? tY + 4 * ((si0 >> 5) - 1) : tS + 4 * j, y0);
+            tld2(tV + 4 * (j - 1), v1);
+            tld2((si1 >> 5) ? tY + 4 * ((si1 >> 5) - 1) : tS + 4 * (j - 1), y1);
+            const int2 pi0 = lds_i2(pi_s + 8 * p0), pi1 = lds_i2(pi_s + 8 * (p0 - 32));
+            twait_ld();
+            down_one(j, v0, y0, pi0, si0, g0, u0);
+            down_one(j - 1, v1, y1, pi1, si1, g1, u1);
+          } else {
+            D2 v0, y0;
+            tld2(tV + 4 * j, v0);
+            tld2((si0 >> 5) ? tY + 4 * ((si0 >> 5) - 1) : tS + 4 * j, y0);
+            const int2 pi0 = lds_i2(pi_s + 8 * p0);
+            twait_ld();
+            down_one(j, v0, y0, pi0, si0, g0, u0);
+          }
+          __syncwarp();
+          j = jn;
+        };
+        int j = NS - 1;
+        double2 ga0 = __ldg(cg + base + 32 * j), ua0 = __ldg(cu + base + 32 * j);
+        double2 ga1 = j >= 1 ? __ldg(cg + base + 32 * (j - 1)) : ga0;
+        double2 ua1 = j >= 1 ? __ldg(cu + base + 32 * (j - 1)) : ua0;
+        double2 gb0 = ga0, ub0 = ua0, gb1 = ga1, ub1 = ua1;
+        while (j >= 0) {
+          down_step(j, ga0, ua0, ga1, ua1, gb0, ub0, gb1, ub1);
+          if (j < 0) break;
+          down_step(j, gb0, ub0, gb1, ub1, ga0, ua0, ga1, ua1);
+        }
+      }
+      twait_st();
       ++it;
       if (it == a.max_iter) break;
     }
-  converged:
     __syncthreads();  // every warp is done with X (the cap path leaves without a barrier)
     // ---- retire: V into X in original node order (top nodes: warp 0's copy) ----
-#pragma unroll
-    for (int j = 0; j < NSL; ++j) {
+    for (int j = 0; j < NS; ++j) {
       D2 vv;
-      tmem_ld2(tm_v + 4 * j, vv);
-      tmem_wait_ld();
-      if ((vmask >> j & 1u) && (j < NS || warp == 0)) X[uint32_t(PI[base + 32 * j].y) >> 16] = vv.get();
+      tld2(tV + 4 * j, vv);
+      twait_ld();
+      const uint32_t o = uint32_t(PI[base + 32 * j].y) >> 16;
+      if (o != 0xFFFFu) X[o] = vv.get();
+    }
+    if (warp == 0) {
+      for (int t = 0; t < NT; ++t) {
+        const uint32_t o = uint32_t(PI[topbase + 32 * t + lane].y) >> 16;
+        if (o != 0xFFFFu) X[o] = TV[tpriv + 32 * t];
+      }
     }
     fence_async_smem();
     __syncthreads();
@@ -307,40 +462,53 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     }
     if (a.resid) {
       // residual_per_case (fpi.py:221-240): max_i |s_i + v_i conj(src_i + (Y_dd v)_i)|,
-      // the operations of residual_kernel in the same order (Y_dd rows in CSR order)
+      // the operations of residual_kernel in the same order (Y_dd rows in CSR order;
+      // padding columns -1); the next slot's row is loaded while this one is summed
       double worst = 0.0;
+      const int nres = NS + (warp == 0 ? NT : 0);
+      int cn[kMaxRW];
+      double2 yn[kMaxRW];
+      auto load_row = [&](const int j, int* c, double2* y) {
+        const int p = base + 32 * j;
 #pragma unroll
-      for (int j = 0; j < NSL; ++j) {
-        D2 sd;
-        tmem_ld2(tm_s + 4 * j, sd);
-        tmem_wait_ld();
+        for (int r = 0; r < kMaxRW; ++r) {
+          c[r] = r < a.RW ? __ldg(a.ell_col + r * P + p) : -1;
+          y[r] = r < a.RW ? __ldg(a.ell_val + r * P + p) : make_double2(0.0, 0.0);
+        }
+      };
+      load_row(0, cn, yn);
+      for (int j = 0; j < nres; ++j) {
+        int c[kMaxRW];
+        double2 y[kMaxRW];
+#pragma unroll
+        for (int r = 0; r < kMaxRW; ++r) {
+          c[r] = cn[r];
+          y[r] = yn[r];
+        }
+        if (j + 1 < nres) load_row(j + 1, cn, yn);
         const int p = base + 32 * j;
         const int2 pi = PI[p];
-        const int rl = (pi.y >> 8) & 0xFF;
-        if ((vmask >> j & 1u) && rl > 0) {
-          const double2 si = __ldg(cs_src + p);
+        double2 sl;
+        if (j < NS) {
+          D2 sd;
+          tld2(tS + 4 * j, sd);
+          twait_ld();
+          sl = sd.get();
+        } else {
+          sl = TS[tpriv + 32 * (j - NS)];
+        }
+        if (c[0] >= 0) {
+          const double2 si = __ldg(csrc + p);
           double ar = si.x, ai = si.y;
-          for (int r0 = 0; r0 < rl; r0 += 4) {  // ELL entries 4 at a time (loads issued together)
-            int c[4];
-            double2 y[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              if (r0 + r < rl) {
-                c[r] = __ldg(a.ell_col + (r0 + r) * P + p);
-                y[r] = __ldg(a.ell_val + (r0 + r) * P + p);
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              if (r0 + r < rl) {
-                const double2 v = X[c[r]];
-                ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
-                ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
-              }
+          for (int r = 0; r < kMaxRW; ++r) {
+            if (c[r] >= 0) {
+              const double2 v = X[c[r]];
+              ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
+              ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
             }
           }
           const double2 v = X[uint32_t(pi.y) >> 16];
-          const double2 sl = sd.get();
           const double mr = sl.x + (v.x * ar + v.y * ai);
           const double mi = sl.y + (v.y * ar - v.x * ai);
           worst = nanmax(worst, hypot(mr, mi));
@@ -397,10 +565,9 @@ int column_map(CUtensorMap* m, const void* base, int64_t tau, int b, int64_t nod
   return TPF_OK;
 }
 
-template <int NSL>
 int sub_launch(const SubArgs& a, const CUtensorMap& ms, const CUtensorMap& mv, size_t smem, int grid,
                cudaStream_t st) {
-  auto kern = sparse_subtree_kernel<NSL>;
+  auto kern = sparse_subtree_kernel;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(subtree)", err);
   kern<<<unsigned(grid), kSubThreads, smem, st>>>(a, ms, mv);
@@ -416,8 +583,17 @@ using namespace tpf;
 
 extern "C" int tpf_sparse_subtree_warps(void) { return kSubWarps; }
 
-extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t* meta, int32_t nsl, int32_t ns,
-                                           int32_t rmax, int32_t rw, int32_t nkids, const int32_t* pinfo,
+extern "C" size_t tpf_sparse_subtree_smem_bytes(int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t nkids) {
+  const int64_t P = int64_t(kSubWarps) * (ns + nt) * 32;
+  const int boxrows = b < 256 ? b : 256;
+  const int64_t nbox = (b + boxrows - 1) / boxrows;
+  const int64_t xcap = P > nbox * boxrows ? P : nbox * boxrows;
+  return size_t(xcap + int64_t(2) * kSubWarps * rmax * 32 + 1) * 16 + size_t(3) * kSubWarps * nt * 32 * 16 +
+         size_t(P) * 8 + size_t(kSubWarps) * ns * 4 + (size_t(nkids) * 2 + 15) / 16 * 16;
+}
+
+extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t rw,
+                                           int32_t nkids, const int32_t* pinfo, const int32_t* slotinfo,
                                            const uint16_t* kids, const double* coef, const int32_t* ell_col,
                                            const double* ell_val, const double* S, int64_t s_node_stride,
                                            int64_t s_case_stride, double v_flat_re, double v_flat_im, double tol,
@@ -429,10 +605,10 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
   if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
   if (tau == 0) return TPF_OK;
-  if (!meta || !pinfo || !kids || !coef || !ell_col || !ell_val || !S || !V || !iters || !workspace ||
+  if (!pinfo || !slotinfo || !kids || !coef || !ell_col || !ell_val || !S || !V || !iters || !workspace ||
       workspace_bytes < 256)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_fpi_c128: null pointer or small workspace");
-  if (ns < 1 || ns >= nsl || rmax < 1 || rw < 1 || rw > kMaxRW || nkids < 1)
+  if (ns < 1 || nt < 1 || 8 * ns > 168 || rmax < 1 || rw < 1 || rw > kMaxRW || nkids < 1)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_fpi_c128: bad schedule");
   int mode;
   if (s_case_stride == 1 && v_case_stride == 1 && s_node_stride >= tau && v_node_stride >= tau)
@@ -448,9 +624,11 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t
   a.tau = tau;
   a.b = b;
   a.NS = ns;
+  a.NT = nt;
+  a.NSL = ns + nt;
   a.RMAX = rmax;
   a.RW = rw;
-  a.P = kSubWarps * nsl * 32;
+  a.P = kSubWarps * a.NSL * 32;
   a.boxrows = b < 256 ? b : 256;
   a.nbox = (b + a.boxrows - 1) / a.boxrows;
   a.xcap = a.P > a.nbox * a.boxrows ? a.P : a.nbox * a.boxrows;
@@ -461,6 +639,7 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t
   a.V = reinterpret_cast<double2*>(V);
   a.v_case = v_case_stride;
   a.pinfo = reinterpret_cast<const int2*>(pinfo);
+  a.slotinfo = slotinfo;
   a.kids = kids;
   a.coef = reinterpret_cast<const double2*>(coef);
   a.ell_col = ell_col;
@@ -471,12 +650,7 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t
   a.v_flat = make_double2(v_flat_re, v_flat_im);
   a.tol2 = tol * tol;
   a.max_iter = max_iter;
-  for (int w = 0; w < kSubWarps; ++w) {
-    a.jD[w] = meta[w];
-    a.sync[w] = unsigned(meta[kSubWarps + w]);
-  }
-  const size_t smem = size_t(a.xcap) * 16 + size_t(a.P) * 8 + size_t(2) * kSubWarps * rmax * 32 * 16 +
-                      (size_t(nkids) * 2 + 15) / 16 * 16;
+  const size_t smem = tpf_sparse_subtree_smem_bytes(b, ns, nt, rmax, nkids);
   if (smem > 227 * 1024) return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_subtree_fpi_c128: schedule too large");
   CUtensorMap ms, mv;
   memset(&ms, 0, sizeof ms);
@@ -494,14 +668,5 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, const int32_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = int(tau < sms ? tau : sms);
-  switch (nsl) {
-    case 6: return sub_launch<6>(a, ms, mv, smem, grid, st);
-    case 9: return sub_launch<9>(a, ms, mv, smem, grid, st);
-    case 12: return sub_launch<12>(a, ms, mv, smem, grid, st);
-    case 15: return sub_launch<15>(a, ms, mv, smem, grid, st);
-    case 18: return sub_launch<18>(a, ms, mv, smem, grid, st);
-    case 21: return sub_launch<21>(a, ms, mv, smem, grid, st);
-    default: break;
-  }
-  return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_subtree_fpi_c128: unsupported slot count");
+  return sub_launch(a, ms, mv, smem, grid, st);
 }

@@ -521,8 +521,8 @@ class SparseOperator:
         if self.sub is not None:
             sb = self.sub
             self.sub_dev = dict(pinfo=t(sb.pinfo), kids=torch.from_numpy(sb.kids.view(np.int16).copy()).to(d),
-                                coef=t(sb.coef), ell_col=t(sb.ell_col), ell_val=t(sb.ell_val),
-                                meta=np.ascontiguousarray(sb.meta, dtype=np.int32))
+                                slotinfo=t(sb.slotinfo), coef=t(sb.coef), ell_col=t(sb.ell_col),
+                                ell_val=t(sb.ell_val))
         if levels is not None:
             # the level kernel: radial feeders without a subtree schedule, and
             # the fallback for S / V layouts the subtree kernel's TMA cannot move
@@ -573,8 +573,8 @@ class SparseOperator:
             sb, g = self.sub, self.sub_dev
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
-            _capi.call("tpf_sparse_subtree_fpi_c128", tau, b, g["meta"].ctypes.data, sb.NSL, sb.NS, sb.RMAX, sb.RW,
-                       int(sb.kids.size), g["pinfo"].data_ptr(), g["kids"].data_ptr(), g["coef"].data_ptr(),
+            _capi.call("tpf_sparse_subtree_fpi_c128", tau, b, sb.NS, sb.NT, sb.RMAX, sb.RW, int(sb.kids.size),
+                       g["pinfo"].data_ptr(), g["slotinfo"].data_ptr(), g["kids"].data_ptr(), g["coef"].data_ptr(),
                        g["ell_col"].data_ptr(), g["ell_val"].data_ptr(), S.data_ptr(), sn, sc,
                        self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                        V.data_ptr(), vn, vc, iters.data_ptr(), 0 if resid is None else resid.data_ptr(),

@@ -71,3 +71,12 @@ n = int(it.sum())
 r = {"ms": ms, "sum_iters": n, "max_iters": int(it.max()), "alg_GBps": 48 * 5000 * n / ms / 1e6,
      "compulsory_GBps": 32 * 5000 * tau / ms / 1e6, "kernel": op.kernel, "resid_max": float(rs.max())}
 print(json.dumps({"c3_full": r}), flush=True)
+
+# case-major (F-order) S / V: each case's column is one contiguous 80 KB block (1-D bulk copies)
+Sf = S.t().contiguous().t()
+del S
+torch.cuda.empty_cache()
+Vf = torch.empty_like(Sf)
+ms = timed(lambda: op.solve(Sf, opts, V=Vf, iters=it, resid=rs), reps=2)
+r = {"ms": ms, "sum_iters": int(it.sum()), "alg_GBps": 48 * 5000 * n / ms / 1e6, "layout": "case-major"}
+print(json.dumps({"c3_full_case_major": r}), flush=True)
