@@ -150,9 +150,13 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
  *               (g, 1/U[m,m], src), ell_col int32[rw * P], ell_val
  *               complex[rw * P]: device arrays of the schedule
  *   S, V        node-major (case stride 1) or case-major (node stride 1), 16-B aligned
- *   workspace  >= 256 device bytes
+ *   workspace  >= 256 device bytes; with tpf_sparse_subtree_workspace_bytes(tau, b)
+ *               a node-major batch is solved in case-major chunks of 65,536
+ *               cases (transposed in and out on the device: contiguous
+ *               per-case columns instead of b scattered rows)
  * tpf_sparse_subtree_smem_bytes: the kernel's shared memory for a schedule. */
 int tpf_sparse_subtree_warps(void);
+size_t tpf_sparse_subtree_workspace_bytes(int64_t tau, int32_t b);
 size_t tpf_sparse_subtree_smem_bytes(int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t nkids);
 int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t rw,
                                 int32_t nkids, const int32_t* pinfo, const int32_t* slotinfo,

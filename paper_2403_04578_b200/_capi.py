@@ -73,6 +73,7 @@ SIGNATURES = {
     "tpf_sparse_tree_max_ell_width": (ctypes.c_int, []),
     "tpf_sparse_subtree_warps": (ctypes.c_int, []),
     "tpf_sparse_subtree_smem_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32]),
+    "tpf_sparse_subtree_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
     "tpf_sparse_subtree_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,

@@ -538,6 +538,39 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 
+// dst[c * ldd + r] = src[r * lds + c] for r < R, c < C (complex128), 32 x 32
+// tiles through shared memory: coalesced on both sides.  Node-major S
+// (b rows of cases) <-> case-major chunks (rows of b nodes) for the subtree
+// kernel, whose per-case column is then one contiguous 16 b-byte block.
+__global__ void __launch_bounds__(256) transpose_c128_kernel(const double2* __restrict__ src, int64_t lds,
+                                                             double2* __restrict__ dst, int64_t ldd, int64_t R,
+                                                             int64_t C) {
+  __shared__ double2 tile[32][33];
+  const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    if (r < R && c < C) tile[i][tx] = src[r * lds + c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + tx;
+    if (r < R && c < C) dst[c * ldd + r] = tile[tx][i];
+  }
+}
+
+int transpose_c128(const double2* src, int64_t lds, double2* dst, int64_t ldd, int64_t R, int64_t C,
+                   cudaStream_t st) {
+  if (R <= 0 || C <= 0) return TPF_OK;
+  const int64_t gx = (C + 31) / 32, gy = (R + 31) / 32;
+  if (gx > 0x7fffffff || gy > 65535) return set_error(TPF_ERR_INVALID, "transpose_c128: matrix too large");
+  transpose_c128_kernel<<<dim3(unsigned(gx), unsigned(gy)), dim3(32, 8), 0, st>>>(src, lds, dst, ldd, R, C);
+  const cudaError_t err = cudaGetLastError();
+  return err == cudaSuccess ? TPF_OK : set_cuda_error("launch(transpose_c128_kernel)", err);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -582,6 +615,13 @@ int sub_launch(const SubArgs& a, const CUtensorMap& ms, const CUtensorMap& mv, s
 using namespace tpf;
 
 extern "C" int tpf_sparse_subtree_warps(void) { return kSubWarps; }
+
+constexpr int64_t kSubChunk = 65536;  // cases per case-major chunk of a node-major batch
+
+extern "C" size_t tpf_sparse_subtree_workspace_bytes(int64_t tau, int32_t b) {
+  const int64_t chunk = tau < kSubChunk ? tau : kSubChunk;
+  return 256 + size_t(2) * size_t(chunk > 0 ? chunk : 0) * size_t(b > 0 ? b : 0) * 16;
+}
 
 extern "C" size_t tpf_sparse_subtree_smem_bytes(int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t nkids) {
   const int64_t P = int64_t(kSubWarps) * (ns + nt) * 32;
@@ -662,11 +702,42 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, i
     if (rc != TPF_OK) return rc;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
-  if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Node-major batches with a chunk workspace: each chunk is transposed into a
+  // case-major scratch, solved there (1-D bulk copies: one 16 b-byte block per
+  // case, one TLB page; a node-major column spans b rows of 16 tau bytes, one
+  // 2 MB page each at C3) and transposed back.
+  const int64_t chunk = tau < kSubChunk ? tau : kSubChunk;
+  const size_t need = size_t(2) * size_t(chunk) * size_t(b) * 16;
+  if (mode == 0 && workspace_bytes >= 256 + need) {
+    double2* Sc = reinterpret_cast<double2*>(static_cast<char*>(workspace) + 256);
+    double2* Vc = Sc + size_t(chunk) * size_t(b);
+    SubArgs c = a;
+    c.mode = 1;
+    c.S = Sc;
+    c.V = Vc;
+    c.s_case = b;
+    c.v_case = b;
+    for (int64_t lo = 0; lo < tau; lo += chunk) {
+      const int64_t n = tau - lo < chunk ? tau - lo : chunk;
+      int rc = transpose_c128(reinterpret_cast<const double2*>(S) + lo, s_node_stride, Sc, b, b, n, st);
+      if (rc != TPF_OK) return rc;
+      cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+      if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
+      c.tau = n;
+      c.iters = iters + lo;
+      c.resid = resid ? resid + lo : nullptr;
+      rc = sub_launch(c, ms, mv, smem, int(n < sms ? n : sms), st);
+      if (rc != TPF_OK) return rc;
+      rc = transpose_c128(Vc, b, reinterpret_cast<double2*>(V) + lo, v_node_stride, n, b, st);
+      if (rc != TPF_OK) return rc;
+    }
+    return TPF_OK;
+  }
+  cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+  if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
   const int grid = int(tau < sms ? tau : sms);
   return sub_launch(a, ms, mv, smem, grid, st);
 }

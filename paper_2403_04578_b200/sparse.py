@@ -568,8 +568,11 @@ class SparseOperator:
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
         if self.sub is not None and _subtree_layout_ok(S, V):
-            if self._ws is None:
-                self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+            # node-major batches are solved in case-major chunks (scratch in the workspace)
+            need = int(_capi.load().tpf_sparse_subtree_workspace_bytes(tau, b)) if S.stride(1) == 1 else 256
+            if self._ws is None or self._ws.numel() < need:
+                self._ws = None
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
             sb, g = self.sub, self.sub_dev
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
