@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           sts2(xs + 16 * (base + 32 * j), P_m);
           const int root = (pi.y >> 4) & 0xFFF;
           if (root) sts2(xs + 16 * (xcap + shift + root - 1), P_m);  // subtree root: to the top via Proot
-          const int ys = si >> 5;
+          const int ys = (si >> 5) & 0x1F;
           if (ys) tst2(tY + 4 * (ys - 1), cmul_s(z, u));  // leaf-only slots recompute it later
         };
         // one step = one slot, or two independent slots; the coefficients of the
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
                             const double2 g, const double2 u) {
           double2 v = vv.get();
           // y_m from TMEM, or (leaf-only slot) recomputed: same operations, same bits
-          double2 w = (si >> 5) ? ys_or_s.get() : cmul_s(rhs_of(v, ys_or_s.get(), make_double2(0.0, 0.0)), u);
+          double2 w = ((si >> 5) & 0x1F) ? ys_or_s.get() : cmul_s(rhs_of(v, ys_or_s.get(), make_double2(0.0, 0.0)), u);
           const uint32_t pc = uint32_t(pi.x) & 0xFFFF;
           if (pc != 0xFFFF) w = cfma_sub_s(w, g, lds2(xs + 16 * pc));
           sts2(xs + 16 * (base + 32 * j), w);
@@ -401,9 +401,9 @@ __global__ void __launch_bounds__(kSubThreads, 1)
             const int si1 = si_w[j - 1];
             D2 v0, y0, v1, y1;
             tld2(tV + 4 * j, v0);
-            tld2((si0 >> 5) ? tY + 4 * ((si0 >> 5) - 1) : tS + 4 * j, y0);
+            tld2(((si0 >> 5) & 0x1F) ? tY + 4 * (((si0 >> 5) & 0x1F) - 1) : tS + 4 * j, y0);
             tld2(tV + 4 * (j - 1), v1);
-            tld2((si1 >> 5) ? tY + 4 * ((si1 >> 5) - 1) : tS + 4 * (j - 1), y1);
+            tld2(((si1 >> 5) & 0x1F) ? tY + 4 * (((si1 >> 5) & 0x1F) - 1) : tS + 4 * (j - 1), y1);
             const int2 pi0 = lds_i2(pi_s + 8 * p0), pi1 = lds_i2(pi_s + 8 * (p0 - 32));
             twait_ld();
             down_one(j, v0, y0, pi0, si0, g0, u0);
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           } else {
             D2 v0, y0;
             tld2(tV + 4 * j, v0);
-            tld2((si0 >> 5) ? tY + 4 * ((si0 >> 5) - 1) : tS + 4 * j, y0);
+            tld2(((si0 >> 5) & 0x1F) ? tY + 4 * (((si0 >> 5) & 0x1F) - 1) : tS + 4 * j, y0);
             const int2 pi0 = lds_i2(pi_s + 8 * p0);
             twait_ld();
             down_one(j, v0, y0, pi0, si0, g0, u0);
@@ -470,10 +470,11 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       double2 yn[kMaxRW];
       auto load_row = [&](const int j, int* c, double2* y) {
         const int p = base + 32 * j;
+        const int rw = j < NS ? (si_w[j] >> 10) & 0xF : a.RW;  // the slot's widest row
 #pragma unroll
         for (int r = 0; r < kMaxRW; ++r) {
-          c[r] = r < a.RW ? __ldg(a.ell_col + r * P + p) : -1;
-          y[r] = r < a.RW ? __ldg(a.ell_val + r * P + p) : make_double2(0.0, 0.0);
+          c[r] = r < rw ? __ldg(a.ell_col + r * P + p) : -1;
+          y[r] = r < rw ? __ldg(a.ell_val + r * P + p) : make_double2(0.0, 0.0);
         }
       };
       load_row(0, cn, yn);

@@ -59,6 +59,7 @@ class SubtreeSchedule:
     P: int            # positions = W * NSL * 32
     NY: int           # TMEM y slots per thread (slots holding an internal node)
     slotinfo: np.ndarray  # int32 [W, NS]: kmax (4 bits) | pair-with-next (bit 4) | y slot + 1 (bits 5-9)
+    #                       | widest residual row (bits 10-13)
     pinfo: np.ndarray  # int32 [P, 2]
     kids: np.ndarray   # uint16 [nk] X indices of children
     coef: np.ndarray   # complex128 [3, P]: g, 1/U[m,m], src
@@ -187,7 +188,8 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
             if km > 0:  # some internal node: z / U_mm kept in TMEM (leaf-only slots recompute it)
                 yk += 1
                 ys = yk
-            slotinfo[w, k] = km | (ys << 5)
+            rwm = max(int(np.diff(rp)[orig[m]]) for m in nodes)  # widest residual row of the slot
+            slotinfo[w, k] = km | (ys << 5) | (rwm << 10)
         for k in range(len(sslots[w]) - 1):  # slots k, k+1 independent: swept as a pair
             if not any(slot_of.get(int(pm[m]), -1) == k + 1 for m in sslots[w][k]):
                 slotinfo[w, k] |= 1 << 4
