@@ -62,6 +62,9 @@ def parse():
     p.add_argument("--chunk-cases", type=int, default=0, help="e2e host-pipeline chunk (0 = library default)")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="time eager launches instead of a CUDA-graph replay of the step")
+    p.add_argument("--scenarios", type=int, default=1000, help="c4: scenario batches in the timed pass")
+    p.add_argument("--no-sparse", dest="sparse_half", action="store_false",
+                   help="default (c2) line without the nested C3 sparse object")
     return p.parse_args()
 
 
@@ -252,6 +255,8 @@ def run_ours():
     from paper_2403_04578_b200 import batch_solve_dense, batch_solve_sparse, SolveOptions
     from paper_2403_04578_b200._device import residual_and_summary
 
+    if ARGS.config == "c4":
+        return run_c4(dev, world, rank, local)
     n_buses = CONFIGS[ARGS.config][0]
     full_tau = ARGS.tau or CONFIGS[ARGS.config][2]
     scenarios = ARGS.config == "c4"
@@ -400,6 +405,12 @@ def run_ours():
     if not ARGS.no_e2e:
         e2e = run_e2e(model, loads, method, dev, batch_solve_dense, batch_solve_sparse, LoadMatrix, world,
                       dtype=edt, opts=opts)
+    sparse = None
+    if ARGS.config == "c2" and not c64 and ARGS.sparse_half and not ARGS.tau:
+        graph = None
+        del S_list, S, V, post
+        torch.cuda.empty_cache()
+        sparse = sparse_half(dev, world, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
@@ -419,11 +430,176 @@ def run_ours():
                                 parallelism=f"tau-sharded x{world} (independent scenario batches)",
                                 **({"c4_full_1000_scenarios_s_extrapolated": 1000 * tau / value} if scenarios else {})),
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
+                    **({"sparse": sparse} if sparse is not None else {}),
                     gpu_launches=launches_per_step(method, op, tau) * ARGS.steps,
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_c4(dev, world, rank, local):
+    """Config C4: the whole probabilistic-PF pass (probabilistic.probabilistic_pf) over
+    --scenarios scenario batches of 525,600 cases (1,000 by default), scenarios
+    dealt round-robin over ranks: per scenario the device generator, the dense
+    solve with residual post-check and summary, and the per-node |V| statistics,
+    all inside the timed region (CUDA events, max over ranks; strong scaling: the
+    total work is fixed).  One untimed warm-up pass of min(--warmup, 3) scenarios."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_04578_b200 import GenSpec, build_network
+    from paper_2403_04578_b200.probabilistic import probabilistic_pf
+    n_buses, _, tau, scale, _, desc = CONFIGS["c4"]
+    if ARGS.tau:
+        tau = ARGS.tau
+    model = build_network(GenSpec(n_buses=n_buses, seed=0, load_scale=scale))
+    n_scen = ARGS.scenarios
+    probabilistic_pf(model, max(1, min(ARGS.warmup, 3)) * world, tau, device=dev)
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        w0 = time.perf_counter()
+        t0.record(stream)
+        st = probabilistic_pf(model, n_scen, tau, device=dev)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - w0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    value = n_scen * tau / (ms * 1e-3)
+    if rank == 0:
+        line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=n_scen, warmup=max(1, min(ARGS.warmup, 3)),
+                    ms_per_step=ms / n_scen, higher_is_better=True, scaling="strong", vs_baseline=None,
+                    dtype="c128", data="synthetic",
+                    config=dict(workload=desc, b=model.n_demand, tau_per_scenario=tau, scenarios=n_scen,
+                                cases=n_scen * tau, method="dense",
+                                step="one scenario batch: device generation + solve + residual/summary + "
+                                     "per-node |V| statistics (nothing copied to the host)",
+                                parallelism=f"scenarios round-robin over {world} rank(s), statistics all-reduced",
+                                pass_s=ms * 1e-3, pass_wall_s=wall),
+                    result=dict(vmin_min=float(st.vmin.min()), vmean_mean=float(st.vmean.mean()),
+                                vmax_max=float(st.vmax.max()), nonconverged=st.nonconverged,
+                                max_iterations=st.max_iterations, sum_iterations=st.sum_iterations),
+                    gpu_launches=5 * n_scen, clocks=clk.summary())  # solve, residual, summary, 2 x stats
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sparse_half(dev, world, rank):
+    """The sparse half of the metric (BASELINE metric "dense+sparse TPF"): config C3
+    (b=5,000 radial feeder, tau=525,600 per rank, device-generated loads, rank r>0
+    seed 1000+r) through SparseOperator.solve (warp-per-subtree kernel, fused
+    residual, node-major input in case-major chunks), device-timed over the same
+    --steps after --warmup steps, max over ranks; e2e through
+    batch_solve_sparse(model, LoadMatrix) on a 65,536-case host sample; the CPU
+    port of the reference's SuperLU block path on a bounded sample (rank 0, N=1)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_04578_b200 import GenSpec, build_network, SparseOperator, SolveOptions, LoadMatrix
+    from paper_2403_04578_b200 import batch_solve_sparse, gen_scenarios
+    from paper_2403_04578_b200.synth import gen_scenarios_device
+    n_buses, _, tau, scale, _, desc = CONFIGS["c3"]
+    model = build_network(GenSpec(n_buses=n_buses, seed=0, load_scale=scale))
+    lspec = GenSpec(n_buses=n_buses, seed=0 if rank == 0 else 1000 + rank, load_scale=scale)
+    b = model.n_demand
+    S = gen_scenarios_device(model, tau, lspec, device=dev)
+    V = torch.empty_like(S)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    resid = torch.empty(tau, dtype=torch.float64, device=dev)
+    op = SparseOperator(model, dev)
+    opts = SolveOptions()
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(ARGS.warmup):
+        op.solve(S, opts, V=V, iters=iters, resid=resid)
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0.record(stream)
+    for _ in range(ARGS.steps):
+        op.solve(S, opts, V=V, iters=iters, resid=resid)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / ARGS.steps
+    sum_n = int(iters.sum().item())
+    conv = int((resid < opts.residual_tolerance).sum().item())
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    del S, V
+    torch.cuda.empty_cache()
+    peak = measured_hbm()
+    alg = 48.0 * b * sum_n
+    gbs = alg / (ms * 1e-3) / 1e9
+    out = dict(workload=desc, b=b, tau_per_gpu=tau, value=world * tau / (ms * 1e-3), unit=UNIT,
+               ms_per_step=ms, kernel=op.kernel, sum_iterations=sum_n, converged=conv,
+               launches_per_step=3 * -(-tau // 65536),
+               timing="device (CUDA events, eager launches; per step: per 65,536-case chunk a transpose in, "
+                      "the subtree kernel with the fused residual, a transpose out), max over ranks",
+               roofline=dict(bound="hbm", achieved=gbs, peak=peak, unit="GB/s", frac=gbs / peak,
+                             kernel=op.kernel, peak_source="MEASURED_PEAKS.json hbm_gbs",
+                             algorithmic=f"48*b*sum(n_j) = {alg:.4e} bytes per step (SURVEY 8(d))",
+                             traffic=traffic_from_profiles("sparse_subtree_kernel", tau),
+                             compulsory=dict(bytes=32.0 * b * tau, gbs=32.0 * b * tau / (ms * 1e-3) / 1e9,
+                                             what="S read once + V written once")))
+    if not ARGS.no_e2e:
+        n = 1 << 16
+        host = gen_scenarios(model, n, lspec)
+        pinned = LoadMatrix(torch.from_numpy(host.values).pin_memory().numpy())
+        for _ in range(2):
+            r = batch_solve_sparse(model, pinned, device=dev)
+        ts = []
+        for _ in range(max(1, min(ARGS.steps, 3))):
+            t_0 = time.perf_counter()
+            r = batch_solve_sparse(model, pinned, device=dev)
+            torch.cuda.synchronize(dev)
+            ts.append(time.perf_counter() - t_0)
+        te = float(np.mean(ts))
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        out["e2e"] = dict(value=world * n / te, unit=UNIT, ms_per_step=te * 1e3, cases_per_step=n,
+                          h2d_bytes_per_step=b * n * 16, d2h_bytes_per_step=b * n * 16 + n * 13,
+                          api="paper_2403_04578_b200.batch_solve_sparse(model, LoadMatrix) incl. the SuperLU "
+                              "factorization of Y_dd (one per call, as the reference)",
+                          iterations=int(r.iterations))
+        if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
+            out["cpu_baseline"] = sparse_cpu_sample(model, host, min(ARGS.cpu_seconds, 10.0))
+    return out
+
+
+def sparse_cpu_sample(model, loads, seconds):
+    """The oracle port of tpflow.batch_solve_sparse (block system + one SuperLU per
+    batch, sparse.py:167-207) on the first columns of the sample, single-threaded."""
+    from oracle import tpf_oracle as orc
+    y, src, v_s = model.admittance.y_dd, model.source_injection(), model.slack.v_s
+    S = loads.values
+
+    def run(cols):
+        sub = np.ascontiguousarray(S[:, :cols])
+        t_0 = time.perf_counter()
+        orc.sparse_block(y, src, v_s, sub)
+        return time.perf_counter() - t_0
+
+    dt = run(16)
+    cols = int(min(1200, max(16, 16 * seconds / max(dt, 1e-6) / 2)))
+    t = float(np.median([run(cols) for _ in range(2)]))
+    return dict(value=cols / t, unit=UNIT, cores=1, kind="port",
+                sample=f"first {cols} of {S.shape[1]} cases, oracle port of tpflow.batch_solve_sparse "
+                       "(block system + SuperLU, setup included), median of 2; the reference's SuperLU "
+                       "fails from tau ~1,800 (SURVEY 8(d))")
 
 
 def dense_kernel_name(b, tau):
@@ -444,6 +620,8 @@ def launches_per_step(method, op, tau):
         # cap (early-exit launches once every case froze), then residual + summary
         return 1 + 4 * 100 + 2 if op.b > 104 else 3
     from paper_2403_04578_b200.sparse import TREE_CHUNK
+    if op.sub is not None:  # per 65,536-case chunk: transpose in, subtree kernel, transpose out; + summary
+        return 3 * -(-tau // 65536) + 1
     if op.tree is not None:
         return (-(-tau // TREE_CHUNK) if tau > TREE_CHUNK else 1) + 1
     return 3

@@ -358,6 +358,30 @@ int tpf_write_pairs_csv(const char* path, const char* header, int32_t b, int64_t
  * tpf_host_unpin), 0 if it was already page-locked or cannot be.          */
 int tpf_host_pin(void* ptr, size_t bytes);
 int tpf_host_unpin(void* ptr);
+/* Per-node statistics of a solved batch (probabilistic PF, config C4):
+ * vmin/vmax/vsum[i] = min / max / sum over the tau cases of |V[i, j]|
+ * (accumulate != 0: folded into the arrays' current values, e.g. over
+ * scenario batches).  Deterministic (fixed reduction order, no atomics).
+ * workspace >= tpf_voltage_stats_workspace_bytes(tau, b).                 */
+size_t tpf_voltage_stats_workspace_bytes(int64_t tau, int32_t b);
+int tpf_voltage_stats_c128(int64_t tau, int32_t b, const double* V, int64_t v_node_stride, int64_t v_case_stride,
+                           double* vmin, double* vmax, double* vsum, int32_t accumulate, void* workspace,
+                           size_t workspace_bytes, void* stream);
+/* Host-buffer pipeline of the warp-per-subtree kernel (schedule arrays on the
+ * HOST, uploaded once per call; same chunked H2D / solve + fused residual /
+ * D2H streams as tpf_sparse_tree_solve_host_c128).                        */
+size_t tpf_sparse_subtree_solve_host_workspace_bytes(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rw,
+                                                     int32_t nkids, int64_t chunk_cases, int64_t ydd_nnz);
+int tpf_sparse_subtree_solve_host_c128(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rmax, int32_t rw,
+                                       int32_t nkids, const int32_t* pinfo, const int32_t* slotinfo,
+                                       const uint16_t* kids, const double* coef, const int32_t* ell_col,
+                                       const double* ell_val, const double* S, int64_t s_node_stride,
+                                       int64_t s_case_stride, const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                       const double* ydd_val, const double* src, double v_flat_re, double v_flat_im,
+                                       double tol, int32_t max_iter, double residual_tol, double* V,
+                                       int64_t v_node_stride, int64_t v_case_stride, int32_t* iters, double* resid,
+                                       uint8_t* mask, int32_t* summary, int64_t chunk_cases, int32_t device,
+                                       void* workspace, size_t workspace_bytes);
 size_t tpf_sparse_tree_solve_host_workspace_bytes(int64_t tau, int32_t b, int64_t chunk_cases, int64_t ydd_nnz);
 int tpf_sparse_tree_solve_host_c128(int64_t tau, int32_t b, int32_t levels,
                                     const int32_t* level_info, const int32_t* node_info, const double* node_coef,

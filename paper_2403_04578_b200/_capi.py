@@ -74,6 +74,12 @@ SIGNATURES = {
     "tpf_sparse_subtree_warps": (ctypes.c_int, []),
     "tpf_sparse_subtree_smem_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32]),
     "tpf_sparse_subtree_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "tpf_sparse_subtree_solve_host_workspace_bytes": (_c_sz, [_c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i64,
+                                                              _c_i64]),
+    "tpf_sparse_subtree_solve_host_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_dbl, _c_ptr,
+        _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i32, _c_ptr, _c_sz]),
     "tpf_sparse_subtree_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
@@ -117,6 +123,9 @@ SIGNATURES = {
                                           _c_i32]),
     "tpf_write_pairs_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _c_i32, _c_i64, _c_ptr, _c_ptr, _c_i64,
                                            _c_i64, _c_ptr, _c_i32]),
+    "tpf_voltage_stats_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "tpf_voltage_stats_c128": (ctypes.c_int, [_c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
+                                               _c_i32, _c_ptr, _c_sz, _c_ptr]),
     "tpf_host_pin": (ctypes.c_int, [_c_ptr, _c_sz]),
     "tpf_host_unpin": (ctypes.c_int, [_c_ptr]),
     "tpf_probe_fp64_tflops": (ctypes.c_int, [ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_dbl)]),

@@ -162,3 +162,98 @@ extern "C" int tpf_probe_fp64_tflops(double* tflops_out, double* ms_out) {
   if (ms_out) *ms_out = best;
   return TPF_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Per-node voltage statistics of a solved batch (probabilistic power flow,
+// config C4: the scenario batches are reduced on the device instead of being
+// copied out).  Pass 1: one CTA per (node, 65,536-case block) reduces
+// min / max / sum of |V| with a fixed thread-to-case mapping and a fixed
+// shuffle tree; pass 2: one thread per node folds the blocks in order into
+// the running arrays.  No atomics: the statistics are bit-reproducible.
+namespace tpf {
+namespace {
+constexpr int kStatBlock = 65536;
+
+__global__ void __launch_bounds__(256) vstats_partial_kernel(int64_t tau, const double2* __restrict__ V, int64_t vn,
+                                                             int64_t vc, double* __restrict__ part) {
+  const int i = blockIdx.x;
+  const int64_t lo = int64_t(blockIdx.y) * kStatBlock;
+  const int64_t hi = lo + kStatBlock < tau ? lo + kStatBlock : tau;
+  double mn = INFINITY, mx = -INFINITY, sm = 0.0;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+    const double2 v = V[int64_t(i) * vn + j * vc];
+    const double a = hypot(v.x, v.y);  // |V| as numpy's abs (hypot)
+    mn = fmin(mn, a);
+    mx = fmax(mx, a);
+    sm += a;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  __shared__ double s[3][8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s[0][w] = mn;
+    s[1][w] = mx;
+    s[2][w] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < 8; ++k) {
+      mn = fmin(mn, s[0][k]);
+      mx = fmax(mx, s[1][k]);
+      sm += s[2][k];
+    }
+    double* o = part + (int64_t(i) * gridDim.y + blockIdx.y) * 3;
+    o[0] = mn;
+    o[1] = mx;
+    o[2] = sm;
+  }
+}
+
+__global__ void vstats_fold_kernel(int b, int nblk, const double* __restrict__ part, double* vmin, double* vmax,
+                                   double* vsum, int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  double mn = accumulate ? vmin[i] : INFINITY, mx = accumulate ? vmax[i] : -INFINITY, sm = accumulate ? vsum[i] : 0.0;
+  for (int k = 0; k < nblk; ++k) {
+    const double* p = part + (int64_t(i) * nblk + k) * 3;
+    mn = fmin(mn, p[0]);
+    mx = fmax(mx, p[1]);
+    sm += p[2];
+  }
+  vmin[i] = mn;
+  vmax[i] = mx;
+  vsum[i] = sm;
+}
+}  // namespace
+}  // namespace tpf
+
+extern "C" size_t tpf_voltage_stats_workspace_bytes(int64_t tau, int32_t b) {
+  const int64_t nblk = (tau + kStatBlock - 1) / kStatBlock;
+  return size_t(b > 0 ? b : 0) * size_t(nblk > 0 ? nblk : 0) * 3 * sizeof(double) + 256;
+}
+
+extern "C" int tpf_voltage_stats_c128(int64_t tau, int32_t b, const double* V, int64_t v_node_stride,
+                                      int64_t v_case_stride, double* vmin, double* vmax, double* vsum,
+                                      int32_t accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+  if (tau < 1 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_voltage_stats_c128: need tau >= 1 and b >= 1");
+  if (!V || !vmin || !vmax || !vsum || !workspace)
+    return set_error(TPF_ERR_INVALID, "tpf_voltage_stats_c128: null pointer");
+  if (workspace_bytes < tpf_voltage_stats_workspace_bytes(tau, b))
+    return set_error(TPF_ERR_INVALID, "tpf_voltage_stats_c128: workspace too small");
+  const int64_t nblk = (tau + kStatBlock - 1) / kStatBlock;
+  if (nblk > 65535) return set_error(TPF_ERR_INVALID, "tpf_voltage_stats_c128: tau too large for one call");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(workspace);
+  vstats_partial_kernel<<<dim3(unsigned(b), unsigned(nblk)), 256, 0, st>>>(
+      tau, reinterpret_cast<const double2*>(V), v_node_stride, v_case_stride, part);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(vstats_partial_kernel)", err);
+  vstats_fold_kernel<<<(b + 127) / 128, 128, 0, st>>>(b, int(nblk), part, vmin, vmax, vsum, accumulate);
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(vstats_fold_kernel)", err);
+  return TPF_OK;
+}

@@ -496,10 +496,105 @@ struct TreeChunk : ChunkSolver {
   }
 };
 
+// warp-per-subtree kernel (tpf_sparse_subtree_fpi_c128) with the fused residual
+struct SubtreeChunk : ChunkSolver {
+  int b, ns, nt, rmax, rw, nkids;
+  const int32_t *pinfo, *slotinfo;
+  const uint16_t* kids;
+  const double *coef, *ell_val;
+  const int32_t* ell_col;
+  double vre, vim, tol;
+  int max_iter;
+  void* ws;
+  size_t ws_bytes;
+  int solve(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+            cudaStream_t st) override {
+    return tpf_sparse_subtree_fpi_c128(n, b, ns, nt, rmax, rw, nkids, pinfo, slotinfo, kids, coef, ell_col, ell_val,
+                                       S, sn, sc, vre, vim, tol, max_iter, V, vn, vc, it, nullptr, ws, ws_bytes, st);
+  }
+  int solve_resid(int64_t n, const double* S, int64_t sn, int64_t sc, double* V, int64_t vn, int64_t vc, int32_t* it,
+                  const int32_t*, const int32_t*, const double*, const double*, double* resid,
+                  cudaStream_t st) override {
+    return tpf_sparse_subtree_fpi_c128(n, b, ns, nt, rmax, rw, nkids, pinfo, slotinfo, kids, coef, ell_col, ell_val,
+                                       S, sn, sc, vre, vim, tol, max_iter, V, vn, vc, it, resid, ws, ws_bytes, st);
+  }
+};
+
 }  // namespace
 }  // namespace tpf
 
 using namespace tpf;
+
+extern "C" size_t tpf_sparse_subtree_solve_host_workspace_bytes(int64_t tau, int32_t b, int32_t ns, int32_t nt,
+                                                                int32_t rw, int32_t nkids, int64_t chunk_cases,
+                                                                int64_t ydd_nnz) {
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
+  const int64_t P = int64_t(tpf_sparse_subtree_warps()) * (ns + nt) * 32;
+  const size_t model = size_t(P) * (8 + 48 + size_t(rw) * 20) + size_t(12) * ns * 4 + size_t(nkids) * 2 +
+                       size_t(ydd_nnz) * 24 + size_t(b) * 32 + 64 * 1024;
+  return pipeline_bytes(tau, b, chunk, model, tpf_sparse_subtree_workspace_bytes(chunk, b));
+}
+
+extern "C" int tpf_sparse_subtree_solve_host_c128(int64_t tau, int32_t b, int32_t ns, int32_t nt, int32_t rmax,
+                                                  int32_t rw, int32_t nkids, const int32_t* pinfo,
+                                                  const int32_t* slotinfo, const uint16_t* kids, const double* coef,
+                                                  const int32_t* ell_col, const double* ell_val, const double* S,
+                                                  int64_t s_node_stride, int64_t s_case_stride,
+                                                  const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                                  const double* ydd_val, const double* src, double v_flat_re,
+                                                  double v_flat_im, double tol, int32_t max_iter, double residual_tol,
+                                                  double* V, int64_t v_node_stride, int64_t v_case_stride,
+                                                  int32_t* iters, double* resid, uint8_t* mask, int32_t* summary,
+                                                  int64_t chunk_cases, int32_t device, void* workspace,
+                                                  size_t workspace_bytes) {
+  if (tau < 0 || b < 1 || ns < 1 || nt < 1)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_solve_host_c128: bad shape");
+  if (!S || !pinfo || !slotinfo || !kids || !coef || !ell_col || !ell_val || !ydd_row_ptr || !src || !V)
+    return set_error(TPF_ERR_INVALID, "null pointer");
+  TPF_CK(cudaSetDevice(device), "cudaSetDevice");
+  if (summary) summary[0] = summary[1] = 0;
+  if (tau == 0) return TPF_OK;
+  if (workspace && workspace_bytes < tpf_sparse_subtree_solve_host_workspace_bytes(tau, b, ns, nt, rw, nkids,
+                                                                                  chunk_cases, ydd_row_ptr[b]))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_solve_host_c128: workspace too small");
+  ArenaScope arena(workspace, workspace_bytes);
+  Streams* ssp = cached_streams(device);
+  if (!ssp) return set_cuda_error("cudaStreamCreate", cudaGetLastError());
+  const Streams& ss = *ssp;
+  const int64_t chunk = pick_chunk(tau, b, chunk_cases);
+  cudaStream_t st = ss.s[1];
+  const int64_t P = int64_t(tpf_sparse_subtree_warps()) * (ns + nt) * 32;
+  DevBuf dpi, dsi, dk, dc, dec, dev_, dws;
+  TPF_CK(upload(dpi, pinfo, size_t(P) * 2, st), "upload(pinfo)");
+  TPF_CK(upload(dsi, slotinfo, size_t(tpf_sparse_subtree_warps()) * ns, st), "upload(slotinfo)");
+  TPF_CK(upload(dk, kids, size_t(nkids), st), "upload(kids)");
+  TPF_CK(upload(dc, coef, size_t(P) * 6, st), "upload(coef)");
+  TPF_CK(upload(dec, ell_col, size_t(rw) * P, st), "upload(ell_col)");
+  TPF_CK(upload(dev_, ell_val, size_t(rw) * P * 2, st), "upload(ell_val)");
+  const size_t wsb = tpf_sparse_subtree_workspace_bytes(chunk, b);
+  TPF_CK(dws.alloc(wsb), "cudaMalloc(workspace)");
+  SubtreeChunk sv;
+  sv.b = b;
+  sv.ns = ns;
+  sv.nt = nt;
+  sv.rmax = rmax;
+  sv.rw = rw;
+  sv.nkids = nkids;
+  sv.pinfo = dpi.as<int32_t>();
+  sv.slotinfo = dsi.as<int32_t>();
+  sv.kids = static_cast<const uint16_t*>(dk.p);
+  sv.coef = dc.as<double>();
+  sv.ell_col = dec.as<int32_t>();
+  sv.ell_val = dev_.as<double>();
+  sv.vre = v_flat_re;
+  sv.vim = v_flat_im;
+  sv.tol = tol;
+  sv.max_iter = max_iter;
+  sv.ws = dws.p;
+  sv.ws_bytes = wsb;
+  return run_pipeline(sv, tau, b, S, s_node_stride, s_case_stride, ydd_row_ptr, ydd_col, ydd_val, src, residual_tol,
+                      V, v_node_stride, v_case_stride, iters, resid, mask, summary, chunk, ss, st);
+}
 
 extern "C" int tpf_host_pin(void* ptr, size_t bytes) {
   if (!ptr || bytes == 0) return 0;

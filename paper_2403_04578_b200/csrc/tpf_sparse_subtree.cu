@@ -44,14 +44,14 @@ namespace {
 
 constexpr int kSubWarps = 12;
 constexpr int kSubThreads = 32 * kSubWarps;
-constexpr int kParentNone = -32768;
 constexpr int kMaxRW = 8;   // residual row width (diagonal + parent + children)
 constexpr int kSubKmax = 8;  // children per node (paper_2403_04578_b200/subtree.py SUB_KMAX)
 
 struct SubArgs {
   int64_t tau;
   int b, NS, NT, NSL, RMAX, RW, P, xcap, nkids;
-  int mode;      // 0: node-major S / V (2-D TMA), 1: case-major (1-D bulk)
+  int mode;      // S: 0 node-major (2-D TMA), 1 case-major (1-D bulk)
+  int vmode;     // V: the same choices
   int nbox, boxrows;
   const double2* S;
   int64_t s_case;  // mode 1: case stride (complex elements)
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
-      if (a.mode == 0) {
+      if (a.vmode == 0) {
         for (int k = 0; k < a.nbox; ++k) tma_store_2d(&tmV, 2 * cs, k * a.boxrows, X + k * a.boxrows);
       } else {
         bulk_store(a.V + int64_t(cs) * a.v_case, X, uint32_t(a.b) * 16u);
@@ -651,15 +651,12 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, i
     return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_fpi_c128: null pointer or small workspace");
   if (ns < 1 || nt < 1 || 8 * ns > 168 || rmax < 1 || rw < 1 || rw > kMaxRW || nkids < 1)
     return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_fpi_c128: bad schedule");
-  int mode;
-  if (s_case_stride == 1 && v_case_stride == 1 && s_node_stride >= tau && v_node_stride >= tau)
-    mode = 0;  // node-major (the reference layout)
-  else if (s_node_stride == 1 && v_node_stride == 1 && s_case_stride >= b && v_case_stride >= b)
-    mode = 1;  // case-major (F-order)
-  else
+  // S and V each node-major (case stride 1: the reference layout) or case-major (node stride 1)
+  const bool s_nm = s_case_stride == 1 && s_node_stride >= tau, s_cm = s_node_stride == 1 && s_case_stride >= b;
+  const bool v_nm = v_case_stride == 1 && v_node_stride >= tau, v_cm = v_node_stride == 1 && v_case_stride >= b;
+  if (!(s_nm || s_cm) || !(v_nm || v_cm))
     return set_error(TPF_ERR_UNSUPPORTED, "tpf_sparse_subtree_fpi_c128: S / V must be node- or case-major");
-  if ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(V)) & 15)
-    return set_error(TPF_ERR_INVALID, "tpf_sparse_subtree_fpi_c128: S and V must be 16-byte aligned");
+  const int mode = s_cm ? 1 : 0, vmode = v_cm ? 1 : 0;
   SubArgs a;
   memset(&a, 0, sizeof a);
   a.tau = tau;
@@ -675,6 +672,7 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, i
   a.xcap = a.P > a.nbox * a.boxrows ? a.P : a.nbox * a.boxrows;
   a.nkids = nkids;
   a.mode = mode;
+  a.vmode = vmode;
   a.S = reinterpret_cast<const double2*>(S);
   a.s_case = s_case_stride;
   a.V = reinterpret_cast<double2*>(V);
@@ -697,9 +695,11 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, i
   memset(&ms, 0, sizeof ms);
   memset(&mv, 0, sizeof mv);
   if (mode == 0) {
-    int rc = column_map(&ms, S, tau, b, s_node_stride, a.boxrows);
+    const int rc = column_map(&ms, S, tau, b, s_node_stride, a.boxrows);
     if (rc != TPF_OK) return rc;
-    rc = column_map(&mv, V, tau, b, v_node_stride, a.boxrows);
+  }
+  if (vmode == 0) {
+    const int rc = column_map(&mv, V, tau, b, v_node_stride, a.boxrows);
     if (rc != TPF_OK) return rc;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -712,28 +712,39 @@ extern "C" int tpf_sparse_subtree_fpi_c128(int64_t tau, int32_t b, int32_t ns, i
   // 2 MB page each at C3) and transposed back.
   const int64_t chunk = tau < kSubChunk ? tau : kSubChunk;
   const size_t need = size_t(2) * size_t(chunk) * size_t(b) * 16;
-  if (mode == 0 && workspace_bytes >= 256 + need) {
+  if ((mode == 0 || vmode == 0) && workspace_bytes >= 256 + need) {
     double2* Sc = reinterpret_cast<double2*>(static_cast<char*>(workspace) + 256);
     double2* Vc = Sc + size_t(chunk) * size_t(b);
     SubArgs c = a;
     c.mode = 1;
-    c.S = Sc;
-    c.V = Vc;
-    c.s_case = b;
-    c.v_case = b;
+    c.vmode = 1;
     for (int64_t lo = 0; lo < tau; lo += chunk) {
       const int64_t n = tau - lo < chunk ? tau - lo : chunk;
-      int rc = transpose_c128(reinterpret_cast<const double2*>(S) + lo, s_node_stride, Sc, b, b, n, st);
-      if (rc != TPF_OK) return rc;
+      if (mode == 0) {
+        const int rc = transpose_c128(reinterpret_cast<const double2*>(S) + lo, s_node_stride, Sc, b, b, n, st);
+        if (rc != TPF_OK) return rc;
+        c.S = Sc;
+        c.s_case = b;
+      } else {
+        c.S = reinterpret_cast<const double2*>(S) + lo * s_case_stride;
+      }
+      if (vmode == 0) {
+        c.V = Vc;
+        c.v_case = b;
+      } else {
+        c.V = reinterpret_cast<double2*>(V) + lo * v_case_stride;
+      }
       cudaError_t err = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
       if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(counter)", err);
       c.tau = n;
       c.iters = iters + lo;
       c.resid = resid ? resid + lo : nullptr;
-      rc = sub_launch(c, ms, mv, smem, int(n < sms ? n : sms), st);
+      int rc = sub_launch(c, ms, mv, smem, int(n < sms ? n : sms), st);
       if (rc != TPF_OK) return rc;
-      rc = transpose_c128(Vc, b, reinterpret_cast<double2*>(V) + lo, v_node_stride, n, b, st);
-      if (rc != TPF_OK) return rc;
+      if (vmode == 0) {
+        rc = transpose_c128(Vc, b, reinterpret_cast<double2*>(V) + lo, v_node_stride, n, b, st);
+        if (rc != TPF_OK) return rc;
+      }
     }
     return TPF_OK;
   }

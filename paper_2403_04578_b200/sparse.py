@@ -302,15 +302,15 @@ SUBTREE_MIN_B = 0       # radial feeders from this size run the warp-per-subtree
 
 
 def _subtree_layout_ok(S: torch.Tensor, V: torch.Tensor) -> bool:
-    """The subtree kernel moves whole case columns by TMA: node-major (case
-    stride 1) or case-major (node stride 1) S and V, 16-byte aligned."""
+    """The subtree kernel moves whole case columns by TMA: S and V each
+    node-major (case stride 1) or case-major (node stride 1), 16-byte aligned."""
     b, tau = S.shape
     sn, sc = S.stride()
     vn, vc = V.stride()
     aligned = S.data_ptr() % 16 == 0 and V.data_ptr() % 16 == 0
-    node_major = sc == 1 and vc == 1 and sn >= tau and vn >= tau
-    case_major = sn == 1 and vn == 1 and sc >= b and vc >= b
-    return aligned and (node_major or case_major) and tau < (1 << 30)
+    s_ok = (sc == 1 and sn >= tau) or (sn == 1 and sc >= b)
+    v_ok = (vc == 1 and vn >= tau) or (vn == 1 and vc >= b)
+    return aligned and s_ok and v_ok and tau < (1 << 30)
 
 
 @dataclass
@@ -569,7 +569,8 @@ class SparseOperator:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
         if self.sub is not None and _subtree_layout_ok(S, V):
             # node-major batches are solved in case-major chunks (scratch in the workspace)
-            need = int(_capi.load().tpf_sparse_subtree_workspace_bytes(tau, b)) if S.stride(1) == 1 else 256
+            need = (int(_capi.load().tpf_sparse_subtree_workspace_bytes(tau, b))
+                    if S.stride(1) == 1 or V.stride(1) == 1 else 256)
             if self._ws is None or self._ws.numel() < need:
                 self._ws = None
                 self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
@@ -704,14 +705,19 @@ def _batch_lu(contract, use_tree: bool):
     memoised: the host setup (C3: ~30 ms) is part of every call, as it is of
     the reference's."""
     f = factorize_ydd(contract.y_dd)
-    tree = tree_schedule(f, contract.src) if use_tree else None
-    return f, tree
+    levels = tree_levels(f, contract.src) if use_tree else None
+    sub = None
+    if levels is not None and contract.b >= SUBTREE_MIN_B:
+        from .subtree import subtree_schedule
+        sub = subtree_schedule(levels, *host_csr(contract))
+    tree = tree_schedule(f, contract.src) if levels is not None and sub is None else None
+    return f, tree, sub
 
 
 def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chunk_cases: int,
                          use_tree: bool = True):
     c = ModelContract.of(model)
-    f, tree = _batch_lu(c, use_tree)  # one factorization per batch, shared by every device
+    f, tree, sub = _batch_lu(c, use_tree)  # one factorization per batch, shared by every device
     rp, ci, yv = host_csr(c)
     S, sn, sc = host_loads(loads.values)
     b, tau = S.shape
@@ -732,6 +738,16 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chu
         outs = (ptr(V) + 16 * lo, tau, 1, ptr(iters) + 4 * lo, ptr(resid) + 8 * lo, ptr(mask) + lo, ptr(summ),
                 int(chunk_cases), dev.index)
         s_lo = ptr(S) + 16 * lo * sc
+        if sub is not None:
+            ws = device_workspace_slot(dev, lib.tpf_sparse_subtree_solve_host_workspace_bytes(
+                n, b, sub.NS, sub.NT, sub.RW, int(sub.kids.size), int(chunk_cases), yv.size), slot)
+            torch.cuda.current_stream(dev).synchronize()
+            _capi.call("tpf_sparse_subtree_solve_host_c128", n, b, sub.NS, sub.NT, sub.RMAX, sub.RW,
+                       int(sub.kids.size), ptr(sub.pinfo), ptr(sub.slotinfo), ptr(sub.kids), ptr(sub.coef),
+                       ptr(sub.ell_col), ptr(sub.ell_val), s_lo, sn, sc, ptr(rp), ptr(ci), ptr(yv), ptr(c.src),
+                       v_flat.real, v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
+                       float(opts.residual_tolerance), *outs, ws.data_ptr(), ws.numel())
+            return summ
         if tree is not None:
             ws = device_workspace_slot(
                 dev, lib.tpf_sparse_tree_solve_host_workspace_bytes(n, b, int(chunk_cases), yv.size), slot)

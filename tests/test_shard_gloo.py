@@ -83,3 +83,47 @@ def test_two_rank_gloo_matches_unsharded():
     assert np.array_equal(mask, ref.converged_mask)
     assert np.abs(vals - ref.values).max() < 1e-14
     assert local_shape == (34, 151)
+
+
+def _stats_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2403_04578_b200.probabilistic import combine_ranks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(rank)
+        vmin = torch.from_numpy(rng.uniform(0.9, 1.0, 7))
+        vmax = torch.from_numpy(rng.uniform(1.0, 1.1, 7))
+        vsum = torch.from_numpy(rng.uniform(0.0, 5.0, 7))
+        counts = torch.tensor([rank, 10 * (rank + 1), 5 + 2 * rank], dtype=torch.int64)
+        combine_ranks(vmin, vmax, vsum, counts)
+        if rank == 0:
+            q.put((vmin.numpy(), vmax.numpy(), vsum.numpy(), counts.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_scenario_statistics_combine():
+    """C4 scenario statistics over ranks (probabilistic.combine_ranks): per-node
+    MIN / MAX / SUM of |V|, summed counts, MAX of the batch iteration count."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_stats_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    vmin, vmax, vsum, counts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r = [np.random.default_rng(k) for k in range(2)]
+    parts = [(g.uniform(0.9, 1.0, 7), g.uniform(1.0, 1.1, 7), g.uniform(0.0, 5.0, 7)) for g in r]
+    assert np.array_equal(vmin, np.minimum(parts[0][0], parts[1][0]))
+    assert np.array_equal(vmax, np.maximum(parts[0][1], parts[1][1]))
+    assert np.allclose(vsum, parts[0][2] + parts[1][2], rtol=0, atol=1e-15)
+    assert counts.tolist() == [1, 30, 7]

@@ -205,3 +205,86 @@ def test_feeder_beyond_tree_kernel_limits_uses_general_kernel():
     loads = gen_scenarios(model, 64, spec)
     out = batch_solve_sparse(model, loads)
     assert out.converged_mask.all() and 3 <= out.iterations <= 10
+
+
+@pytest.mark.parametrize("name", ["acc3_b100_t100", "nine_t500", "acc7_mixed_zero", "c3_slice6", "nine_zero_batch",
+                                  "twobus_infeasible"])
+@pytest.mark.parametrize("layout", ["node", "case"])
+def test_subtree_and_level_kernels_bitwise(golden, name, layout):
+    """Warp-per-subtree kernel (default for radial feeders) == level kernel: same
+    V, counts and fused residual bits, node-major (chunked transposes) and
+    case-major (1-D bulk copies) layouts."""
+    import torch
+    from paper_2403_04578_b200 import SparseOperator
+    g = golden(name)
+    sub = SparseOperator(g.model, kernel="subtree")
+    lvl = SparseOperator(g.model, kernel="tree")
+    if sub.sub is None or lvl.tree is None:
+        pytest.skip("not a radial feeder the tree kernels take")
+    S = torch.from_numpy(g.S).cuda()
+    if layout == "case":
+        S = S.t().contiguous().t()
+    out = []
+    for op in (sub, lvl):
+        r = torch.empty(S.shape[1], dtype=torch.float64, device="cuda")
+        V, it = op.solve(S, g.opts(), V=torch.empty_like(S), resid=r)
+        out.append((V, it, r))
+    assert sub.kernel == "sparse_subtree_kernel"
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    assert torch.equal(torch.isnan(out[0][2]), torch.isnan(out[1][2]))
+    keep = ~torch.isnan(out[0][2])
+    assert torch.equal(out[0][2][keep], out[1][2][keep])
+
+
+@pytest.mark.parametrize("n_buses,seed", [(35, 4), (301, 5), (1001, 6), (5001, 0)])
+def test_subtree_kernel_random_feeders(n_buses, seed):
+    """Subtree kernel vs level kernel on generated feeders of several shapes (bitwise)."""
+    import torch
+    from paper_2403_04578_b200 import GenSpec, build_network, SparseOperator, SolveOptions
+    from paper_2403_04578_b200.synth import gen_scenarios_device
+    spec = GenSpec(n_buses=n_buses, seed=seed)
+    model = build_network(spec)
+    S = gen_scenarios_device(model, 3000, spec, device="cuda:0")
+    res = []
+    for k in ("subtree", "tree"):
+        op = SparseOperator(model, kernel=k)
+        r = torch.empty(3000, dtype=torch.float64, device="cuda")
+        V, it = op.solve(S, SolveOptions(), resid=r)
+        res.append((V, it, r, op.kernel))
+    assert res[0][3] == "sparse_subtree_kernel"
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert torch.equal(res[0][2], res[1][2])
+
+
+def test_sparse_full_c3_sampled_vs_oracle():
+    """Full config C3 (b=5,000, tau=525,600, device-generated loads) through the
+    default sparse path (subtree kernel, case-major chunks): every case
+    converges, and 300 sampled columns match the oracle's single-case solver
+    (fpi.py:107-206: SuperLU of Y_dd) to 1e-12 with the same counts."""
+    import torch
+    from paper_2403_04578_b200 import GenSpec, build_network, SparseOperator
+    from paper_2403_04578_b200.synth import gen_scenarios_device
+    spec = GenSpec(n_buses=5001, seed=0)
+    model = build_network(spec)
+    tau = 525600
+    S = gen_scenarios_device(model, tau, spec, device="cuda:0")
+    op = SparseOperator(model)
+    assert op.kernel == "sparse_subtree_kernel"
+    resid = torch.empty(tau, dtype=torch.float64, device="cuda")
+    V, it = op.solve(S, resid=resid)
+    it_h = it.cpu().numpy()
+    assert it_h.max() < 100 and bool((resid < 1e-8).all())
+    cols = np.random.default_rng(0).choice(tau, 300, replace=False)
+    idx = torch.from_numpy(cols).cuda()
+    Sh = S[:, idx].cpu().numpy()
+    Vg = V[:, idx].cpu().numpy()
+    del S, V
+    y, src, v_s = model.admittance.y_dd, model.source_injection(), model.slack.v_s
+    exact = 0
+    for k, j in enumerate(cols):
+        v, n, conv = orc.fpi_single(y, src, v_s, Sh[:, k])
+        assert conv
+        assert abs(n - int(it_h[j])) <= 1
+        exact += n == int(it_h[j])
+        assert np.abs(Vg[:, k] - v).max() < 1e-12
+    assert exact >= 297
