@@ -310,6 +310,30 @@ def run_ours():
         return residual_and_summary(op.contract, Sk, V, itk, opts.residual_tolerance, dev, csr=csr, out=post,
                                     have_resid=fused)
 
+    if world > 1:
+        # N > 1: every step goes through the product's tau-sharding (shard.solve_sharded,
+        # local=True: each rank's resident slice; the batch iteration count and slice
+        # sizes all-gathered over NCCL, no data-path collective)
+        from paper_2403_04578_b200.shard import solve_sharded
+        from paper_2403_04578_b200.dense import finish
+        one_step = step
+
+        def sharded_fn(_model, Sk, _opts):
+            resid_k, mask_k, summ_k = one_step(None, S_list.index(Sk) if len(S_list) > 1 else 0)
+            itk = iters_list[S_list.index(Sk) if len(S_list) > 1 else 0]
+            return finish(V, itk, resid_k, mask_k, summ_k, True)
+
+        def step(ev=None, k=0):  # noqa: F811 -- the sharded step
+            Sk = S_list[k % len(S_list)]
+            if ev:
+                ev[0].record(stream)
+            res = solve_sharded(model, Sk, opts, solve_fn=sharded_fn, local=True, gather=False,
+                                return_on_device=True)
+            if ev:
+                ev[1].record(stream)
+            return (res.residuals, res.converged_mask,
+                    torch.stack([torch.tensor(res.iterations, device=dev), res.converged_mask.sum()]))
+
     for _ in range(ARGS.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -323,7 +347,7 @@ def run_ours():
     # summary: the same kernels on the same buffers, no per-launch host cost);
     # several scenario batches (C4) or --no-graph: eager launches
     graph = None
-    if ARGS.graph and len(S_list) == 1:
+    if ARGS.graph and len(S_list) == 1 and world == 1:
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
@@ -401,6 +425,23 @@ def run_ours():
                                         frac=32.0 * b * tau / (kms * 1e-3) / 1e9 / peak,
                                         what="S read once + V written once"))
 
+    shard_gather = None
+    if world > 1:
+        # the optional final gather of the sharded path: all_gather of every
+        # rank's device-resident V / counts / residuals / mask over NCCL, checked on this slice
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        g0 = time.perf_counter()
+        full = solve_sharded(model, S_list[0], opts, solve_fn=sharded_fn, local=True, gather=True,
+                             return_on_device=True)
+        torch.cuda.synchronize(dev)
+        g_s = time.perf_counter() - g0
+        mine_ok = bool(torch.equal(full.values[:, rank * tau:(rank + 1) * tau], V))
+        shard_gather = dict(api="paper_2403_04578_b200.shard.solve_sharded(..., local=True, gather=True, "
+                                "return_on_device=True)", backend=dist.get_backend(), wall_ms=g_s * 1e3,
+                            gathered_cases=int(full.values.shape[1]), own_slice_bitwise=mine_ok,
+                            gathered_bytes=int(full.values.numel() * 16))
+        del full
     e2e = None
     if not ARGS.no_e2e:
         e2e = run_e2e(model, loads, method, dev, batch_solve_dense, batch_solve_sparse, LoadMatrix, world,
@@ -431,6 +472,7 @@ def run_ours():
                                 **({"c4_full_1000_scenarios_s_extrapolated": 1000 * tau / value} if scenarios else {})),
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
                     **({"sparse": sparse} if sparse is not None else {}),
+                    **({"shard_gather": shard_gather} if shard_gather is not None else {}),
                     gpu_launches=launches_per_step(method, op, tau) * ARGS.steps,
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)

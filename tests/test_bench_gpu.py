@@ -44,6 +44,21 @@ def test_bench_two_ranks_plumbing():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    # the N > 1 steps go through shard.solve_sharded; its final gather reassembles both slices
+    g = d["shard_gather"]
+    assert g["gathered_cases"] == 2 * d["config"]["tau_per_gpu"] and g["own_slice_bitwise"]
+    assert d["config"]["converged"] == 2 * d["config"]["tau_per_gpu"]
+
+
+def test_bench_c4_pass_line():
+    """Config C4: the probabilistic-PF pass (generation + solve + statistics) over every scenario."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "c4", "--scenarios", "4", "--tau", "65536",
+                        "--warmup", "3", "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert d["steps"] == 4 and d["config"]["cases"] == 4 * 65536 and d["scaling"] == "strong"
+    assert d["result"]["nonconverged"] == 0 and 0.9 < d["result"]["vmin_min"] < d["result"]["vmax_max"] <= 1.0
 
 
 def test_bench_c64_line():

@@ -52,9 +52,14 @@ def _worker(rank, world, port, q):
         loads = gen_scenarios(model, 301, spec)
         out = solve_sharded(model, loads, SolveOptions(), solve_fn=_oracle_solver)
         local = solve_sharded(model, loads, SolveOptions(), solve_fn=_oracle_solver, gather=False)
+        # each rank hands over only its own (uneven) slice: slices concatenate in rank order
+        cut = 170
+        mine = loads.values[:, :cut] if rank == 0 else loads.values[:, cut:]
+        own = solve_sharded(model, mine, SolveOptions(), solve_fn=_oracle_solver, local=True,
+                            return_on_device=True)
         if rank == 0:
             q.put((out.values, out.iterations, out.iterations_per_case, out.converged_mask, out.residuals,
-                   local.values.shape, local.iterations))
+                   local.values.shape, local.iterations, own.values.numpy(), own.iterations))
     finally:
         dist.destroy_process_group()
 
@@ -70,7 +75,7 @@ def test_two_rank_gloo_matches_unsharded():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    vals, iters, per_case, mask, res, local_shape, local_it = q.get(timeout=240)
+    vals, iters, per_case, mask, res, local_shape, local_it, own_vals, own_it = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -83,6 +88,7 @@ def test_two_rank_gloo_matches_unsharded():
     assert np.array_equal(mask, ref.converged_mask)
     assert np.abs(vals - ref.values).max() < 1e-14
     assert local_shape == (34, 151)
+    assert np.abs(own_vals - vals).max() < 1e-14 and own_it == iters  # oracle BLAS blocking: not bitwise
 
 
 def _stats_worker(rank, world, port, q):

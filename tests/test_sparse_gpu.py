@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 from conftest import gpu_available
+from oracle import tpf_oracle as orc
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
