@@ -43,6 +43,19 @@ namespace tpf {
 namespace {
 
 constexpr int kSubWarps = 12;
+
+#ifdef TPF_PHASE_TIMING
+// debug build only (tools/build_timing.sh): thread 0 of every CTA accumulates
+// cycles per phase: {load, subtree up, barrier wait, top, subtree down,
+// retire + store, residual, end barrier + claim, cases, iterations, total}
+__device__ long long g_sub_cyc[148 * 12];
+#define SUB_T(v) const long long v = clock64()
+#define SUB_ACC(i, t0) \
+  if (tid == 0) tc[i] += clock64() - (t0)
+#else
+#define SUB_T(v)
+#define SUB_ACC(i, t0)
+#endif
 constexpr int kSubThreads = 32 * kSubWarps;
 constexpr int kMaxRW = 8;   // residual row width (diagonal + parent + children)
 constexpr int kSubKmax = 8;  // children per node (paper_2403_04578_b200/subtree.py SUB_KMAX)
@@ -178,7 +191,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   double2* TV = X + xcap + 2 * RR + 1;                 // top copies: iterate, load, z / U_mm
   double2* TS = TV + NTOP;
   double2* TY = TS + NTOP;
-  int2* PI = reinterpret_cast<int2*>(TY + NTOP);       // [P]
+  double2* TC = TY + NTOP;                             // top coefficients, shared: g, 1/U, src [3][NT * 32]
+  int2* PI = reinterpret_cast<int2*>(TC + 3 * NT * 32);  // [P]
   int32_t* SI = reinterpret_cast<int32_t*>(PI + P);   // [W][NS]
   uint16_t* KD = reinterpret_cast<uint16_t*>(SI + kSubWarps * NS);  // [nkids]
   __shared__ __align__(8) uint64_t s_bar;
@@ -191,6 +205,12 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   for (int i = tid; i < kSubWarps * NS; i += kSubThreads) SI[i] = __ldg(a.slotinfo + i);
   for (int i = tid; i < a.nkids; i += kSubThreads) KD[i] = __ldg(a.kids + i);
   if (tid == 0) X[xcap + 2 * RR] = make_double2(0.0, 0.0);
+  for (int i = tid; i < NT * 32; i += kSubThreads) {  // warp 0's top copy: the same for every warp
+    const int p = NS * 32 + i;
+    TC[i] = __ldg(a.coef + p);
+    TC[NT * 32 + i] = __ldg(a.coef + P + p);
+    TC[2 * NT * 32 + i] = __ldg(a.coef + 2 * P + p);
+  }
   if (warp == 0) tmem_alloc(&s_tmem, 512);
   if (tid == 0) {
     mbar_init(&s_bar, 1);
@@ -209,7 +229,6 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   const int32_t* si_w = SI + warp * NS;
   const double2* cg = a.coef;
   const double2* cu = a.coef + P;
-  const double2* csrc = a.coef + 2 * P;
   const uint32_t in_bytes =
       a.mode == 0 ? uint32_t(a.nbox) * uint32_t(a.boxrows) * 16u : uint32_t(a.b) * 16u;
   const uint32_t xs = smem_u32(X), pi_s = smem_u32(PI), kd_s = smem_u32(KD);
@@ -225,8 +244,13 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   }
   __syncthreads();
   uint32_t phase = 0;
+#ifdef TPF_PHASE_TIMING
+  long long tc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_begin = clock64();
+#endif
 
   for (;;) {
+    SUB_T(t_load);
     const int cs = s_case, nx = s_next;
     if (cs < 0) break;
     // ---- S of case cs into X (original node order); L2 prefetch of case nx ----
@@ -255,10 +279,15 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     }
     twait_st();
     __syncthreads();  // X is free for the sweeps
+    SUB_ACC(0, t_load);
+#ifdef TPF_PHASE_TIMING
+    if (tid == 0) tc[8] += 1;
+#endif
 
     int it = 0;
     bool small = false;
     for (;;) {
+      SUB_T(t_up);
       const int shift = (it & 1) ? RR : 0;  // Proot parity
       // ---- subtree up-sweep: z_m = r_m - sum_c X[c], X[m] = g_m z_m, y_m = z_m / U_mm ----
       {
@@ -327,28 +356,33 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           up_step(j, gb0, ub0, gb1, ub1, ga0, ua0, ga1, ua1);
         }
       }
+      SUB_ACC(1, t_up);
+      SUB_T(t_bar);
       // the previous iteration's step test, AND over the CTA (false at it = 0); the
       // subtree roots' products are visible after this barrier
-      if (__syncthreads_and(small)) break;
+      const int conv = __syncthreads_and(small);
+      SUB_ACC(2, t_bar);
+      if (conv) break;
+      SUB_T(t_top);
       // ---- top (every warp on its own copy): up-sweep, then down-sweep ----
       small = true;
       for (int t = 0; t < NT; ++t) {
         const int p = topbase + 32 * t + lane, q = tpriv + 32 * t;
         const int2 pi = PI[p];
         if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
-          const int pc = pi.x & 0xFFFF;
-          const double2 src = pc == 0xFFFF ? __ldg(csrc + p) : make_double2(0.0, 0.0);  // next to the slack
+          const int pc = pi.x & 0xFFFF, tq = 32 * t + lane;
+          const double2 src = pc == 0xFFFF ? TC[2 * NT * 32 + tq] : make_double2(0.0, 0.0);  // next to the slack
           double2 z = rhs_of(TV[q], TS[q], src);
-          const int kf = int(uint32_t(pi.x) >> 16), kc = pi.y & 0xF;
-          for (int k = 0; k < kc; ++k) {
-            int idx = KD[kf + k];
-            if (idx >= xcap) idx += shift;  // a subtree root: Proot
-            const double2 c = X[idx];
+          const uint32_t kf = uint32_t(pi.x) >> 16, kc = uint32_t(pi.y) & 0xF;
+          for (uint32_t k = 0; k < kc; ++k) {
+            uint32_t idx = lds_u16(kd_s + 2 * (kf + k));
+            if (idx >= uint32_t(xcap)) idx += shift;  // a subtree root: Proot
+            const double2 c = lds2(xs + 16 * idx);
             z.x -= c.x;
             z.y -= c.y;
           }
-          X[p] = cmul_s(__ldg(cg + p), z);
-          TY[q] = cmul_s(z, __ldg(cu + p));
+          sts2(xs + 16 * p, cmul_s(TC[tq], z));
+          TY[q] = cmul_s(z, TC[NT * 32 + tq]);
         }
         __syncwarp();
       }
@@ -358,8 +392,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
           const int pc = pi.x & 0xFFFF;
           double2 w = TY[q];
-          if (pc != 0xFFFF) w = cfma_sub_s(w, __ldg(cg + p), X[pc]);
-          X[p] = w;
+          if (pc != 0xFFFF) w = cfma_sub_s(w, TC[32 * t + lane], lds2(xs + 16 * pc));
+          sts2(xs + 16 * p, w);
           double2 v = TV[q];
           if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
           const double dr = w.x - v.x, di = w.y - v.y;
@@ -368,6 +402,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         }
         __syncwarp();
       }
+      SUB_ACC(3, t_top);
+      SUB_T(t_down);
       // ---- subtree down-sweep: w_m = y_m - g_m w_parent, step test |w - v|^2 < tol^2 ----
       {
         auto down_one = [&](const int j, const D2& vv, const D2& ys_or_s, const int2 pi, const int si,
@@ -431,9 +467,14 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         }
       }
       twait_st();
+      SUB_ACC(4, t_down);
       ++it;
       if (it == a.max_iter) break;
     }
+#ifdef TPF_PHASE_TIMING
+    if (tid == 0) tc[9] += it;
+#endif
+    SUB_T(t_ret);
     __syncthreads();  // every warp is done with X (the cap path leaves without a barrier)
     // ---- retire: V into X in original node order (top nodes: warp 0's copy) ----
     for (int j = 0; j < NS; ++j) {
@@ -460,6 +501,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       bulk_commit();
       a.iters[cs] = it;
     }
+    SUB_ACC(5, t_ret);
+    SUB_T(t_res);
     if (a.resid) {
       // residual_per_case (fpi.py:221-240): max_i |s_i + v_i conj(src_i + (Y_dd v)_i)|,
       // the operations of residual_kernel in the same order (Y_dd rows in CSR order;
@@ -499,17 +542,18 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           sl = TS[tpriv + 32 * (j - NS)];
         }
         if (c[0] >= 0) {
-          const double2 si = __ldg(csrc + p);
+          // src is zero below the cut: the loaded +0 and the literal +0 give the same bits
+          const double2 si = j >= NS ? TC[2 * NT * 32 + 32 * (j - NS) + lane] : make_double2(0.0, 0.0);
           double ar = si.x, ai = si.y;
 #pragma unroll
           for (int r = 0; r < kMaxRW; ++r) {
             if (c[r] >= 0) {
-              const double2 v = X[c[r]];
+              const double2 v = lds2(xs + 16 * uint32_t(c[r]));
               ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
               ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
             }
           }
-          const double2 v = X[uint32_t(pi.y) >> 16];
+          const double2 v = lds2(xs + 16 * (uint32_t(pi.y) >> 16));
           const double mr = sl.x + (v.x * ar + v.y * ai);
           const double mi = sl.y + (v.y * ar - v.x * ai);
           worst = nanmax(worst, hypot(mr, mi));
@@ -518,6 +562,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       for (int o = 16; o > 0; o >>= 1) worst = nanmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
       if (lane == 0) s_red[warp] = worst;
     }
+    SUB_ACC(6, t_res);
+    SUB_T(t_end);
     fence_async_smem();  // generic accesses to X before the next case's TMA load into it
     __syncthreads();     // X reads of the residual done; s_red complete
     if (tid == 0) {
@@ -531,7 +577,14 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       s_next = nx >= 0 ? claim() : -1;
     }
     __syncthreads();
+    SUB_ACC(7, t_end);
   }
+#ifdef TPF_PHASE_TIMING
+  if (tid == 0 && blockIdx.x < 148) {
+    tc[10] = clock64() - t_begin;
+    for (int i = 0; i < 12; ++i) g_sub_cyc[blockIdx.x * 12 + i] = tc[i];
+  }
+#endif
   if (tid == 0) bulk_wait0();
   tmem_fence_before();
   __syncthreads();
@@ -617,6 +670,12 @@ using namespace tpf;
 
 extern "C" int tpf_sparse_subtree_warps(void) { return kSubWarps; }
 
+#ifdef TPF_PHASE_TIMING
+extern "C" int tpf_debug_subtree_phase_cycles(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_sub_cyc, sizeof(g_sub_cyc)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 constexpr int64_t kSubChunk = 65536;  // cases per case-major chunk of a node-major batch
 
 extern "C" size_t tpf_sparse_subtree_workspace_bytes(int64_t tau, int32_t b) {
@@ -630,6 +689,7 @@ extern "C" size_t tpf_sparse_subtree_smem_bytes(int32_t b, int32_t ns, int32_t n
   const int64_t nbox = (b + boxrows - 1) / boxrows;
   const int64_t xcap = P > nbox * boxrows ? P : nbox * boxrows;
   return size_t(xcap + int64_t(2) * kSubWarps * rmax * 32 + 1) * 16 + size_t(3) * kSubWarps * nt * 32 * 16 +
+         size_t(3) * nt * 32 * 16 +
          size_t(P) * 8 + size_t(kSubWarps) * ns * 4 + (size_t(nkids) * 2 + 15) / 16 * 16;
 }
 

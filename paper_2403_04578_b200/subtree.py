@@ -262,7 +262,7 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
             lo, hi = int(rp[i]), int(rp[i + 1])
             ell_col[:hi - lo, p] = ci[lo:hi]
             ell_val[:hi - lo, p] = yv[lo:hi]
-    top_priv = 3 * W * NT * 32 * 16
+    top_priv = 3 * W * NT * 32 * 16 + 3 * NT * 32 * 16
     smem = (xcap + 2 * RR + 1) * 16 + top_priv + P * 8 + W * NS * 4 + kids.size * 2 + 1024
     smem = (smem + 15) // 16 * 16
     if smem > SUB_SMEM_MAX:
