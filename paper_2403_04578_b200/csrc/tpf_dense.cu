@@ -549,7 +549,7 @@ extern "C" int tpf_dense_max_nodes(void) { return 104; }
 
 extern "C" size_t tpf_dense_workspace_bytes(int32_t b) {
   (void)b;
-  return 256;
+  return 256 + 232448;  // counter slot + the ws kernel's shared-memory image (<= 227 KB)
 }
 
 extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,

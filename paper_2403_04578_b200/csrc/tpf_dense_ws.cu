@@ -66,6 +66,10 @@ struct Args {
   unsigned long long* counter;
   // step-test bracket (3M variant): high words of |delta| bounds, see step_small
   int tol_hi_small, tol_hi_big;
+  // the CTA's shared-memory image of K^T (B-fragment order), W and (3M) Kr + Ki,
+  // W_re + W_im, built once per launch by ws_image_kernel and streamed into every
+  // CTA by two cp.async.bulk copies: [0, stage_off) and [wsum_off, bytes)
+  const unsigned char* img;
 };
 
 #ifdef TPF_PHASE_TIMING
@@ -123,6 +127,7 @@ struct Shared {
   uint64_t ew_u[4][2];    // EW -> MMA (3M, NE > 0): the EW warp's share of the GEMM has read U
   int done[4][2];
   uint32_t tmem;
+  uint64_t kbar;          // the K / W image has landed (bulk copy)
 };
 
 // Two k-steps (kp, kp+1) of the complex GEMM for all NB node blocks.  Per
@@ -597,20 +602,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   double* ks_sm = reinterpret_cast<double*>(smem_raw + L::ks_off);       // [NKS][KS][32] (3M)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  constexpr int kT = 32 * (8 + 4 * SPLIT);
-  for (int idx = tid; idx < NB * KS * 32; idx += kT) {
-    const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
-    const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
-    const double2 k = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
-    k_sm[idx] = k;
-    if (M3 && nb < L::NKS) ks_sm[idx] = k.x + k.y;  // the same DADD the GEMM does for the other blocks
-  }
-  for (int i = tid; i < NB * 8; i += kT) {
-    const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
-    w_re[i] = w.x;
-    w_im[i] = w.y;
-    if (M3) w_sum[i] = w.x + w.y;
-  }
   if (tid == 0) {
     for (int q = 0; q < 4; ++q)
       for (int g = 0; g < 2; ++g) {
@@ -619,7 +610,25 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
         mbar_init(&sh.ew_u[q][g], 32);
         sh.done[q][g] = 0;
       }
+    // K^T, W (and the 3M sums) arrive as two bulk copies of the launch's image (TMA engine)
+    mbar_init(&sh.kbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    constexpr uint32_t bytes_a = uint32_t(L::stage_off), bytes_b = uint32_t(L::bytes - L::wsum_off);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sh.kbar)),
+                 "r"(bytes_a + bytes_b)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem_raw)),
+                 "l"(a.img), "r"(bytes_a), "r"(smem_u32(&sh.kbar))
+                 : "memory");
+    if (bytes_b)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(smem_raw + L::wsum_off)),
+                   "l"(a.img + L::wsum_off), "r"(bytes_b), "r"(smem_u32(&sh.kbar))
+                   : "memory");
   }
+  __syncthreads();
+  mbar_wait(&sh.kbar, 0);
   if (warp == 0) tmem_alloc(&sh.tmem, kTmemCols);
   tmem_fence_before();
   __syncthreads();
@@ -644,10 +653,46 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   if (warp == 0) tmem_dealloc(sh.tmem, kTmemCols);
 }
 
+// The launch's shared-memory image of K^T in DMMA B-fragment order (conflict-free
+// LDS.128 per fragment), W, and for the 3M GEMM Kr + Ki of the first NKS node
+// blocks and W_re + W_im (the same DADDs the GEMM would do): what every CTA's
+// prologue used to gather from K and W element by element, built once.
+template <int NB, int KS, bool M3>
+__global__ void __launch_bounds__(256) ws_image_kernel(const double* __restrict__ K, const double* __restrict__ W,
+                                                       int b, unsigned char* img) {
+  using L = Layout<NB, KS, M3>;
+  double2* k_sm = reinterpret_cast<double2*>(img);
+  double* w_re = reinterpret_cast<double*>(img + L::w_off);
+  double* w_im = w_re + NB * 8;
+  double* w_sum = reinterpret_cast<double*>(img + L::wsum_off);
+  double* ks_sm = reinterpret_cast<double*>(img + L::ks_off);
+  const int stride = gridDim.x * blockDim.x;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < NB * KS * 32; idx += stride) {
+    const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
+    const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
+    const double2 k = (row < b && col < b) ? ldg_c128(K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
+    k_sm[idx] = k;
+    if (M3 && nb < L::NKS) ks_sm[idx] = k.x + k.y;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NB * 8; i += stride) {
+    const double2 w = (i < b) ? ldg_c128(W, i) : make_double2(0.0, 0.0);
+    w_re[i] = w.x;
+    w_im[i] = w.y;
+    if (M3) w_sum[i] = w.x + w.y;
+  }
+}
+
 template <int NB, int KS, int SPLIT, bool M3, int NM = NB>
-int launch(const Args& a, cudaStream_t st, int sms) {
+int launch(const Args& a_in, cudaStream_t st, int sms) {
   static_assert(sizeof(Shared) <= 256, "Shared must fit its 256-byte slot");
   const size_t smem = Layout<NB, KS, M3>::bytes;
+  Args a = a_in;
+  // the image lives in the workspace after the 256-byte counter slot
+  unsigned char* img = static_cast<unsigned char*>(static_cast<void*>(a.counter)) + 256;
+  ws_image_kernel<NB, KS, M3><<<16, 256, 0, st>>>(a.K, a.W, a.b, img);
+  cudaError_t e0 = cudaGetLastError();
+  if (e0 != cudaSuccess) return set_cuda_error("launch(ws_image_kernel)", e0);
+  a.img = img;
   cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT, M3, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
@@ -946,7 +991,7 @@ extern "C" int tpf_dense_ws_fpi_c128(int64_t tau, int32_t b, const double* S, in
   if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
   if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
   if (tau == 0) return TPF_OK;
-  if (!S || !K || !W || !V || !iters || !workspace || workspace_bytes < 256)
+  if (!S || !K || !W || !V || !iters || !workspace || workspace_bytes < tpf_dense_workspace_bytes(b))
     return set_error(TPF_ERR_INVALID, "tpf_dense_ws_fpi_c128: null pointer or small workspace");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int dev = 0, sms = 0;
