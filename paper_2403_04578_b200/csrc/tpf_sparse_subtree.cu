@@ -374,12 +374,20 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           const double2 src = pc == 0xFFFF ? TC[2 * NT * 32 + tq] : make_double2(0.0, 0.0);  // next to the slack
           double2 z = rhs_of(TV[q], TS[q], src);
           const uint32_t kf = uint32_t(pi.x) >> 16, kc = uint32_t(pi.y) & 0xF;
-          for (uint32_t k = 0; k < kc; ++k) {
-            uint32_t idx = lds_u16(kd_s + 2 * (kf + k));
-            if (idx >= uint32_t(xcap)) idx += shift;  // a subtree root: Proot
-            const double2 c = lds2(xs + 16 * idx);
-            z.x -= c.x;
-            z.y -= c.y;
+          // children in groups of 4, their loads issued together (past the count: the zero slot)
+          for (uint32_t k0 = 0; k0 < kc; k0 += 4) {
+            double2 c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              uint32_t idx = lds_u16(kd_s + 2 * (kf + k0 + u));
+              if (idx >= uint32_t(xcap)) idx += shift;  // a subtree root: Proot
+              c[u] = lds2(xs + 16 * (k0 + u < kc ? idx : zero_idx));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              z.x -= c[u].x;
+              z.y -= c[u].y;
+            }
           }
           sts2(xs + 16 * p, cmul_s(TC[tq], z));
           TY[q] = cmul_s(z, TC[NT * 32 + tq]);
