@@ -602,6 +602,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
   double* ks_sm = reinterpret_cast<double*>(smem_raw + L::ks_off);       // [NKS][KS][32] (3M)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  constexpr int kT = 32 * (8 + 4 * SPLIT);
+  if (!a.img) {  // A/B (TPF_WS_GATHER=1): every CTA gathers K^T / W from global itself
+    for (int idx = tid; idx < NB * KS * 32; idx += kT) {
+      const int l = idx & 31, ks = (idx >> 5) % KS, nb = (idx >> 5) / KS;
+      const int row = 8 * nb + (l >> 2), col = 4 * ks + (l & 3);
+      const double2 k = (row < b && col < b) ? ldg_c128(a.K, int64_t(row) * b + col) : make_double2(0.0, 0.0);
+      k_sm[idx] = k;
+      if (M3 && nb < L::NKS) ks_sm[idx] = k.x + k.y;
+    }
+    for (int i = tid; i < NB * 8; i += kT) {
+      const double2 w = (i < b) ? ldg_c128(a.W, i) : make_double2(0.0, 0.0);
+      w_re[i] = w.x;
+      w_im[i] = w.y;
+      if (M3) w_sum[i] = w.x + w.y;
+    }
+  }
   if (tid == 0) {
     for (int q = 0; q < 4; ++q)
       for (int g = 0; g < 2; ++g) {
@@ -610,25 +626,28 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SPLIT), 1) dense_ws_kernel(const
         mbar_init(&sh.ew_u[q][g], 32);
         sh.done[q][g] = 0;
       }
-    // K^T, W (and the 3M sums) arrive as two bulk copies of the launch's image (TMA engine)
     mbar_init(&sh.kbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    constexpr uint32_t bytes_a = uint32_t(L::stage_off), bytes_b = uint32_t(L::bytes - L::wsum_off);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sh.kbar)),
-                 "r"(bytes_a + bytes_b)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(smem_raw)),
-                 "l"(a.img), "r"(bytes_a), "r"(smem_u32(&sh.kbar))
-                 : "memory");
-    if (bytes_b)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(smem_raw + L::wsum_off)),
-                   "l"(a.img + L::wsum_off), "r"(bytes_b), "r"(smem_u32(&sh.kbar))
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the async proxy sees the initialised barrier
+    if (a.img) {
+      // K^T, W (and the 3M sums) arrive as two bulk copies of the launch's image (TMA engine)
+      constexpr uint32_t bytes_a = uint32_t(L::stage_off), bytes_b = uint32_t(L::bytes - L::wsum_off);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sh.kbar)),
+                   "r"(bytes_a + bytes_b)
                    : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(smem_raw)),
+                   "l"(a.img), "r"(bytes_a), "r"(smem_u32(&sh.kbar))
+                   : "memory");
+      if (bytes_b)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(smem_raw + L::wsum_off)),
+            "l"(a.img + L::wsum_off), "r"(bytes_b), "r"(smem_u32(&sh.kbar))
+            : "memory");
+    }
   }
   __syncthreads();
-  mbar_wait(&sh.kbar, 0);
+  if (a.img) mbar_wait(&sh.kbar, 0);
   if (warp == 0) tmem_alloc(&sh.tmem, kTmemCols);
   tmem_fence_before();
   __syncthreads();
@@ -688,11 +707,22 @@ int launch(const Args& a_in, cudaStream_t st, int sms) {
   const size_t smem = Layout<NB, KS, M3>::bytes;
   Args a = a_in;
   // the image lives in the workspace after the 256-byte counter slot
+  static const bool gather = [] {  // A/B: TPF_WS_GATHER=1 gathers K per CTA instead
+    const char* e = getenv("TPF_WS_GATHER");
+    return e && e[0] == '1';
+  }();
+  static const bool img_only = [] {  // A/B: TPF_WS_GATHER=2 builds the image but gathers per CTA
+    const char* e = getenv("TPF_WS_GATHER");
+    return e && e[0] == '2';
+  }();
   unsigned char* img = static_cast<unsigned char*>(static_cast<void*>(a.counter)) + 256;
-  ws_image_kernel<NB, KS, M3><<<16, 256, 0, st>>>(a.K, a.W, a.b, img);
-  cudaError_t e0 = cudaGetLastError();
-  if (e0 != cudaSuccess) return set_cuda_error("launch(ws_image_kernel)", e0);
-  a.img = img;
+  a.img = nullptr;
+  if (!gather) {
+    ws_image_kernel<NB, KS, M3><<<16, 256, 0, st>>>(a.K, a.W, a.b, img);
+    cudaError_t e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) return set_cuda_error("launch(ws_image_kernel)", e0);
+    if (!img_only) a.img = img;
+  }
   cudaError_t err = cudaFuncSetAttribute(dense_ws_kernel<NB, KS, SPLIT, M3, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(dense_ws)", err);
   int64_t grid = sms;
