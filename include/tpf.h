@@ -147,8 +147,10 @@ int tpf_sparse_fpi_c128(int64_t tau, int32_t b,
  *   rmax, rw    root slots per warp, residual row width (<= 8)
  *   pinfo       int32[2 * P] (P = 12 * (ns + nt) * 32 positions),
  *   slotinfo    int32[12 * ns], kids uint16[nkids], coef complex[3 * P]
- *               (g, 1/U[m,m], src), ell_col int32[rw * P], ell_val
- *               complex[rw * P]: device arrays of the schedule
+ *               (g, 1/U[m,m], src), ell_col int32[P / 32][rw][32] and
+ *               ell_val complex[P / 32][rw][32] (Y_dd rows in CSR order, blocked
+ *               by slot; padding: X's zero entry, value 0): device arrays of
+ *               the schedule
  *   S, V        node-major (case stride 1) or case-major (node stride 1), 16-B aligned
  *   workspace  >= 256 device bytes; with tpf_sparse_subtree_workspace_bytes(tau, b)
  *               a node-major batch is solved in case-major chunks of 65,536

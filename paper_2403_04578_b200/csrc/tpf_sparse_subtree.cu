@@ -57,7 +57,7 @@ __device__ long long g_sub_cyc[148 * 12];
 #define SUB_ACC(i, t0)
 #endif
 constexpr int kSubThreads = 32 * kSubWarps;
-constexpr int kMaxRW = 8;   // residual row width (diagonal + parent + children)
+constexpr int kMaxRW = 7;   // residual row width (diagonal + parent + children)
 constexpr int kSubKmax = 8;  // children per node (paper_2403_04578_b200/subtree.py SUB_KMAX)
 
 struct SubArgs {
@@ -162,6 +162,11 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ int2 lds_i2(uint32_t a) {
   int2 v;
   asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
@@ -226,12 +231,17 @@ __global__ void __launch_bounds__(kSubThreads, 1)
   const int base = warp * a.NSL * 32 + lane;  // position of slot j: base + 32 j
   const int topbase = (warp * a.NSL + NS) * 32;
   const int tpriv = warp * NT * 32 + lane;    // top copy of slot t: tpriv + 32 t
-  const int32_t* si_w = SI + warp * NS;
   const double2* cg = a.coef;
   const double2* cu = a.coef + P;
   const uint32_t in_bytes =
       a.mode == 0 ? uint32_t(a.nbox) * uint32_t(a.boxrows) * 16u : uint32_t(a.b) * 16u;
-  const uint32_t xs = smem_u32(X), pi_s = smem_u32(PI), kd_s = smem_u32(KD);
+  uint32_t xs = smem_u32(X), pi_s = smem_u32(PI), kd_s = smem_u32(KD), si_s = smem_u32(SI + warp * NS);
+  // opaque to the compiler: kept in registers instead of being rematerialised
+  // (S2R SR_CgaCtaId + address arithmetic) at every shared-memory access
+  asm volatile("" : "+r"(xs), "+r"(pi_s), "+r"(kd_s), "+r"(si_s));
+  const uint32_t tv_s = xs + 16u * uint32_t(xcap + 2 * RR + 1), ts_s = tv_s + 16u * NTOP, ty_s = ts_s + 16u * NTOP,
+                 tc_s = ty_s + 16u * NTOP;
+  auto SIW = [&](const int j) { return lds_s32(si_s + 4 * j); };
   const uint32_t zero_idx = uint32_t(xcap + 2 * RR);
 
   auto claim = [&]() {
@@ -268,14 +278,14 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     mbar_wait(&s_bar, phase);
     phase ^= 1u;
     for (int j = 0; j < NS; ++j) {
-      const uint32_t o = uint32_t(PI[base + 32 * j].y) >> 16;
-      tst2(tS + 4 * j, o != 0xFFFFu ? X[o] : make_double2(0.0, 0.0));
+      const uint32_t o = uint32_t(lds_i2(pi_s + 8 * (base + 32 * j)).y) >> 16;
+      tst2(tS + 4 * j, o != 0xFFFFu ? lds2(xs + 16 * o) : make_double2(0.0, 0.0));
       tst2(tV + 4 * j, a.v_flat);  // flat start (dense.py:155)
     }
     for (int t = 0; t < NT; ++t) {
-      const uint32_t o = uint32_t(PI[topbase + 32 * t + lane].y) >> 16;
-      TS[tpriv + 32 * t] = o != 0xFFFFu ? X[o] : make_double2(0.0, 0.0);
-      TV[tpriv + 32 * t] = a.v_flat;
+      const uint32_t o = uint32_t(lds_i2(pi_s + 8 * (topbase + 32 * t + lane)).y) >> 16;
+      sts2(ts_s + 16 * (tpriv + 32 * t), o != 0xFFFFu ? lds2(xs + 16 * o) : make_double2(0.0, 0.0));
+      sts2(tv_s + 16 * (tpriv + 32 * t), a.v_flat);
     }
     twait_st();
     __syncthreads();  // X is free for the sweeps
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         auto up_step = [&](int& j, double2& g0, double2& u0, double2& g1, double2& u1, double2& gn0, double2& un0,
                            double2& gn1, double2& un1) {
           const int p0 = base + 32 * j;
-          const int si0 = si_w[j];
+          const int si0 = SIW(j);
           const bool pair = (si0 >> 4 & 1) && j + 1 < NS;
           const int jn = j + (pair ? 2 : 1);
           if (jn < NS) {
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
             tld2(tV + 4 * (j + 1), v1);
             tld2(tS + 4 * (j + 1), s1);
             const int2 pi0 = lds_i2(pi_s + 8 * p0), pi1 = lds_i2(pi_s + 8 * (p0 + 32));
-            const int si1 = si_w[j + 1];
+            const int si1 = SIW(j + 1);
             twait_ld();
             up_one(j, v0, s0, pi0, si0, g0, u0);
             up_one(j + 1, v1, s1, pi1, si1, g1, u1);
@@ -368,11 +378,11 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       small = true;
       for (int t = 0; t < NT; ++t) {
         const int p = topbase + 32 * t + lane, q = tpriv + 32 * t;
-        const int2 pi = PI[p];
+        const int2 pi = lds_i2(pi_s + 8 * p);
         if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
           const int pc = pi.x & 0xFFFF, tq = 32 * t + lane;
-          const double2 src = pc == 0xFFFF ? TC[2 * NT * 32 + tq] : make_double2(0.0, 0.0);  // next to the slack
-          double2 z = rhs_of(TV[q], TS[q], src);
+          const double2 src = pc == 0xFFFF ? lds2(tc_s + 16 * (2 * NT * 32 + tq)) : make_double2(0.0, 0.0);  // next to the slack
+          double2 z = rhs_of(lds2(tv_s + 16 * q), lds2(ts_s + 16 * q), src);
           const uint32_t kf = uint32_t(pi.x) >> 16, kc = uint32_t(pi.y) & 0xF;
           // children in groups of 4, their loads issued together (past the count: the zero slot)
           for (uint32_t k0 = 0; k0 < kc; k0 += 4) {
@@ -389,24 +399,24 @@ __global__ void __launch_bounds__(kSubThreads, 1)
               z.y -= c[u].y;
             }
           }
-          sts2(xs + 16 * p, cmul_s(TC[tq], z));
-          TY[q] = cmul_s(z, TC[NT * 32 + tq]);
+          sts2(xs + 16 * p, cmul_s(lds2(tc_s + 16 * tq), z));
+          sts2(ty_s + 16 * q, cmul_s(z, lds2(tc_s + 16 * (NT * 32 + tq))));
         }
         __syncwarp();
       }
       for (int t = NT - 1; t >= 0; --t) {
         const int p = topbase + 32 * t + lane, q = tpriv + 32 * t;
-        const int2 pi = PI[p];
+        const int2 pi = lds_i2(pi_s + 8 * p);
         if ((uint32_t(pi.y) >> 16) != 0xFFFFu) {
           const int pc = pi.x & 0xFFFF;
-          double2 w = TY[q];
-          if (pc != 0xFFFF) w = cfma_sub_s(w, TC[32 * t + lane], lds2(xs + 16 * pc));
+          double2 w = lds2(ty_s + 16 * q);
+          if (pc != 0xFFFF) w = cfma_sub_s(w, lds2(tc_s + 16 * (32 * t + lane)), lds2(xs + 16 * pc));
           sts2(xs + 16 * p, w);
-          double2 v = TV[q];
+          double2 v = lds2(tv_s + 16 * q);
           if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
           const double dr = w.x - v.x, di = w.y - v.y;
           if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;  // NaN never passes
-          TV[q] = w;
+          sts2(tv_s + 16 * q, w);
         }
         __syncwarp();
       }
@@ -430,8 +440,8 @@ __global__ void __launch_bounds__(kSubThreads, 1)
         auto down_step = [&](int& j, double2& g0, double2& u0, double2& g1, double2& u1, double2& gn0,
                              double2& un0, double2& gn1, double2& un1) {
           const int p0 = base + 32 * j;
-          const int si0 = si_w[j];
-          const bool pair = j >= 1 && (si_w[j - 1] >> 4 & 1);
+          const int si0 = SIW(j);
+          const bool pair = j >= 1 && (SIW(j - 1) >> 4 & 1);
           const int jn = j - (pair ? 2 : 1);
           if (jn >= 0) {
             gn0 = __ldg(cg + base + 32 * jn);
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(kSubThreads, 1)
             }
           }
           if (pair) {
-            const int si1 = si_w[j - 1];
+            const int si1 = SIW(j - 1);
             D2 v0, y0, v1, y1;
             tld2(tV + 4 * j, v0);
             tld2(((si0 >> 5) & 0x1F) ? tY + 4 * (((si0 >> 5) & 0x1F) - 1) : tS + 4 * j, y0);
@@ -489,13 +499,13 @@ __global__ void __launch_bounds__(kSubThreads, 1)
       D2 vv;
       tld2(tV + 4 * j, vv);
       twait_ld();
-      const uint32_t o = uint32_t(PI[base + 32 * j].y) >> 16;
-      if (o != 0xFFFFu) X[o] = vv.get();
+      const uint32_t o = uint32_t(lds_i2(pi_s + 8 * (base + 32 * j)).y) >> 16;
+      if (o != 0xFFFFu) sts2(xs + 16 * o, vv.get());
     }
     if (warp == 0) {
       for (int t = 0; t < NT; ++t) {
-        const uint32_t o = uint32_t(PI[topbase + 32 * t + lane].y) >> 16;
-        if (o != 0xFFFFu) X[o] = TV[tpriv + 32 * t];
+        const uint32_t o = uint32_t(lds_i2(pi_s + 8 * (topbase + 32 * t + lane)).y) >> 16;
+        if (o != 0xFFFFu) sts2(xs + 16 * o, lds2(tv_s + 16 * (tpriv + 32 * t)));
       }
     }
     fence_async_smem();
@@ -513,33 +523,27 @@ __global__ void __launch_bounds__(kSubThreads, 1)
     SUB_T(t_res);
     if (a.resid) {
       // residual_per_case (fpi.py:221-240): max_i |s_i + v_i conj(src_i + (Y_dd v)_i)|,
-      // the operations of residual_kernel in the same order (Y_dd rows in CSR order;
-      // padding columns -1); the next slot's row is loaded while this one is summed
-      double worst = 0.0;
+      // the operations of residual_kernel in the same order (Y_dd rows in CSR
+      // order).  ELL block of slot j: entry r of the lane's row at
+      // ((warp * NSL + j) * RW + r) * 32 + lane (one base, immediate offsets, coalesced);
+      // rows narrower than the slot's widest are padded with the zero entry of X and
+      // value 0 (adds +-0: the same magnitude, hence the same hypot).  The next
+      // slot's row is loaded while this one is summed (two register sets).
+      double worst = 0.0, thr = -1.0;
       const int nres = NS + (warp == 0 ? NT : 0);
-      int cn[kMaxRW];
-      double2 yn[kMaxRW];
-      auto load_row = [&](const int j, int* c, double2* y) {
-        const int p = base + 32 * j;
-        const int rw = j < NS ? (si_w[j] >> 10) & 0xF : a.RW;  // the slot's widest row
+      auto rw_of = [&](const int j) { return j < NS ? (SIW(j) >> 10) & 0xF : a.RW; };
+      auto load_row = [&](const int j, const int rw, int (&c)[kMaxRW], double2 (&y)[kMaxRW]) {
+        const size_t o = size_t((warp * a.NSL + j) * a.RW) * 32 + lane;
+        const int32_t* cp = a.ell_col + o;
+        const double2* vp = a.ell_val + o;
 #pragma unroll
-        for (int r = 0; r < kMaxRW; ++r) {
-          c[r] = r < rw ? __ldg(a.ell_col + r * P + p) : -1;
-          y[r] = r < rw ? __ldg(a.ell_val + r * P + p) : make_double2(0.0, 0.0);
+        for (int r = 0; r < kMaxRW; ++r) {  // every element assigned: no stale values kept live
+          c[r] = r < rw ? __ldg(cp + 32 * r) : 0;
+          y[r] = r < rw ? __ldg(vp + 32 * r) : make_double2(0.0, 0.0);
         }
       };
-      load_row(0, cn, yn);
-      for (int j = 0; j < nres; ++j) {
-        int c[kMaxRW];
-        double2 y[kMaxRW];
-#pragma unroll
-        for (int r = 0; r < kMaxRW; ++r) {
-          c[r] = cn[r];
-          y[r] = yn[r];
-        }
-        if (j + 1 < nres) load_row(j + 1, cn, yn);
-        const int p = base + 32 * j;
-        const int2 pi = PI[p];
+      auto row = [&](const int j, const int rw, const int (&c)[kMaxRW], const double2 (&y)[kMaxRW]) {
+        const uint32_t o = uint32_t(lds_i2(pi_s + 8 * (base + 32 * j)).y) >> 16;
         double2 sl;
         if (j < NS) {
           D2 sd;
@@ -547,25 +551,47 @@ __global__ void __launch_bounds__(kSubThreads, 1)
           twait_ld();
           sl = sd.get();
         } else {
-          sl = TS[tpriv + 32 * (j - NS)];
+          sl = lds2(ts_s + 16 * (tpriv + 32 * (j - NS)));
         }
-        if (c[0] >= 0) {
-          // src is zero below the cut: the loaded +0 and the literal +0 give the same bits
-          const double2 si = j >= NS ? TC[2 * NT * 32 + 32 * (j - NS) + lane] : make_double2(0.0, 0.0);
-          double ar = si.x, ai = si.y;
+        if (o == 0xFFFFu) return;  // no node at this position
+        // src is zero below the cut: the loaded +0 and the literal +0 give the same bits
+        const double2 si = j >= NS ? lds2(tc_s + 16 * (2 * NT * 32 + 32 * (j - NS) + lane)) : make_double2(0.0, 0.0);
+        double ar = si.x, ai = si.y;
 #pragma unroll
-          for (int r = 0; r < kMaxRW; ++r) {
-            if (c[r] >= 0) {
-              const double2 v = lds2(xs + 16 * uint32_t(c[r]));
-              ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
-              ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
-            }
+        for (int r = 0; r < kMaxRW; ++r)
+          if (r < rw) {
+            const double2 v = lds2(xs + 16 * uint32_t(c[r]));
+            ar = __fma_rn(y[r].x, v.x, __fma_rn(-y[r].y, v.y, ar));
+            ai = __fma_rn(y[r].x, v.y, __fma_rn(y[r].y, v.x, ai));
           }
-          const double2 v = lds2(xs + 16 * (uint32_t(pi.y) >> 16));
-          const double mr = sl.x + (v.x * ar + v.y * ai);
-          const double mi = sl.y + (v.y * ar - v.x * ai);
+        const double2 v = lds2(xs + 16 * o);
+        const double mr = sl.x + (v.x * ar + v.y * ai);
+        const double mi = sl.y + (v.y * ar - v.x * ai);
+        // hypot only where it can raise the maximum: m2 <= thr = worst^2 (1 - 1e-13)
+        // bounds |m| below worst by far more than the rounding of m2 and of hypot;
+        // NaN and inf always take the hypot, so the max is that of every row
+        const double m2 = __fma_rn(mr, mr, mi * mi);
+        if (!(m2 <= thr)) {
           worst = nanmax(worst, hypot(mr, mi));
+          thr = worst > 1e-150 ? worst * worst * (1.0 - 1e-13) : -1.0;
         }
+      };
+      int ca[kMaxRW], cb[kMaxRW];
+      double2 ya[kMaxRW], yb[kMaxRW];
+      int rwa = rw_of(0), rwb = 0;
+      load_row(0, rwa, ca, ya);
+      for (int j = 0; j < nres; j += 2) {
+        if (j + 1 < nres) {
+          rwb = rw_of(j + 1);
+          load_row(j + 1, rwb, cb, yb);
+        }
+        row(j, rwa, ca, ya);
+        if (j + 1 >= nres) break;
+        if (j + 2 < nres) {
+          rwa = rw_of(j + 2);
+          load_row(j + 2, rwa, ca, ya);
+        }
+        row(j + 1, rwb, cb, yb);
       }
       for (int o = 16; o > 0; o >>= 1) worst = nanmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
       if (lane == 0) s_red[warp] = worst;

@@ -63,8 +63,8 @@ class SubtreeSchedule:
     pinfo: np.ndarray  # int32 [P, 2]
     kids: np.ndarray   # uint16 [nk] X indices of children
     coef: np.ndarray   # complex128 [3, P]: g, 1/U[m,m], src
-    ell_col: np.ndarray  # int32 [RW, P] original column indices (CSR order), -1 padding
-    ell_val: np.ndarray  # complex128 [RW, P]
+    ell_col: np.ndarray  # int32 [P / 32, RW, 32] original column indices (CSR order); padding: X's zero entry
+    ell_val: np.ndarray  # complex128 [P / 32, RW, 32] (padding 0)
     m_at: np.ndarray     # int32 [P]: level-order node at each position (-1 empty)
     smem_bytes: int
 
@@ -242,8 +242,10 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
         return None
     pinfo = np.zeros((P, 2), dtype=np.int64)
     coef = np.zeros((3, P), dtype=np.complex128)
-    ell_col = np.full((RW, P), -1, dtype=np.int32)
-    ell_val = np.zeros((RW, P), dtype=np.complex128)
+    # ELL rows blocked by slot: entry r of position p at [p // 32, r, p % 32];
+    # padding points at X's zero entry with value 0
+    ell_col = np.full((P // 32, RW, 32), xcap + 2 * RR, dtype=np.int32)
+    ell_val = np.zeros((P // 32, RW, 32), dtype=np.complex128)
     for p in range(P):
         m = m_at[p]
         if m < 0:
@@ -260,8 +262,8 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
         if depth[m] >= D or w == 0:  # residual rows: subtree nodes and warp 0's top copies
             i = int(orig[m])
             lo, hi = int(rp[i]), int(rp[i + 1])
-            ell_col[:hi - lo, p] = ci[lo:hi]
-            ell_val[:hi - lo, p] = yv[lo:hi]
+            ell_col[p // 32, :hi - lo, p % 32] = ci[lo:hi]
+            ell_val[p // 32, :hi - lo, p % 32] = yv[lo:hi]
     top_priv = 3 * W * NT * 32 * 16 + 3 * NT * 32 * 16
     smem = (xcap + 2 * RR + 1) * 16 + top_priv + P * 8 + W * NS * 4 + kids.size * 2 + 1024
     smem = (smem + 15) // 16 * 16
