@@ -693,15 +693,16 @@ def launches_per_step(method, op, tau):
 
 
 def executed_dense(b, sum_n, kms, peak_tf):
-    """FP64 tensor work the default kernel actually issues (b <= 104: 3M GEMM,
-    3 real DMMAs per complex 8x8x4 block-product on the padded 8*ceil(b/8) x
-    4*ceil(b/4) operator; b > 104: the 4M tiled kernel on 64-padded tiles)."""
+    """FP64 tensor work the default kernel actually issues: 3M complex GEMM (3
+    real DMMAs per complex 8x8x4 block-product) in both kernels; b <= 104 on
+    the padded 8*ceil(b/8) x 4*ceil(b/4) operator, b > 104 (tiled active-set
+    kernel) counted on the unpadded b x b operator."""
     if b <= 104:
         flop = 6.0 * (8 * -(-b // 8)) * (4 * -(-b // 4)) * sum_n
         how = "3M: 6 * 8ceil(b/8) * 4ceil(b/4) * sum(n_j)"
     else:
-        flop = 8.0 * b * b * sum_n
-        how = "4M: 8 b^2 sum(n_j) (padding not counted)"
+        flop = 6.0 * b * b * sum_n
+        how = "3M: 6 b^2 sum(n_j) (tile padding not counted)"
     tf = flop / (kms * 1e-3) / 1e12
     return dict(flop=flop, tflops=tf, frac=tf / peak_tf if peak_tf else None, formula=how)
 

@@ -55,6 +55,8 @@ const char* tpf_last_error(void);
  * per-iteration op chain _iterate_chunk (dense.py:114-126):
  *     V <- K (S* ./ conj(V)) + W,   K = -inv(Y_dd) (dense.py:151),
  *                                   W = K (Y_ds v_s) (dense.py:152).
+ * K, W of the host pipelines (*_solve_host_c128) may be host or device
+ * pointers (unified addressing).
  * FP64 tensor-core (DMMA) kernel with K resident in shared memory:
  * requires b <= tpf_dense_max_nodes() (104); larger b: the _large_ entry below.
  *   S      b x tau complex loads (consumption positive), device
@@ -64,6 +66,18 @@ const char* tpf_last_error(void);
  *   iters  int32[tau] per-case update counts, device
  *   workspace >= tpf_dense_workspace_bytes(b) device bytes
  */
+/* Dense setup on the device for radial feeders (replaces dense.py:150-152,
+ * K = -inv(Y_dd) and W = K src on the host by LAPACK): column j of K is the
+ * tree-LU solve Y_dd x = -e_j (one thread per column, O(b) each), then
+ * W = K src.  The tree LU is the sparse path's (sparse.py:186; layout of
+ * tpf_sparse_tree_fpi_c128: level offsets int32[levels + 1], node_info
+ * int32[4 b] {original node, parent, first child, child count} in level
+ * order, node_coef complex[4 b] planes e, g, 1/U[m,m], src).  K agrees with
+ * LAPACK's inverse to rounding (not bitwise).  All pointers device; K b x b
+ * row-major complex, W b complex, src b complex (original order).
+ * Stream-ordered. */
+int tpf_dense_setup_tree_c128(int32_t b, int32_t levels, const int32_t* level_off, const int32_t* node_info,
+                              const double* node_coef, const double* src, double* K, double* W, void* stream);
 int tpf_dense_max_nodes(void);
 size_t tpf_dense_workspace_bytes(int32_t b);
 int tpf_dense_fpi_c128(int64_t tau, int32_t b,

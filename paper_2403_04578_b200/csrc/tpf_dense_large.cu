@@ -13,7 +13,7 @@
 //   gemm    V'[a, n] = W[n] + sum_k U[k, a] K[n, k] on FP64 tensor cores:
 //           64x64 complex CTA tiles, 16-node k-slabs double-buffered through
 //           shared memory with cp.async (zero-filled at the edges), 8 warps of
-//           32x16 complex each, 4 real DMMA.8x8x4 per complex fragment; the
+//           32x16 complex each, 3 real DMMA.8x8x4 per complex fragment (3M); the
 //           epilogue reads the old iterate, writes the new one in place and
 //           flags the case if any |dv|^2 >= tol^2 (or non-finite);
 //   compact count the update, keep flagged cases below max_iter.

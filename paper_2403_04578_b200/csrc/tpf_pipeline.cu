@@ -247,7 +247,7 @@ template <class T>
 cudaError_t upload(DevBuf& d, const T* h, size_t n, cudaStream_t st) {
   cudaError_t e = d.alloc(n * sizeof(T));
   if (e != cudaSuccess || n == 0) return e;
-  return cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st);
+  return cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyDefault, st);  // host or device source (UVA)
 }
 
 // Solver callback: run the iteration on device chunk (S_dev -> V_dev) for n cases.

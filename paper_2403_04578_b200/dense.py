@@ -13,9 +13,12 @@ Reference: pkg/src/tpflow/dense.py:129-205.  Same signature, same
 * ``numpy.linalg.LinAlgError`` from the inverse of a singular Y_dd
   (dense.py:151, uncaught in the reference too).
 
-Setup follows the reference exactly (K = -inv(Y_dd) by LAPACK on the host,
-W = K src); the iteration, the residual post-check and the converged mask run
-in libtpf.so.  ``workers`` is accepted and ignored (results are bitwise
+Setup (dense.py:150-152): K = -inv(Y_dd) and W = K src by LAPACK on the host
+exactly as the reference (bitwise the reference's K) for b < DEVICE_SETUP_MIN_B
+or meshed networks; radial feeders from that size get K and W on the device
+(``tpf_dense_setup_tree_c128``: column j of K is one tree-LU solve, O(b^2) in
+all instead of the O(b^3) host inverse; equal to LAPACK's to rounding).  The
+iteration, the residual post-check and the converged mask run in libtpf.so.  ``workers`` is accepted and ignored (results are bitwise
 independent of any partitioning, like the reference's, test_dense.py:96-102).
 """
 
@@ -39,6 +42,59 @@ __all__ = ["batch_solve_dense", "DenseOperator"]
 _KW_CACHE: "OrderedDict[bytes, tuple[np.ndarray, np.ndarray]]" = OrderedDict()
 _KW_CACHE_MAX = 8
 _KW_LOCK = threading.Lock()
+
+
+DEVICE_SETUP_MIN_B = 256  # radial feeders from this size: K, W built on the device
+
+
+def device_kw(contract: ModelContract, device) -> tuple[torch.Tensor, torch.Tensor] | None:
+    """K = -inv(Y_dd), W = K src on ``device`` from the tree LU of a radial
+    feeder (``tpf_dense_setup_tree_c128``), or None when Y_dd has no zero-fill
+    tree elimination (meshed networks: host LAPACK).  Memoised with the host
+    entries (same cache, so clearing it re-times the setup)."""
+    from .sparse import factorize_ydd, tree_levels
+    dev = torch.device(device)
+    key = contract.fingerprint() + b"|device:" + str(dev.index).encode()
+    with _KW_LOCK:
+        hit = _KW_CACHE.get(key)
+        if hit is not None:
+            _KW_CACHE.move_to_end(key)
+            return hit
+    t = tree_levels(factorize_ydd(contract.y_dd, count=False), contract.src)
+    if t is None:
+        return None
+    b = contract.b
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    lvl = up(t.level_info[:t.levels + 1].astype(np.int32))
+    info = up(t.node_info.astype(np.int32))
+    coef = up(t.node_coef.astype(np.complex128))
+    src = up(contract.src.astype(np.complex128))
+    K = torch.empty((b, b), dtype=torch.complex128, device=dev)
+    W = torch.empty(b, dtype=torch.complex128, device=dev)
+    _capi.call("tpf_dense_setup_tree_c128", b, int(t.levels), lvl.data_ptr(), info.data_ptr(), coef.data_ptr(),
+               src.data_ptr(), K.data_ptr(), W.data_ptr(), stream_ptr(dev))
+    torch.cuda.current_stream(dev).synchronize()  # the inputs above are freed on return
+    with _KW_LOCK:
+        _KW_CACHE[key] = (K, W)
+        while len(_KW_CACHE) > _KW_CACHE_MAX:
+            _KW_CACHE.popitem(last=False)
+    return K, W
+
+
+def operator_kw(contract: ModelContract, device, setup: str = "auto"):
+    """(K, W) for ``device``: device tensors from ``device_kw`` (``setup``
+    "device", or "auto" with b >= DEVICE_SETUP_MIN_B, on radial feeders), else
+    the host LAPACK arrays of ``dense_kw``."""
+    if setup not in ("auto", "host", "device"):
+        raise ValueError(f"setup must be 'auto', 'host' or 'device', not {setup!r}")
+    if setup == "device" or (setup == "auto" and contract.b >= DEVICE_SETUP_MIN_B):
+        kw = device_kw(contract, device)
+        if kw is not None:
+            return kw
+    return dense_kw(contract)
 
 
 def dense_kw(contract: ModelContract) -> tuple[np.ndarray, np.ndarray]:
@@ -73,17 +129,21 @@ class DenseOperator:
     what ``batch_solve_dense`` and ``bench.py`` call.
     """
 
-    def __init__(self, model, device=None, dtype=None):
+    def __init__(self, model, device=None, dtype=None, setup: str = "auto"):
         self.device = require_cuda(device)
         self.contract = ModelContract.of(model)
         self.dtype = engine_dtype(dtype)
         b = self.contract.b
-        K, W = dense_kw(self.contract)
-        self.K_host = K
-        self.W_host = W
+        K, W = operator_kw(self.contract, self.device, setup)
+        self.setup = "device" if torch.is_tensor(K) else "host"
         # K, W in the engine's dtype (c64: rounded from the float64 inverse)
-        self.K = torch.from_numpy(np.array(K, dtype=self.dtype)).to(self.device)
-        self.W = torch.from_numpy(np.array(W, dtype=self.dtype)).to(self.device)
+        tdt = torch.complex64 if self.dtype == np.complex64 else torch.complex128
+        if torch.is_tensor(K):
+            self.K = K.to(tdt)
+            self.W = W.to(tdt)
+        else:
+            self.K = torch.from_numpy(np.array(K, dtype=self.dtype)).to(self.device)
+            self.W = torch.from_numpy(np.array(W, dtype=self.dtype)).to(self.device)
         self.large = b > _capi.load().tpf_dense_max_nodes()
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
@@ -404,7 +464,6 @@ def finish(V, iters, resid, mask, summ, on_device: bool) -> VoltageBatch:
 
 def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chunk_cases: int):
     c = ModelContract.of(model)
-    K, W = dense_kw(c)
     rp, ci, yv = host_csr(c)
     S, sn, sc = host_loads(loads.values)
     b, tau = S.shape
@@ -422,8 +481,11 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chu
             return summ
         ws = device_workspace_slot(dev, lib.tpf_dense_solve_host_workspace_bytes(n, b, int(chunk_cases), yv.size),
                                    slot)
+        K, W = operator_kw(c, dev)  # host LAPACK arrays, or device tensors on dev (radial, large b)
+        kp = K.data_ptr() if torch.is_tensor(K) else ptr(K)
+        wp = W.data_ptr() if torch.is_tensor(W) else ptr(W)
         torch.cuda.current_stream(dev).synchronize()  # the pipeline runs on its own streams
-        _capi.call("tpf_dense_solve_host_c128", n, b, ptr(S) + 16 * lo * sc, sn, sc, ptr(K), ptr(W), ptr(rp),
+        _capi.call("tpf_dense_solve_host_c128", n, b, ptr(S) + 16 * lo * sc, sn, sc, kp, wp, ptr(rp),
                    ptr(ci), ptr(yv), ptr(c.src), v_flat.real, v_flat.imag, float(opts.tolerance),
                    int(opts.max_iterations), float(opts.residual_tolerance), ptr(V) + 16 * lo, tau, 1,
                    ptr(iters) + 4 * lo, ptr(resid) + 8 * lo, ptr(mask) + lo, ptr(summ), int(chunk_cases),
