@@ -23,6 +23,12 @@ int set_cuda_error(const char* where, cudaError_t err) {
 // residual_per_case (fpi.py:221-240): one thread per case; Y_dd rows are read
 // uniformly by the warp (broadcast), V/S accesses coalesce over cases when the
 // case stride is 1 (the reference's b x tau layout).
+// Batches too small to fill the GPU one thread per case (C5: 8,760 cases of
+// b = 1,000) split the rows over blockIdx.y: each thread takes rows [i0, i1)
+// of its case and the per-case maximum is an atomicMax on the bits of the
+// non-negative partial maxima (their order as unsigned integers is the numeric
+// order, and NaN's patterns sort above every number, as nanmax keeps NaN), so
+// the result is the same number as the single-thread row loop.
 __global__ void residual_kernel(int64_t tau, int b, const double* __restrict__ S, int64_t sn, int64_t sc,
                                 const double* __restrict__ V, int64_t vn, int64_t vc,
                                 const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -30,8 +36,10 @@ __global__ void residual_kernel(int64_t tau, int b, const double* __restrict__ S
                                 double* __restrict__ resid) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= tau) return;
+  const int nrb = int(gridDim.y);
+  const int i0 = int(int64_t(b) * blockIdx.y / nrb), i1 = int(int64_t(b) * (blockIdx.y + 1) / nrb);
   double worst = 0.0;
-  for (int i = 0; i < b; ++i) {
+  for (int i = i0; i < i1; ++i) {
     const double2 si = ldg_c128(src, i);
     double ar = si.x, ai = si.y;
     for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k) {
@@ -47,7 +55,11 @@ __global__ void residual_kernel(int64_t tau, int b, const double* __restrict__ S
     const double mi = s.y + (v.y * ar - v.x * ai);
     worst = nanmax(worst, hypot(mr, mi));
   }
-  resid[j] = worst;
+  if (nrb == 1) {
+    resid[j] = worst;
+  } else {
+    atomicMax(reinterpret_cast<unsigned long long*>(resid) + j, __double_as_longlong(worst));
+  }
 }
 
 __global__ void summary_kernel(int64_t tau, const int32_t* __restrict__ iters, const double* __restrict__ resid,
@@ -107,7 +119,21 @@ extern "C" int tpf_residual_c128(int64_t tau, int32_t b, const double* S, int64_
     return set_error(TPF_ERR_INVALID, "tpf_residual_c128: null pointer");
   const int threads = 256;
   const int64_t blocks = (tau + threads - 1) / threads;
-  residual_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // row blocks: enough threads for ~8 resident warps per scheduler on every SM,
+  // at least 16 rows each
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t nrb = (int64_t(sms) * 2048 + tau - 1) / tau;
+  if (nrb > b / 16) nrb = b / 16;
+  if (nrb > 65535) nrb = 65535;
+  if (nrb < 1) nrb = 1;
+  if (nrb > 1) {
+    cudaError_t e = cudaMemsetAsync(resid, 0, size_t(tau) * sizeof(double), st);  // +0.0: nanmax's start
+    if (e != cudaSuccess) return set_cuda_error("cudaMemsetAsync(resid)", e);
+  }
+  residual_kernel<<<dim3(unsigned(blocks), unsigned(nrb)), threads, 0, st>>>(
       tau, b, S, s_node_stride, s_case_stride, V, v_node_stride, v_case_stride, ydd_row_ptr, ydd_col, ydd_val,
       src, resid);
   cudaError_t err = cudaGetLastError();

@@ -97,16 +97,19 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
 
-// CTA tile TMV cases x TN nodes, 8 warps as WM x (8/WM).  Two instantiations:
-// TMV = 64 for the bulk of the solve and TMV = 8 for the heavy tail, when at
-// most kTailM cases are still active (near voltage collapse a few cases need
-// many more iterations; 64-row tiles would then be mostly empty rows).  Each
-// launch exits at once when the active count is outside its range.  Both
-// issue the same DMMAs in the same order for every output element, so a
+// CTA tile TMV cases x TN nodes, 8 warps as WM x (8/WM), for the bulk of the
+// solve (TMV = 64).  When at most kTailM cases are still active (near voltage
+// collapse a few cases need many more iterations) tail_kernel runs instead;
+// each launch exits at once when the active count is outside its range.
+// Both issue the same DMMAs in the same order for every output element, so a
 // case's bits do not depend on which one ran an iteration.
 constexpr int kTailM = 64;
 
-template <int TMV, int WM>
+// NST-stage cp.async pipeline over the k-slabs: the bulk kernel double-buffers;
+// the tail (few cases, so few CTAs each streaming a 64-node slice of K from L2)
+// keeps NST - 1 slabs in flight to cover the L2 latency.  The stage count does
+// not change the k-order.
+template <int TMV, int WM, int NST>
 __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
   constexpr int WN = 8 / WM;
   constexpr int MFR = TMV / WM / 8, NFR = TN / WN / 8;  // fragments per warp tile
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
   // fragment-ordered slabs: A[ks][mf][lane], B[ks][nf][lane]
   extern __shared__ __align__(16) double2 dyn_smem[];
   double2 (*As)[KSTEPS * MFT * 32] = reinterpret_cast<double2 (*)[KSTEPS * MFT * 32]>(dyn_smem);
-  double2 (*Bs)[KSTEPS * NF * 32] = reinterpret_cast<double2 (*)[KSTEPS * NF * 32]>(dyn_smem + 2 * KSTEPS * MFT * 32);
+  double2 (*Bs)[KSTEPS * NF * 32] = reinterpret_cast<double2 (*)[KSTEPS * NF * 32]>(dyn_smem + NST * KSTEPS * MFT * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN;
   const int wn = warp % WN;
@@ -159,16 +162,23 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
       for (int e = 0; e < 2; ++e) p1[i][j][e] = p2[i][j][e] = p3[i][j][e] = 0.0;
 
   const int nslabs = (b + TK - 1) / TK;
-  load_slab(0, 0);
+  // one commit group per slab (empty past the end), so slab s is complete when
+  // at most NST - 2 newer groups are pending
+#pragma unroll
+  for (int st = 0; st < NST - 1; ++st) {
+    if (st < nslabs)
+      load_slab(st, st * TK);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int s = 0; s < nslabs; ++s) {
-    const int stage = s & 1;
-    if (s + 1 < nslabs) {
-      load_slab(stage ^ 1, (s + 1) * TK);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
+    const int stage = s % NST;
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
+    __syncthreads();  // slab s visible to all; every thread is done with slab s - 1
+    if (s + NST - 1 < nslabs)
+      load_slab((s + NST - 1) % NST, (s + NST - 1) * TK);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
       double2 af[MFR], bf[NFR];
@@ -193,8 +203,8 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
         }
       }
     }
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   double cr[MFR][NFR][2], ci[MFR][NFR][2];
 #pragma unroll
   for (int i = 0; i < MFR; ++i)
@@ -235,6 +245,91 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
     row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 2);
     if (row_bad && mvalid && (lane & 3) == 0) atomicOr(a.bad + m, 1);
   }
+}
+
+// The heavy tail (at most kTailM cases still active): one warp per 8 x 8
+// output fragment (8 cases x 8 nodes), no CTA barriers.  Each lane streams the
+// single A element (case lane / 4, k = 4 ks + lane % 4) and B element (node
+// lane / 4, same k) it feeds to the DMMA through a private ring of kTailDepth
+// cp.async stages, so the only serial chain per fragment is the DMMA
+// accumulation itself.  The k-steps, the zero padding of k to a multiple of TK,
+// the 3M products and the epilogue are those of gemm_kernel: a case's bits do
+// not depend on which kernel ran an iteration.
+constexpr int kTailDepth = 16;
+
+constexpr int kTailWarps = 4;  // one fragment per SM sub-partition: the DMMA pipe is per SMSP
+
+__global__ void __launch_bounds__(32 * kTailWarps) tail_kernel(LargeArgs a, int cur) {
+  const int n_act = a.count[cur];
+  if (n_act > kTailM) return;
+  const int m0 = blockIdx.y * 8;
+  if (m0 >= n_act) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = a.b;
+  const int n0 = (blockIdx.x * kTailWarps + warp) * 8;
+  if (n0 >= b) return;
+  extern __shared__ __align__(16) double2 dyn_smem[];  // [warps][kTailDepth][A, B][32 lanes]
+  double2 (*rg)[2][32] = reinterpret_cast<double2 (*)[2][32]>(dyn_smem + size_t(warp) * kTailDepth * 64);
+  const int nks = (b + TK - 1) / TK * KSTEPS;  // k-steps of 4, padded like the slabs
+  const int mr = m0 + (lane >> 2), nr = n0 + (lane >> 2), kk = lane & 3;
+  const bool mok = mr < n_act, nok = nr < b;
+  const double2* ua = a.U + mr;
+  const double2* kb = a.K + int64_t(nok ? nr : 0) * b;
+  auto issue = [&](const int ks) {
+    const int k = 4 * ks + kk;
+    const bool kok = k < b;
+    const int st = ks % kTailDepth;
+    cp_async16(&rg[st][0][lane], (mok && kok) ? ua + int64_t(k) * a.tau : a.U, mok && kok);
+    cp_async16(&rg[st][1][lane], (nok && kok) ? kb + k : a.K, nok && kok);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll 1
+  for (int ks = 0; ks < kTailDepth - 1; ++ks) {
+    if (ks < nks)
+      issue(ks);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+#pragma unroll 1
+  for (int ks = 0; ks < nks; ++ks) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kTailDepth - 2) : "memory");
+    const int st = ks % kTailDepth;
+    const double2 af = rg[st][0][lane], bf = rg[st][1][lane];  // this lane's own copies
+    if (ks + kTailDepth - 1 < nks)
+      issue(ks + kTailDepth - 1);
+    else
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    const double as = af.x + af.y, bs = bf.x + bf.y;
+    dmma884(p1[0], p1[1], af.x, bf.x);
+    dmma884(p2[0], p2[1], af.y, bf.y);
+    dmma884(p3[0], p3[1], as, bs);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // epilogue of gemm_kernel for one fragment
+  const int* act = a.act[cur];
+  const int m = mr;
+  bool row_bad = false;
+  const int c = mok ? act[m] : 0;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int n = n0 + 2 * (lane & 3) + e;
+    if (mok && n < b) {
+      const double cr = p1[e] - p2[e];
+      const double ci = (p3[e] - p1[e]) - p2[e];
+      double2* vp = a.V + n * a.v_node + int64_t(c) * a.v_case;
+      double2 old = *vp;
+      if (__fma_rn(old.x, old.x, old.y * old.y) < kZeroGuard2) old = make_double2(kZeroGuard, 0.0);
+      const double2 w = __ldg(a.W + n);
+      const double2 nv = make_double2(cr + w.x, ci + w.y);
+      const double dr = nv.x - old.x, di = nv.y - old.y;
+      if (!(__fma_rn(dr, dr, di * di) < a.tol2)) row_bad = true;
+      *vp = nv;
+    }
+  }
+  row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 1);
+  row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 2);
+  if (row_bad && mok && (lane & 3) == 0) atomicOr(a.bad + m, 1);
 }
 
 __global__ void compact_kernel(LargeArgs a, int cur) {
@@ -311,16 +406,22 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const dim3 ggrid(unsigned((tau + TM - 1) / TM), unsigned((b + TN - 1) / TN));
   const unsigned pgrid = unsigned(sms) * 8;
-  const int gsmem = int(2 * KSTEPS * (MF + NF) * 32 * sizeof(double2));
-  const int gsmem_tail = int(2 * KSTEPS * (1 + NF) * 32 * sizeof(double2));
-  cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel<TM, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
+  constexpr int kBulkStages = 2;
+  const int gsmem = int(kBulkStages * KSTEPS * (MF + NF) * 32 * sizeof(double2));
+  cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel<TM, 2, kBulkStages>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
   if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(gemm_kernel)", aerr);
-  const dim3 tgrid(unsigned(kTailM / 8), unsigned((b + TN - 1) / TN));
+  // node groups fastest: the active fragments (cases m0 < n_act) of one
+  // iteration spread over the SMs
+  const dim3 tgrid(unsigned((b + 8 * kTailWarps - 1) / (8 * kTailWarps)), unsigned(kTailM / 8));
+  const int tsmem = int(kTailWarps * kTailDepth * 64 * sizeof(double2));
+  aerr = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+  if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tail_kernel)", aerr);
   for (int it = 0; it < max_iter; ++it) {
     const int cur = it & 1;
     prep_kernel<<<pgrid, 256, 0, st>>>(a, cur);
-    gemm_kernel<TM, 2><<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
-    gemm_kernel<8, 1><<<tgrid, LTHREADS, gsmem_tail, st>>>(a, cur);
+    gemm_kernel<TM, 2, kBulkStages><<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
+    tail_kernel<<<tgrid, 32 * kTailWarps, tsmem, st>>>(a, cur);
     compact_kernel<<<tb, 256, 0, st>>>(a, cur);
   }
   cudaError_t err = cudaGetLastError();
