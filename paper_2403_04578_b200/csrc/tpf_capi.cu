@@ -127,6 +127,8 @@ extern "C" int tpf_residual_c128(int64_t tau, int32_t b, const double* S, int64_
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t nrb = (int64_t(sms) * 2048 + tau - 1) / tau;
   if (nrb > b / 16) nrb = b / 16;
+  if (const char* e = getenv("TPF_RESID_NRB")) nrb = atoi(e);  // A/B knob (tools/c2_resid_probe.py)
+  if (nrb > b) nrb = b;
   if (nrb > 65535) nrb = 65535;
   if (nrb < 1) nrb = 1;
   if (nrb > 1) {
