@@ -272,6 +272,22 @@ int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, const int32_t*
                            double* V, int64_t v_node_stride, int64_t v_case_stride, int32_t* iters,
                            double* resid, uint8_t* step_met, int32_t* status,
                            void* workspace, size_t workspace_bytes, void* stream);
+/* ZIP loads on small meshed networks (b <= tpf_sparse_zip_dense_max_nodes(),
+ * 64) with partial pivoting, as the reference's per-case splu (fpi.py:119):
+ * one thread per case, dense LU of B = Y_dd + diag(alpha_z s*) with row
+ * pivoting (largest |.| in the column), then fpi_solve's iteration and ZIP
+ * residual as tpf_sparse_zip_lu_c128.  y_dense = Y_dd b x b row-major; alpha
+ * [3][b], src, S, V, v0 in original node order; the residual reads Y_dd in
+ * CSR.  workspace >= tpf_sparse_zip_dense_workspace_bytes(tau, b).
+ * *status = 1 on a zero pivot (a singular B).                             */
+int tpf_sparse_zip_dense_max_nodes(void);
+size_t tpf_sparse_zip_dense_workspace_bytes(int64_t tau, int32_t b);
+int tpf_sparse_zip_dense_c128(int64_t tau, int32_t b, const double* y_dense, const double* alpha, const double* src,
+                              const int32_t* y_row_ptr, const int32_t* y_col, const double* y_val, const double* S,
+                              int64_t s_node_stride, int64_t s_case_stride, double v_flat_re, double v_flat_im,
+                              const double* v0, double tol, int32_t max_iter, double* V, int64_t v_node_stride,
+                              int64_t v_case_stride, int32_t* iters, double* resid, uint8_t* step_met,
+                              int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
 size_t tpf_sparse_tree_zip_workspace_bytes(int64_t tau, int32_t b);
 int tpf_sparse_tree_zip_fpi_c128(int64_t tau, int32_t b, int32_t levels,
                                  const int32_t* level_info, const int32_t* node_info, const double* node_coef,

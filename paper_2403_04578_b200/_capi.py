@@ -96,6 +96,11 @@ SIGNATURES = {
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64,
         _c_i64, _c_dbl, _c_dbl, _c_ptr, _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
         _c_sz, _c_ptr]),
+    "tpf_sparse_zip_dense_max_nodes": (ctypes.c_int, []),
+    "tpf_sparse_zip_dense_workspace_bytes": (_c_sz, [_c_i64, _c_i32]),
+    "tpf_sparse_zip_dense_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_ptr,
+        _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_sz, _c_ptr]),
     "tpf_sparse_tree_zip_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_i64, _c_i64, _c_dbl, _c_dbl, _c_ptr,
         _c_dbl, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_sz,

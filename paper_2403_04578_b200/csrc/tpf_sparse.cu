@@ -17,6 +17,8 @@
 // until its own step test passes (per-case freeze).
 #include <climits>
 
+#include <cstring>
+
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
 
@@ -639,5 +641,227 @@ extern "C" int tpf_sparse_zip_lu_c128(int64_t tau, int32_t b, int32_t nslot, con
   sparse_zip_lu_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(a);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(sparse_zip_lu_kernel)", err);
+  return TPF_OK;
+}
+
+// ZIP loads on small meshed networks with the pivoting of the reference's
+// per-case SuperLU (fpi.py:119, splu's partial pivoting): one thread per case,
+// B = Y_dd + diag(alpha_z s*) dense (b <= kZipDenseMaxB), LU with partial
+// pivoting by rows (largest |.|^2 in the column, first on ties), then
+// fpi_solve's iteration and ZIP residual exactly as sparse_zip_lu_kernel, in
+// original node order.  Scratch, case-minor: the factors [b * b][tau], one
+// right-hand side [b][tau] and the pivot rows [b][tau].
+namespace tpf {
+namespace {
+
+constexpr int kZipDenseMaxB = 64;
+
+__global__ void __launch_bounds__(128) sparse_zip_dense_kernel(const ZipLuArgs a, int32_t* __restrict__ piv) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= a.tau) return;
+  const int b = a.b;
+  const int64_t t = a.tau;
+  double2* F = a.F + j;
+  double2* Z = a.Z + j;
+  int32_t* P = piv + j;
+  auto A = [&](int r, int c) -> double2& { return F[(int64_t(r) * b + c) * t]; };
+  auto Sk = [&](int k) { return a.S[int64_t(k) * a.s_node + j * a.s_case]; };
+  auto Vn = [&](int node) -> double2& { return a.V[int64_t(node) * a.v_node + j * a.v_case]; };
+  for (int s = 0; s < b * b; ++s) F[s * t] = __ldg(a.base + s);
+  bool any = false, bad = false;
+  for (int k = 0; k < b; ++k) {
+    const double2 s = Sk(k);
+    const double az = __ldg(a.alpha + k), ap = __ldg(a.alpha + 2 * b + k);
+    const double2 yd = A(k, k);
+    A(k, k) = make_double2(__fma_rn(az, s.x, yd.x), __fma_rn(-az, s.y, yd.y));
+    if (ap != 0.0 && (s.x != 0.0 || s.y != 0.0)) any = true;
+  }
+  // right-looking LU with row pivoting; the diagonal keeps 1 / U[k,k]
+  for (int k = 0; k < b; ++k) {
+    int p = k;
+    double best = -1.0;
+    for (int r = k; r < b; ++r) {
+      const double2 x = A(r, k);
+      const double n2 = __fma_rn(x.x, x.x, x.y * x.y);
+      if (n2 > best) {
+        best = n2;
+        p = r;
+      }
+    }
+    P[k * t] = p;
+    if (p != k)
+      for (int c = 0; c < b; ++c) {
+        const double2 x = A(k, c);
+        A(k, c) = A(p, c);
+        A(p, c) = x;
+      }
+    const double2 pv = A(k, k);
+    const double n2 = __fma_rn(pv.x, pv.x, pv.y * pv.y);
+    if (!(n2 > 0.0) || !isfinite(n2)) bad = true;
+    const double rr = 1.0 / n2;
+    const double2 ui = make_double2(pv.x * rr, -pv.y * rr);
+    A(k, k) = ui;
+    for (int r = k + 1; r < b; ++r) {
+      const double2 l = cmulz(A(r, k), ui);
+      A(r, k) = l;
+      for (int c = k + 1; c < b; ++c) {
+        const double2 lu = cmulz(l, A(k, c));
+        double2 x = A(r, c);
+        x.x -= lu.x;
+        x.y -= lu.y;
+        A(r, c) = x;
+      }
+    }
+  }
+  if (bad) atomicExch(a.status, 1);
+  for (int k = 0; k < b; ++k) Vn(k) = a.v0 ? __ldg(a.v0 + k) : a.v_flat;  // fpi.py:141-145
+  int n = 0;
+  bool met = false;
+  while (n < a.max_iter) {
+    for (int k = 0; k < b; ++k) {
+      double2 v = Vn(k);
+      double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+      if (m2 < kZeroGuard2) {
+        v = make_double2(kZeroGuard, 0.0);
+        m2 = kZeroGuard * kZeroGuard;
+      }
+      const double r = 1.0 / m2;
+      const double2 s = Sk(k);
+      const double ai = __ldg(a.alpha + b + k), ap = __ldg(a.alpha + 2 * b + k);
+      const double2 c = __ldg(a.src + k);
+      const double ur = __fma_rn(s.x, v.x, s.y * v.y) * r, uim = __fma_rn(s.x, v.y, -(s.y * v.x)) * r;
+      Z[k * t] = any ? make_double2(-(ap * ur + c.x + ai * s.x), -(ap * uim + c.y - ai * s.y))
+                     : make_double2(-(c.x + ai * s.x), -(c.y - ai * s.y));
+    }
+    for (int k = 0; k < b; ++k) {  // the row swaps, in order
+      const int p = P[k * t];
+      if (p != k) {
+        const double2 x = Z[k * t];
+        Z[k * t] = Z[int64_t(p) * t];
+        Z[int64_t(p) * t] = x;
+      }
+    }
+    for (int k = 0; k < b; ++k) {  // forward (unit L)
+      const double2 zk = Z[k * t];
+      for (int r = k + 1; r < b; ++r) {
+        const double2 lz = cmulz(A(r, k), zk);
+        double2 x = Z[r * t];
+        x.x -= lz.x;
+        x.y -= lz.y;
+        Z[r * t] = x;
+      }
+    }
+    bool small = true, fin = true;
+    for (int k = b - 1; k >= 0; --k) {  // backward (U), the step test and the update
+      double2 acc = Z[k * t];
+      for (int c = k + 1; c < b; ++c) {
+        const double2 uz = cmulz(A(k, c), Z[c * t]);
+        acc.x -= uz.x;
+        acc.y -= uz.y;
+      }
+      const double2 w = cmulz(acc, A(k, k));
+      Z[k * t] = w;
+      double2& vk = Vn(k);
+      double2 v = vk;
+      if (__fma_rn(v.x, v.x, v.y * v.y) < kZeroGuard2) v = make_double2(kZeroGuard, 0.0);
+      const double dr = w.x - v.x, di = w.y - v.y;
+      if (!(__fma_rn(dr, dr, di * di) < a.tol2)) small = false;
+      if (!(isfinite(w.x) && isfinite(w.y))) fin = false;
+      vk = w;
+    }
+    ++n;
+    if (!any) {
+      met = true;
+      break;
+    }
+    if (!fin) break;
+    if (small) {
+      met = true;
+      break;
+    }
+  }
+  // ZIP residual: max_k |az s |v|^2 + ai s v + ap s + v conj(src + (Y v)_k)|
+  double worst = 0.0;
+  for (int k = 0; k < b; ++k) {
+    double2 yv = make_double2(0.0, 0.0);
+    for (int e = __ldg(a.rp + k); e < __ldg(a.rp + k + 1); ++e) {
+      const double2 x = cmulz(__ldg(a.yv + e), Vn(__ldg(a.ci + e)));
+      yv.x += x.x;
+      yv.y += x.y;
+    }
+    const double2 v = Vn(k), s = Sk(k), c = __ldg(a.src + k);
+    const double az = __ldg(a.alpha + k), zi = __ldg(a.alpha + b + k), zp = __ldg(a.alpha + 2 * b + k);
+    const double v2 = v.x * v.x + v.y * v.y;
+    const double2 sv = cmulz(s, v);
+    const double lr = az * s.x * v2 + zi * sv.x + zp * s.x, li = az * s.y * v2 + zi * sv.y + zp * s.y;
+    const double ar = c.x + yv.x, aim = c.y + yv.y;
+    const double mr = lr + (v.x * ar + v.y * aim), mi = li + (v.y * ar - v.x * aim);
+    worst = nanmax(worst, hypot(mr, mi));
+  }
+  a.iters[j] = n;
+  a.resid[j] = worst;
+  a.met[j] = met ? 1 : 0;
+}
+
+}  // namespace
+}  // namespace tpf
+
+extern "C" int tpf_sparse_zip_dense_max_nodes(void) { return tpf::kZipDenseMaxB; }
+
+extern "C" size_t tpf_sparse_zip_dense_workspace_bytes(int64_t tau, int32_t b) {
+  return (size_t(b) * size_t(b) + size_t(b)) * size_t(tau) * 16 + size_t(b) * size_t(tau) * 4 + 512;
+}
+
+extern "C" int tpf_sparse_zip_dense_c128(int64_t tau, int32_t b, const double* y_dense, const double* alpha,
+                                         const double* src, const int32_t* y_row_ptr, const int32_t* y_col,
+                                         const double* y_val, const double* S, int64_t s_node_stride,
+                                         int64_t s_case_stride, double v_flat_re, double v_flat_im, const double* v0,
+                                         double tol, int32_t max_iter, double* V, int64_t v_node_stride,
+                                         int64_t v_case_stride, int32_t* iters, double* resid, uint8_t* step_met,
+                                         int32_t* status, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace tpf;
+  if (tau < 0 || b < 1 || b > kZipDenseMaxB)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_dense_c128: need tau >= 0, 1 <= b <= 64");
+  if (!(tol > 0.0)) return set_error(TPF_ERR_INVALID, "tolerance must be positive");
+  if (max_iter < 1) return set_error(TPF_ERR_INVALID, "max_iterations must be >= 1");
+  if (tau == 0) return TPF_OK;
+  if (!y_dense || !alpha || !src || !y_row_ptr || !y_col || !y_val || !S || !V || !iters || !resid || !step_met ||
+      !status || !workspace)
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_dense_c128: null pointer");
+  if (workspace_bytes < tpf_sparse_zip_dense_workspace_bytes(tau, b))
+    return set_error(TPF_ERR_INVALID, "tpf_sparse_zip_dense_c128: workspace too small");
+  ZipLuArgs a;
+  memset(&a, 0, sizeof a);
+  a.tau = tau;
+  a.b = b;
+  a.nslot = b * b;
+  a.S = reinterpret_cast<const double2*>(S);
+  a.s_node = s_node_stride;
+  a.s_case = s_case_stride;
+  a.base = reinterpret_cast<const double2*>(y_dense);
+  a.alpha = alpha;
+  a.src = reinterpret_cast<const double2*>(src);
+  a.rp = y_row_ptr;
+  a.ci = y_col;
+  a.yv = reinterpret_cast<const double2*>(y_val);
+  a.v_flat = make_double2(v_flat_re, v_flat_im);
+  a.v0 = reinterpret_cast<const double2*>(v0);
+  a.tol2 = tol * tol;
+  a.max_iter = max_iter;
+  a.V = reinterpret_cast<double2*>(V);
+  a.v_node = v_node_stride;
+  a.v_case = v_case_stride;
+  a.iters = iters;
+  a.resid = resid;
+  a.met = step_met;
+  a.status = status;
+  a.F = static_cast<double2*>(workspace);
+  a.Z = a.F + size_t(b) * size_t(b) * size_t(tau);
+  int32_t* piv = reinterpret_cast<int32_t*>(a.Z + size_t(b) * size_t(tau));
+  const int threads = 128;
+  const int64_t blocks = (tau + threads - 1) / threads;
+  sparse_zip_dense_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(a, piv);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return set_cuda_error("launch(sparse_zip_dense_kernel)", err);
   return TPF_OK;
 }

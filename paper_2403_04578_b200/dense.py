@@ -388,12 +388,51 @@ def _solve_zip_chain(model, c, loads, opts, device, return_on_device):
     return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)
 
 
+def _solve_zip_dense(model, c, loads, opts, device, return_on_device):
+    """ZIP loads on small meshed networks (b <= 64) with the pivoting of the
+    reference's splu (fpi.py:119): one thread per case, dense LU of B with
+    row partial pivoting (``tpf_sparse_zip_dense_c128``)."""
+    dev = require_cuda(device)
+    v0 = _zip_start(c, opts, dev)
+    b = c.b
+    z = model.zip
+    alpha = np.concatenate([np.asarray(z.alpha_z, float), np.asarray(z.alpha_i, float), np.asarray(z.alpha_p, float)])
+    rp, ci, yv = host_csr(c)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    g = dict(yd=t(np.asarray(c.y_dd.toarray(), np.complex128)), alpha=t(alpha), src=t(np.asarray(c.src, np.complex128)),
+             rp=t(rp), ci=t(ci), yv=t(yv))
+    S = loads_to_device(loads.values, dev)
+    tau = S.shape[1]
+    V = torch.empty((b, tau), dtype=torch.complex128, device=dev)
+    iters = torch.empty(tau, dtype=torch.int32, device=dev)
+    resid = torch.empty(tau, dtype=torch.float64, device=dev)
+    met = torch.zeros(tau, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _capi.load()
+    chunk = max(1, min(tau, (1 << 30) // (16 * (b * b + b) + 4 * b)))  # scratch <= 1 GB
+    ws = torch.empty(int(lib.tpf_sparse_zip_dense_workspace_bytes(chunk, b)), dtype=torch.uint8, device=dev)
+    sn, sc = complex_strides(S)
+    v_flat = complex(abs(c.v_s))
+    for lo in range(0, tau, chunk):
+        hi = min(tau, lo + chunk)
+        _capi.call("tpf_sparse_zip_dense_c128", hi - lo, b, g["yd"].data_ptr(), g["alpha"].data_ptr(),
+                   g["src"].data_ptr(), g["rp"].data_ptr(), g["ci"].data_ptr(), g["yv"].data_ptr(),
+                   S.data_ptr() + 16 * lo * sc, sn, sc, v_flat.real, v_flat.imag, _ptr_or_null(v0),
+                   float(opts.tolerance), int(opts.max_iterations), V.data_ptr() + 16 * lo, tau, 1,
+                   iters.data_ptr() + 4 * lo, resid.data_ptr() + 8 * lo, met.data_ptr() + lo, status.data_ptr(),
+                   ws.data_ptr(), ws.numel(), stream_ptr(dev))
+    return _zip_outputs(V, iters, resid, met, status, opts, return_on_device)
+
+
 def _solve_zip_lu(model, c, loads, opts, device, return_on_device):
     """ZIP loads on meshed (or non-symmetric) networks: the reference's per-case
-    SuperLU route (dense.py:214-230 -> fpi.py:107-206) as one thread per case
-    factorizing B = Y_dd + diag(alpha_z s*) on a fixed minimum-degree fill
-    pattern without pivoting (``tpf_sparse_zip_lu_c128``).  A zero pivot raises
-    SingularSystemError, as splu does for a singular B."""
+    SuperLU route (dense.py:214-230 -> fpi.py:107-206).  Up to b = 64 with
+    splu's row pivoting (``_solve_zip_dense``); larger networks as one thread
+    per case factorizing B = Y_dd + diag(alpha_z s*) on a fixed minimum-degree
+    fill pattern without pivoting (``tpf_sparse_zip_lu_c128``).  A zero pivot
+    raises SingularSystemError, as splu does for a singular B."""
+    if c.b <= _capi.load().tpf_sparse_zip_dense_max_nodes():
+        return _solve_zip_dense(model, c, loads, opts, device, return_on_device)
     from .sparse import zip_lu_schedule
     dev = require_cuda(device)
     sch = zip_lu_schedule(c.y_dd)

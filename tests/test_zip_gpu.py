@@ -157,3 +157,30 @@ def test_zip_meshed_vs_oracle(n_buses, loops):
     assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
     assert abs(out.iterations - it) <= 1
     assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
+
+
+def test_zip_meshed_zero_diagonal_needs_pivoting():
+    """A meshed network whose B = Y_dd + diag(alpha_z s*) has an exactly zero
+    diagonal entry (series capacitor and reactor cancelling at bus 2, no
+    constant-impedance share there): nonsingular, so the reference's splu
+    pivots past it (fpi.py:119); the GPU route for small meshed networks
+    pivots too (tpf_sparse_zip_dense_c128) and matches the oracle."""
+    from paper_2403_04578_b200 import (Branch, LoadMatrix, NetworkModel, SlackSpec, SolveOptions, ZipCoefficients,
+                                       batch_solve_dense)
+    from paper_2403_04578_b200.sparse import tree_parents
+    branches = [Branch(from_bus=0, to_bus=1, r=0.0, x=0.1), Branch(from_bus=1, to_bus=2, r=0.0, x=-0.1),
+                Branch(from_bus=2, to_bus=3, r=0.0, x=0.1), Branch(from_bus=1, to_bus=3, r=0.01, x=0.05)]
+    z = ZipCoefficients(alpha_z=np.array([0.3, 0.0, 0.2]), alpha_i=np.array([0.3, 0.5, 0.3]),
+                        alpha_p=np.array([0.4, 0.5, 0.5]))
+    model = NetworkModel.from_branches(branches, 4, slack=SlackSpec(), zip_coeffs=z)
+    y = model.admittance.y_dd.toarray()
+    assert tree_parents(model.admittance.y_dd) is None and y[1, 1] == 0
+    rng = np.random.default_rng(3)
+    S = (rng.uniform(0.01, 0.2, (3, 64)) + 1j * rng.uniform(0.0, 0.05, (3, 64))).astype(np.complex128)
+    opts = SolveOptions(max_iterations=60)
+    out = batch_solve_dense(model, LoadMatrix(S), opts)
+    V, n, mask, res, it = orc.dense_zip_batch(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                              z.alpha_z, z.alpha_i, z.alpha_p, S, max_iter=60)
+    assert np.array_equal(out.converged_mask, mask)
+    assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
+    assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
