@@ -50,6 +50,19 @@ int tpf_version(void);
 /* Message of the last failed call on this thread ("" if none). */
 const char* tpf_last_error(void);
 
+/* ------------------------------------------------------ scenario loads --
+ * Device scenario generator (replaces synth.py:131-156 for batches that only
+ * exist on the device): per case j, node i: p = base[i] exp(sigma (sqrt(rho)
+ * common_j + sqrt(1 - rho) idio_ij)), power factor U[0.9, 1] lagging, then
+ * the batch scaled so max_j |sum_i s_ij| = scale_num (load_scale x margin).
+ * Draws: Philox4x32-10 keyed by `key`, counter (case_offset + j, node pair,
+ * stream): the same loads for a case whatever the launch or chunking.  S b x
+ * tau complex (any strides), device; workspace >= tpf_gen_loads_workspace_bytes(). */
+size_t tpf_gen_loads_workspace_bytes(void);
+int tpf_gen_loads_c128(int64_t tau, int32_t b, const double* base, double rho, double sigma, uint64_t key,
+                       int64_t case_offset, double scale_num, double* S, int64_t s_node_stride,
+                       int64_t s_case_stride, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- dense --
  * Replaces the hot loop of batch_solve_dense (dense.py:166-193) and its
  * per-iteration op chain _iterate_chunk (dense.py:114-126):

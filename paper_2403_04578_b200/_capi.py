@@ -27,6 +27,9 @@ _c_flt = ctypes.c_float
 SIGNATURES = {
     "tpf_version": (ctypes.c_int, []),
     "tpf_last_error": (ctypes.c_char_p, []),
+    "tpf_gen_loads_workspace_bytes": (_c_sz, []),
+    "tpf_gen_loads_c128": (ctypes.c_int, [_c_i64, _c_i32, _c_ptr, _c_dbl, _c_dbl, ctypes.c_uint64, _c_i64, _c_dbl,
+                                          _c_ptr, _c_i64, _c_i64, _c_ptr, _c_sz, _c_ptr]),
     "tpf_dense_max_nodes": (ctypes.c_int, []),
     "tpf_dense_setup_tree_c128": (ctypes.c_int, [_c_i32, _c_i32, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr,
                                                 _c_ptr]),
