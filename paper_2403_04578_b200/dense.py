@@ -13,11 +13,11 @@ Reference: pkg/src/tpflow/dense.py:129-205.  Same signature, same
 * ``numpy.linalg.LinAlgError`` from the inverse of a singular Y_dd
   (dense.py:151, uncaught in the reference too).
 
-Setup (dense.py:150-152): K = -inv(Y_dd) and W = K src by LAPACK on the host
-exactly as the reference (bitwise the reference's K) for b < DEVICE_SETUP_MIN_B
-or meshed networks; radial feeders from that size get K and W on the device
-(``tpf_dense_setup_tree_c128``: column j of K is one tree-LU solve, O(b^2) in
-all instead of the O(b^3) host inverse; equal to LAPACK's to rounding).  The
+Setup (dense.py:150-152): radial feeders get K = -inv(Y_dd) and W = K src on
+the device (``tpf_dense_setup_tree_c128``: column j of K is one tree-LU
+solve, O(b^2) in all instead of the O(b^3) host inverse; equal to LAPACK's
+to rounding); meshed networks (no zero-fill tree elimination) use LAPACK on
+the host exactly as the reference.  The
 iteration, the residual post-check and the converged mask run in libtpf.so.  ``workers`` is accepted and ignored (results are bitwise
 independent of any partitioning, like the reference's, test_dense.py:96-102).
 """
@@ -44,7 +44,10 @@ _KW_CACHE_MAX = 8
 _KW_LOCK = threading.Lock()
 
 
-DEVICE_SETUP_MIN_B = 256  # radial feeders from this size: K, W built on the device
+# radial feeders from this size: K, W built on the device (every radial feeder:
+# the host inverse also leaves OpenBLAS's workers spinning, which starves the
+# host threads staging a pageable caller array, tools/e2e_pageable2.py)
+DEVICE_SETUP_MIN_B = 1
 
 
 def device_kw(contract: ModelContract, device) -> tuple[torch.Tensor, torch.Tensor] | None:

@@ -37,11 +37,10 @@ def test_meshed_network_keeps_host_setup(golden):
     assert op.setup == "host"  # no zero-fill tree elimination: LAPACK, as the reference
 
 
-def test_auto_setup_threshold():
+def test_auto_setup_choice():
     from paper_2403_04578_b200 import DenseOperator
-    from paper_2403_04578_b200.dense import DEVICE_SETUP_MIN_B
-    assert DenseOperator(_model(101)).setup == "host"           # bitwise the reference's K
-    assert DenseOperator(_model(DEVICE_SETUP_MIN_B + 1)).setup == "device"
+    assert DenseOperator(_model(101)).setup == "device"          # radial feeders: on the device
+    assert DenseOperator(_model(101), setup="host").setup == "host"  # LAPACK, bitwise the reference's K
     with pytest.raises(ValueError):
         DenseOperator(_model(101), setup="gpu")
 
