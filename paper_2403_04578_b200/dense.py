@@ -55,7 +55,7 @@ def device_kw(contract: ModelContract, device) -> tuple[torch.Tensor, torch.Tens
     feeder (``tpf_dense_setup_tree_c128``), or None when Y_dd has no zero-fill
     tree elimination (meshed networks: host LAPACK).  Memoised with the host
     entries (same cache, so clearing it re-times the setup)."""
-    from .sparse import factorize_ydd, tree_levels
+    from .sparse import tree_direct
     dev = torch.device(device)
     key = contract.fingerprint() + b"|device:" + str(dev.index).encode()
     with _KW_LOCK:
@@ -63,7 +63,7 @@ def device_kw(contract: ModelContract, device) -> tuple[torch.Tensor, torch.Tens
         if hit is not None:
             _KW_CACHE.move_to_end(key)
             return hit
-    t = tree_levels(factorize_ydd(contract.y_dd, count=False), contract.src)
+    t = tree_direct(contract.y_dd, contract.src)
     if t is None:
         return None
     b = contract.b

@@ -411,6 +411,101 @@ def tree_levels(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
                         node_coef=np.ascontiguousarray(coef.T.ravel()), slots=int(j0[-1]))
 
 
+def tree_direct(y_dd, src: np.ndarray) -> TreeSchedule | None:
+    """The zero-fill tree elimination of a symmetric radial Y_dd computed
+    directly, without SuperLU (the dense setup, ``dense.device_kw``): BFS
+    levels from one root per component (a node next to the slack where there
+    is one), leaves first U_pp -= e_m g_m with e_m = Y[m, parent], g_m = e_m /
+    U_mm.  The same layout as ``tree_levels``; the values equal the SuperLU
+    factors' to rounding.  None unless Y_dd's graph is a forest with
+    symmetric values."""
+    y = y_dd if sparse.isspmatrix_csr(y_dd) and y_dd.dtype == complex else sparse.csr_matrix(y_dd, dtype=complex)
+    b = y.shape[0]
+    if b < 1 or y.shape[1] != b:
+        return None
+    if not y.has_sorted_indices:
+        y = y.sorted_indices()
+    rp, ci, yv = y.indptr.astype(np.int64), y.indices.astype(np.int64), y.data
+    rows = np.repeat(np.arange(b), np.diff(rp))
+    off = ci != rows
+    srcv = np.asarray(src)
+    # level-synchronous BFS (numpy), roots: the nodes next to the slack, then
+    # one node of any component still unreached
+    parent = np.full(b, -1, dtype=np.int64)
+    depth = np.full(b, -1, dtype=np.int64)
+    frontier = np.nonzero(srcv != 0)[0]
+    roots = list(frontier)
+    depth[frontier] = 0
+    while True:
+        while frontier.size:
+            lens = rp[frontier + 1] - rp[frontier]
+            total = int(lens.sum())
+            start = np.repeat(rp[frontier] - np.concatenate([[0], np.cumsum(lens)[:-1]]), lens)
+            k = start + np.arange(total)
+            nb, fr = ci[k], np.repeat(frontier, lens)
+            keep = (nb != fr) & (nb != parent[fr])
+            nb, fr = nb[keep], fr[keep]
+            if np.any(depth[nb] >= 0) or np.unique(nb).size != nb.size:
+                return None  # a cycle: not a forest
+            parent[nb] = fr
+            depth[nb] = depth[fr] + 1
+            frontier = nb
+        rest = np.nonzero(depth < 0)[0]
+        if rest.size == 0:
+            break
+        frontier = rest[:1]
+        roots.append(int(rest[0]))
+        depth[frontier] = 0
+    ncomp = len(roots)
+    if int(off.sum()) != 2 * (b - ncomp):
+        return None
+    levels = int(depth.max()) + 1
+    # e_m = Y[m, parent(m)], and Y[parent(m), m] must be the same value
+    e = np.zeros(b, dtype=complex)
+    fwd = off & (ci == parent[rows])
+    e[rows[fwd]] = yv[fwd]
+    bwd = off & (rows == parent[ci])
+    if int(fwd.sum()) != b - ncomp or not np.array_equal(yv[bwd], e[ci[bwd]]):
+        return None
+    # leaves first
+    U = y.diagonal().astype(complex)
+    g = np.zeros(b, dtype=complex)
+    for lv in range(levels - 1, 0, -1):
+        nodes = np.nonzero(depth == lv)[0]
+        g[nodes] = e[nodes] / U[nodes]
+        np.subtract.at(U, parent[nodes], e[nodes] * g[nodes])
+    if np.any(U == 0) or not np.all(np.isfinite(U)):
+        return None
+    uinv = 1.0 / U
+    # level order: roots, then each level's children contiguous by parent position
+    pos_in_level = np.zeros(b, dtype=np.int64)
+    level_nodes = [np.sort(np.nonzero(depth == 0)[0])]
+    pos_in_level[level_nodes[0]] = np.arange(level_nodes[0].size)
+    for lv in range(1, levels):
+        cand = np.nonzero(depth == lv)[0]
+        level_nodes.append(cand[np.lexsort((cand, pos_in_level[parent[cand]]))])
+        pos_in_level[level_nodes[-1]] = np.arange(cand.size)
+    order = np.concatenate(level_nodes)
+    m_of = np.empty(b, dtype=np.int64)
+    m_of[order] = np.arange(b)
+    sizes = np.array([x.size for x in level_nodes])
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    slots_per = -(-sizes // TREE_THREADS)
+    j0 = np.concatenate([[0], np.cumsum(slots_per)])
+    pm = np.where(parent[order] >= 0, m_of[np.maximum(parent[order], 0)], -1)
+    cnt = np.zeros(b, dtype=np.int64)
+    kids = pm >= 0
+    np.add.at(cnt, pm[kids], 1)
+    first_seen = np.full(b, b, dtype=np.int64)
+    np.minimum.at(first_seen, pm[kids], np.nonzero(kids)[0])
+    first = np.where(cnt > 0, first_seen, 0)
+    info = np.stack([order, pm, first, cnt], axis=1).astype(np.int32)
+    coef = np.stack([e[order], g[order], uinv[order], srcv[order].astype(complex)], axis=1)
+    return TreeSchedule(b=b, levels=levels, level_info=np.concatenate([offs, j0]).astype(np.int32),
+                        node_info=np.ascontiguousarray(info.ravel()),
+                        node_coef=np.ascontiguousarray(coef.T.ravel()), slots=int(j0[-1]))
+
+
 def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
     """``tree_levels`` within the level kernel's limits (tpf_sparse_tree_fpi_c128), else None."""
     if f.b > TREE_MAX_NODES:
