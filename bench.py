@@ -269,6 +269,9 @@ def run_ours():
         if os.environ.get("TPF_BENCH_ONE_GPU") == "1":
             dist.init_process_group("gloo")
         else:
+            # NCCL's init log on stderr (communicator size per rank: the driver's nranks check)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
