@@ -291,19 +291,34 @@ __global__ void __launch_bounds__(32 * kTailWarps) tail_kernel(LargeArgs a, int 
       asm volatile("cp.async.commit_group;" ::: "memory");
   }
   double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+  // kTailUnroll k-steps per pass (nks is a multiple of KSTEPS = 4): their
+  // operands read together, then the DMMA chains; slabs of the next pass
+  // refill the stages the previous pass read
+  constexpr int kTailUnroll = KSTEPS;
 #pragma unroll 1
-  for (int ks = 0; ks < nks; ++ks) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kTailDepth - 2) : "memory");
-    const int st = ks % kTailDepth;
-    const double2 af = rg[st][0][lane], bf = rg[st][1][lane];  // this lane's own copies
-    if (ks + kTailDepth - 1 < nks)
-      issue(ks + kTailDepth - 1);
-    else
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    const double as = af.x + af.y, bs = bf.x + bf.y;
-    dmma884(p1[0], p1[1], af.x, bf.x);
-    dmma884(p2[0], p2[1], af.y, bf.y);
-    dmma884(p3[0], p3[1], as, bs);
+  for (int ks0 = 0; ks0 < nks; ks0 += kTailUnroll) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kTailDepth - 1 - kTailUnroll) : "memory");
+    double2 af[kTailUnroll], bf[kTailUnroll];
+#pragma unroll
+    for (int u = 0; u < kTailUnroll; ++u) {  // this lane's own copies
+      const int st = (ks0 + u) % kTailDepth;
+      af[u] = rg[st][0][lane];
+      bf[u] = rg[st][1][lane];
+    }
+#pragma unroll
+    for (int u = 0; u < kTailUnroll; ++u) {
+      if (ks0 + kTailDepth - 1 + u < nks)
+        issue(ks0 + kTailDepth - 1 + u);
+      else
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < kTailUnroll; ++u) {
+      const double as = af[u].x + af[u].y, bs = bf[u].x + bf[u].y;
+      dmma884(p1[0], p1[1], af[u].x, bf[u].x);
+      dmma884(p2[0], p2[1], af[u].y, bf[u].y);
+      dmma884(p3[0], p3[1], as, bs);
+    }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   // epilogue of gemm_kernel for one fragment
