@@ -131,7 +131,10 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
     def kids_of(m):
         return range(first[m], first[m] + cnt[m])
 
-    best = None
+    # per cut depth D: subtrees packed onto warps (largest first onto the least
+    # loaded); the Hu schedule is built only for the cuts whose lower bound
+    # max_w max(ceil(n_w / 32), height_w) could still win
+    cands = []
     for D in range(1, L):
         root_of = np.arange(b)
         for _ in range(L):
@@ -139,6 +142,8 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
         roots = np.arange(offs[D], offs[D + 1])
         sub = depth >= D
         size = np.bincount(root_of[sub] - offs[D], minlength=roots.size)
+        height = np.zeros(roots.size, dtype=np.int64)
+        np.maximum.at(height, root_of[sub] - offs[D], depth[sub] - D + 1)
         owner = np.empty(roots.size, dtype=np.int64)
         load = np.zeros(W, dtype=np.int64)
         for r in np.argsort(-size, kind="stable"):
@@ -147,12 +152,22 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
             load[w] += size[r]
         warp_of = np.full(b, -1, dtype=np.int64)
         warp_of[sub] = owner[root_of[sub] - offs[D]]
+        hw = np.zeros(W, dtype=np.int64)
+        np.maximum.at(hw, owner, height)
+        lb = max(int(np.max(np.maximum(-(-load // 32), hw))), 1)
+        nt = int((-(-sizes[:D] // 32)).sum())
+        pen = 12 * W * nt * 32 * 3 * 16 > 48 * 1024
+        cands.append(((lb > SUB_MAX_NS, lb + nt + pen, nt), D, nt, pen, warp_of))
+    cands.sort(key=lambda x: x[0])
+    best = None
+    for lbkey, D, nt, pen, warp_of in cands:
+        if best is not None and (lbkey > best[0] or (lbkey == best[0] and D > best[1])):
+            continue  # this cut cannot beat the best schedule found
         sslots = [_superslots(np.nonzero(warp_of == w)[0], kids_of, pm, depth, width=32) for w in range(W)]
         ns = max(max(len(x) for x in sslots), 1)
-        nt = int((-(-sizes[:D] // 32)).sum())
         rmax = int(max(-(-np.count_nonzero((warp_of == w) & (depth == D)) // 32) for w in range(W)))
-        key = (ns > SUB_MAX_NS, ns + nt + (12 * W * nt * 32 * 3 * 16 > 48 * 1024), nt)
-        if best is None or key < best[0]:
+        key = (ns > SUB_MAX_NS, ns + nt + pen, nt)
+        if best is None or key < best[0] or (key == best[0] and D < best[1]):
             best = (key, D, ns, nt, max(rmax, 1), warp_of, sslots)
     (_, D, NS, NT, RMAX, warp_of, sslots) = best
     if NS > SUB_MAX_NS:
@@ -169,101 +184,103 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
     rho = np.full(b, -1, dtype=np.int64)     # subtree roots: Proot index
     m_at = np.full(P, -1, dtype=np.int64)
     slotinfo = np.zeros((W, NS), dtype=np.int64)
+    rlen = np.diff(rp).astype(np.int64)
     ny = 0
     for w in range(W):
-        nroot = 0
-        yk = 0
-        slot_of = {}
-        for k, nodes in enumerate(sslots[w]):
-            for i, m in enumerate(nodes):
-                p = (w * NSL + k) * 32 + i
-                pos[m] = p
-                m_at[p] = m
-                slot_of[m] = k
-                if depth[m] == D:
-                    rho[m] = (w * RMAX + nroot // 32) * 32 + nroot % 32
-                    nroot += 1
-            km = max(int(cnt[m]) for m in nodes)
-            ys = 0
-            if km > 0:  # some internal node: z / U_mm kept in TMEM (leaf-only slots recompute it)
-                yk += 1
-                ys = yk
-            rwm = max(int(np.diff(rp)[orig[m]]) for m in nodes)  # widest residual row of the slot
-            slotinfo[w, k] = km | (ys << 5) | (rwm << 10)
-        for k in range(len(sslots[w]) - 1):  # slots k, k+1 independent: swept as a pair
-            if not any(slot_of.get(int(pm[m]), -1) == k + 1 for m in sslots[w][k]):
-                slotinfo[w, k] |= 1 << 4
-        ny = max(ny, yk)
+        if not sslots[w]:
+            continue
+        nodes_w = np.concatenate([np.asarray(x, dtype=np.int64) for x in sslots[w]])
+        slot_w = np.repeat(np.arange(len(sslots[w])), [len(x) for x in sslots[w]])
+        lane_w = np.concatenate([np.arange(len(x)) for x in sslots[w]])
+        pw = (w * NSL + slot_w) * 32 + lane_w
+        pos[nodes_w] = pw
+        m_at[pw] = nodes_w
+        rt = nodes_w[depth[nodes_w] == D]  # subtree roots, in slot order
+        rho[rt] = (w * RMAX + np.arange(rt.size) // 32) * 32 + np.arange(rt.size) % 32
+        km = np.zeros(len(sslots[w]), dtype=np.int64)
+        np.maximum.at(km, slot_w, cnt[nodes_w])
+        rwm = np.zeros(len(sslots[w]), dtype=np.int64)
+        np.maximum.at(rwm, slot_w, rlen[orig[nodes_w]])  # widest residual row of the slot
+        has_y = km > 0  # some internal node: z / U_mm kept in TMEM (leaf-only slots recompute it)
+        ys = np.where(has_y, np.cumsum(has_y), 0)
+        slotinfo[w, :len(sslots[w])] = km | (ys << 5) | (rwm << 10)
+        # slots k, k+1 independent (no node of k has its parent in k + 1): swept as a pair
+        par = pm[nodes_w]
+        dep = (par >= 0) & (pos[np.maximum(par, 0)] // 32 == (w * NSL + slot_w + 1)) & (depth[np.maximum(par, 0)] >= D)
+        blocked = np.zeros(len(sslots[w]), dtype=bool)
+        blocked[slot_w[dep]] = True
+        pairable = ~blocked[:-1]
+        slotinfo[w, :len(sslots[w]) - 1] |= np.where(pairable, 1 << 4, 0)
+        ny = max(ny, int(has_y.sum()))
     if 8 * NS + 4 * ny > SUB_TMEM_COLS or ny >= 31:
         return None
     tj = 0
     for d in range(D - 1, -1, -1):  # top: depth D-1 first (up order), index q = (slot - NS) * 32 + lane
-        nodes = np.arange(offs[d], offs[d + 1])
-        for k, m in enumerate(nodes):
-            qidx[m] = (tj + k // 32) * 32 + k % 32
-        tj += -(-nodes.size // 32)
+        k = np.arange(offs[d + 1] - offs[d])
+        qidx[offs[d]:offs[d + 1]] = (tj + k // 32) * 32 + k % 32
+        tj += -(-k.size // 32)
     assert tj == NT
+    top = np.arange(offs[D])
     for w in range(W):
-        for m in range(offs[D]):
-            m_at[(w * NSL + NS) * 32 + qidx[m]] = m
+        m_at[(w * NSL + NS) * 32 + qidx[top]] = top
 
     # X index space of the kernel: positions [0, xcap), Proot parity 0 at
     # [xcap, xcap + RR), parity 1 at [xcap + RR, xcap + 2 RR) (the kernel adds
     # RR on odd iterations), a zero entry at xcap + 2 RR.  Child lists and
     # parents are X indices; a top node's copy in warp w points into w's copy.
     def xidx(c, w):
-        if depth[c] < D:
-            return (w * NSL + NS) * 32 + int(qidx[c])
-        if depth[c] == D:
-            return xcap + int(rho[c])
-        return int(pos[c])
+        return np.where(depth[c] < D, (w * NSL + NS) * 32 + qidx[c],
+                        np.where(depth[c] == D, xcap + rho[c], pos[c]))
 
-    kid_list: list[int] = []
-    kid_first_pos = np.zeros(P, dtype=np.int64)
-    seen = {}
-    for p in range(P):
-        m = m_at[p]
-        if m < 0 or cnt[m] == 0:
-            continue
-        w = p // (NSL * 32)
-        key = (m, w if depth[m] < D else -1)
-        if key not in seen:
-            seen[key] = len(kid_list)
-            kid_list.extend(xidx(c, w) for c in kids_of(m))
-        kid_first_pos[p] = seen[key]
+    pp = np.arange(P)
+    mp = m_at
+    valid = mp >= 0
+    mv = np.maximum(mp, 0)
+    wp = pp // (NSL * 32)
+    nk = np.where(valid, cnt[mv], 0)
+    # one child list per position, in position order (each top node once per warp)
+    kid_first_pos = np.concatenate([[0], np.cumsum(nk)[:-1]])
+    tot = int(nk.sum())
+    owner = np.repeat(pp, nk)
+    child = np.repeat(first[mv], nk) + (np.arange(tot) - np.repeat(kid_first_pos, nk))
+    kid_list = xidx(child, wp[owner]) if tot else np.zeros(0, dtype=np.int64)
+    kid_first_pos = np.where(nk > 0, kid_first_pos, 0)
     # SUB_KMAX padding entries: the kernel's branch-free child sum reads up to the
     # slot's largest child count from every lane's list start
-    kids = np.asarray(kid_list + [xcap + 2 * RR] * SUB_KMAX, dtype=np.uint16)
-    if len(kid_list) + SUB_KMAX >= 0xFFFF:
+    if tot + SUB_KMAX >= 0xFFFF:
         return None
-    rlen_node = np.diff(rp)[orig]
-    RW = int(rlen_node.max(initial=1))
+    kids = np.concatenate([kid_list, np.full(SUB_KMAX, xcap + 2 * RR)]).astype(np.uint16)
+    RW = int(rlen[orig].max(initial=1))
     if RW > SUB_RWMAX:
         return None
+
+    def pack(lo16, hi16):
+        v = (np.asarray(lo16, dtype=np.int64) & 0xFFFF) | ((np.asarray(hi16, dtype=np.int64) & 0xFFFF) << 16)
+        return np.where(v >= (1 << 31), v - (1 << 32), v)
+
+    pmv = pm[mv]
+    pc = np.where(pmv < 0, 0xFFFF, np.where(depth[np.maximum(pmv, 0)] < D, xidx(np.maximum(pmv, 0), wp),
+                                             pos[np.maximum(pmv, 0)]))
+    root = np.where(depth[mv] == D, rho[mv] + 1, 0)
     pinfo = np.zeros((P, 2), dtype=np.int64)
+    pinfo[:, 0] = np.where(valid, pack(pc, kid_first_pos), pack(0xFFFF, 0))
+    pinfo[:, 1] = np.where(valid, pack(cnt[mv] | (root << 4), orig[mv]), pack(0, 0xFFFF))
     coef = np.zeros((3, P), dtype=np.complex128)
+    coef[:, valid] = coef4[1:4, mp[valid]]
     # ELL rows blocked by slot: entry r of position p at [p // 32, r, p % 32];
-    # padding points at X's zero entry with value 0
+    # padding points at X's zero entry with value 0.  Residual rows: subtree
+    # nodes and warp 0's top copies.
     ell_col = np.full((P // 32, RW, 32), xcap + 2 * RR, dtype=np.int32)
     ell_val = np.zeros((P // 32, RW, 32), dtype=np.complex128)
-    for p in range(P):
-        m = m_at[p]
-        if m < 0:
-            pinfo[p] = (_pack(0xFFFF, 0), _pack(0, 0xFFFF))
-            continue
-        w = p // (NSL * 32)
-        pc = 0xFFFF if pm[m] < 0 else xidx(pm[m], w) if depth[pm[m]] < D else int(pos[pm[m]])
-        root = int(rho[m]) + 1 if (depth[m] == D) else 0
-        pinfo[p, 0] = _pack(pc, int(kid_first_pos[p]))
-        pinfo[p, 1] = _pack(int(cnt[m]) | (root << 4), int(orig[m]))
-        coef[0, p] = coef4[1, m]
-        coef[1, p] = coef4[2, m]
-        coef[2, p] = coef4[3, m]
-        if depth[m] >= D or w == 0:  # residual rows: subtree nodes and warp 0's top copies
-            i = int(orig[m])
-            lo, hi = int(rp[i]), int(rp[i + 1])
-            ell_col[p // 32, :hi - lo, p % 32] = ci[lo:hi]
-            ell_val[p // 32, :hi - lo, p % 32] = yv[lo:hi]
+    rowp = pp[valid & ((depth[mv] >= D) | (wp == 0))]
+    ri = orig[mp[rowp]]
+    ln = rlen[ri]
+    tot = int(ln.sum())
+    rpos = np.repeat(rowp, ln)
+    rr = np.arange(tot) - np.repeat(np.concatenate([[0], np.cumsum(ln)[:-1]]), ln)
+    src_k = np.repeat(rp[ri].astype(np.int64), ln) + rr
+    ell_col[rpos // 32, rr, rpos % 32] = ci[src_k]
+    ell_val[rpos // 32, rr, rpos % 32] = yv[src_k]
     top_priv = 3 * W * NT * 32 * 16 + 3 * NT * 32 * 16
     smem = (xcap + 2 * RR + 1) * 16 + top_priv + P * 8 + W * NS * 4 + kids.size * 2 + 1024
     smem = (smem + 15) // 16 * 16
