@@ -8,10 +8,11 @@
 // is scaled so the worst aggregate |sum_i s_ij| is scale_num (load_scale x
 // the solvability margin).  The draws come from a Philox4x32-10 counter
 // generator keyed by the scenario's seed, counter (case, node pair, stream), so any
-// case's loads are the same whatever the launch geometry or chunking, and the
-// scaling pass regenerates instead of re-reading: pass 1 finds the worst
-// aggregate (atomicMax on the bits of non-negative doubles), pass 2 writes
-// the scaled loads (one 16-byte store per element, coalesced over cases).
+// case's loads are the same whatever the launch geometry or chunking.  Pass 1
+// writes the unscaled loads (one 16-byte store per element, coalesced over
+// cases) and the worst aggregate (atomicMax on the bits of non-negative
+// doubles); pass 2 scales them in place (HBM-bound, cheaper than drawing
+// them again).
 // Statistically the reference's model, not bit-identical to numpy's PCG64.
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -51,11 +52,8 @@ struct GenArgs {
   unsigned long long* worst;  // bits of the worst aggregate
 };
 
-template <bool WRITE>
 __global__ void __launch_bounds__(256) gen_loads_kernel(const GenArgs a) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  double f = 1.0;
-  if (WRITE) f = a.scale_num / __longlong_as_double(*a.worst);
   double sr = 0.0, si = 0.0;
   if (j < a.tau) {
     const uint32_t cj = uint32_t(a.case_offset + j);
@@ -77,19 +75,26 @@ __global__ void __launch_bounds__(256) gen_loads_kernel(const GenArgs a) {
         const double pf = 0.9 + 0.1 * (h == 0 ? u01(wp.x, wp.y) : u01(wp.z, wp.w));
         const double p = __ldg(a.base + i) * exp(a.sigma * (a.a_common * common + a.a_idio * idio));
         const double q = p * (sqrt((1.0 - pf) * (1.0 + pf)) / pf);
-        if (WRITE) {
-          a.S[int64_t(i) * a.s_node + j * a.s_case] = make_double2(p * f, q * f);
-        } else {
-          sr += p;
-          si += q;
-        }
+        a.S[int64_t(i) * a.s_node + j * a.s_case] = make_double2(p, q);
+        sr += p;
+        si += q;
       }
     }
   }
-  if (!WRITE) {
-    double m = j < a.tau ? hypot(sr, si) : 0.0;
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(a.worst, __double_as_longlong(m));
+  double m = j < a.tau ? hypot(sr, si) : 0.0;
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(a.worst, __double_as_longlong(m));
+}
+
+// s *= scale_num / worst (the reference's `s *= load_scale * margin / worst`)
+__global__ void __launch_bounds__(256) scale_loads_kernel(const GenArgs a) {
+  const double f = a.scale_num / __longlong_as_double(*a.worst);
+  const int64_t n = a.tau * a.b;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / a.tau, j = e - i * a.tau;
+    double2* p = a.S + i * a.s_node + j * a.s_case;
+    const double2 v = *p;
+    *p = make_double2(v.x * f, v.y * f);
   }
 }
 
@@ -128,8 +133,11 @@ extern "C" int tpf_gen_loads_c128(int64_t tau, int32_t b, const double* base, do
   cudaError_t err = cudaMemsetAsync(workspace, 0, 8, st);
   if (err != cudaSuccess) return set_cuda_error("cudaMemsetAsync(worst)", err);
   const unsigned blocks = unsigned((tau + 255) / 256);
-  gen_loads_kernel<false><<<blocks, 256, 0, st>>>(a);
-  gen_loads_kernel<true><<<blocks, 256, 0, st>>>(a);
+  gen_loads_kernel<<<blocks, 256, 0, st>>>(a);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  scale_loads_kernel<<<unsigned(sms) * 8, 256, 0, st>>>(a);
   err = cudaGetLastError();
   return err == cudaSuccess ? TPF_OK : set_cuda_error("launch(gen_loads_kernel)", err);
 }
