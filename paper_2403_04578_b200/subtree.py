@@ -32,6 +32,7 @@ child order), so both kernels give the same bits.
 
 from __future__ import annotations
 
+import heapq
 from dataclasses import dataclass
 
 import numpy as np
@@ -92,7 +93,6 @@ def _superslots(nodes: np.ndarray, kids_of, parent, prio, width: int = 64) -> li
     independent nodes: at each step the ready nodes (all children in earlier
     super-slots) farthest from their root go first (Hu's rule, optimal for
     unit tasks on an in-forest)."""
-    import heapq
     nodes = [int(m) for m in nodes]
     member = set(nodes)
     left = {m: len(kids_of(m)) for m in nodes}
@@ -145,11 +145,12 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
         height = np.zeros(roots.size, dtype=np.int64)
         np.maximum.at(height, root_of[sub] - offs[D], depth[sub] - D + 1)
         owner = np.empty(roots.size, dtype=np.int64)
-        load = np.zeros(W, dtype=np.int64)
-        for r in np.argsort(-size, kind="stable"):
-            w = int(np.argmin(load))
+        heap = [(0, w) for w in range(W)]  # (load, warp): the least loaded, lowest index first
+        for r in np.argsort(-size, kind="stable").tolist():
+            ld, w = heapq.heappop(heap)
             owner[r] = w
-            load[w] += size[r]
+            heapq.heappush(heap, (ld + int(size[r]), w))
+        load = np.bincount(owner, weights=size, minlength=W).astype(np.int64)
         warp_of = np.full(b, -1, dtype=np.int64)
         warp_of[sub] = owner[root_of[sub] - offs[D]]
         hw = np.zeros(W, dtype=np.int64)
