@@ -506,12 +506,21 @@ def tree_direct(y_dd, src: np.ndarray) -> TreeSchedule | None:
                         node_coef=np.ascontiguousarray(coef.T.ravel()), slots=int(j0[-1]))
 
 
-def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
-    """``tree_levels`` within the level kernel's limits (tpf_sparse_tree_fpi_c128), else None."""
-    if f.b > TREE_MAX_NODES:
-        return None
-    t = tree_levels(f, src)
-    if t is None:
+def radial_levels(contract, count: bool = True) -> TreeSchedule | None:
+    """The batch factorization of a radial feeder: ``tree_direct`` (counted
+    by ``factorization_count`` like a SuperLU factorization), or None for
+    meshed networks (SuperLU, ``factorize_ydd``)."""
+    global _factorizations
+    t = tree_direct(contract.y_dd, contract.src)
+    if t is not None and count:
+        with _lock:
+            _factorizations += 1
+    return t
+
+
+def tree_limits(t: TreeSchedule | None) -> TreeSchedule | None:
+    """``t`` if it is within the level kernel's limits (tpf_sparse_tree_fpi_c128), else None."""
+    if t is None or t.b > TREE_MAX_NODES:
         return None
     offs = t.level_info[:t.levels + 1]
     sizes = np.diff(offs)
@@ -519,6 +528,11 @@ def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
             or sizes[0] > TREE_MAX_ROOTS:
         return None
     return t
+
+
+def tree_schedule(f: TreeLU, src: np.ndarray) -> TreeSchedule | None:
+    """``tree_levels`` within the level kernel's limits (tpf_sparse_tree_fpi_c128), else None."""
+    return tree_limits(tree_levels(f, src)) if f.b <= TREE_MAX_NODES else None
 
 
 def tree_ell(t: TreeSchedule, contract) -> tuple[int, np.ndarray, np.ndarray] | None:
@@ -588,24 +602,24 @@ class SparseOperator:
         self.contract = ModelContract.of(model)
         self.dtype = engine_dtype(dtype)
         c64 = self.dtype == np.complex64
-        self.lu = factorize_ydd(self.contract.y_dd)
         d = self.device
         def t(a):  # never hand a 0-element (null) buffer to the C ABI
             a = np.ascontiguousarray(a)
             if a.size == 0:
                 a = np.zeros(1, dtype=a.dtype)
             return torch.from_numpy(a).to(d)
-        f = self.lu
-        cx = (lambda a: np.asarray(a).astype(np.complex64)) if c64 else (lambda a: a)
-        self.dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(cx(f.l_val)), u_ptr=t(f.u_ptr),
-                        u_col=t(f.u_col), u_val=t(cx(f.u_val)), u_diag_inv=t(cx(f.u_diag_inv)),
-                        perm=t(f.perm), src=t(cx(self.contract.src)))
+        self._t = t
         use_tree = use_tree and not c64 and kernel != "general"  # the c64 twin is the general CSR kernel
+        # one factorization: the tree elimination of a radial feeder, else SuperLU
+        levels = radial_levels(self.contract) if use_tree else None
+        self.lu = None if levels is not None else factorize_ydd(self.contract.y_dd)
+        self._dev = None
         self.v_flat = complex(abs(self.contract.v_s))
         self._ws = None
         self._csr = None
         self._chunk = None
-        levels = tree_levels(f, self.contract.src) if use_tree else None
+        if levels is None and use_tree:
+            levels = tree_levels(self.lu, self.contract.src)
         self.tree = None
         self.sub = None
         if levels is not None and kernel in ("auto", "subtree") and \
@@ -621,7 +635,7 @@ class SparseOperator:
         if levels is not None:
             # the level kernel: radial feeders without a subtree schedule, and
             # the fallback for S / V layouts the subtree kernel's TMA cannot move
-            self.tree = tree_schedule(f, self.contract.src)
+            self.tree = tree_limits(levels)
         if self.tree is not None:
             self.tree_dev = dict(level_info=t(self.tree.level_info), node_info=t(self.tree.node_info),
                                  node_coef=t(self.tree.node_coef))
@@ -632,6 +646,21 @@ class SparseOperator:
     @property
     def b(self) -> int:
         return self.contract.b
+
+    @property
+    def dev(self) -> dict:
+        """The general CSR kernel's LU arrays on the device (built on first use:
+        radial feeders factor as a tree and need them only for layouts the
+        tree kernels cannot take)."""
+        if self._dev is None:
+            if self.lu is None:
+                self.lu = factorize_ydd(self.contract.y_dd, count=False)  # the same matrix, factored again
+            f, t = self.lu, self._t
+            cx = (lambda a: np.asarray(a).astype(np.complex64)) if self.dtype == np.complex64 else (lambda a: a)
+            self._dev = dict(l_ptr=t(f.l_ptr), l_col=t(f.l_col), l_val=t(cx(f.l_val)), u_ptr=t(f.u_ptr),
+                             u_col=t(f.u_col), u_val=t(cx(f.u_val)), u_diag_inv=t(cx(f.u_diag_inv)),
+                             perm=t(f.perm), src=t(cx(self.contract.src)))
+        return self._dev
 
     @property
     def kernel(self) -> str:
@@ -794,18 +823,24 @@ def _nonempty(a):
 
 
 def _batch_lu(contract, use_tree: bool):
-    """The batch's LU of Y_dd and tree schedule: one real SuperLU
-    factorization per batch, exactly as the reference (sparse.py:186), so
-    ``factorization_count`` counts factorizations that ran.  Nothing is
-    memoised: the host setup (C3: ~30 ms) is part of every call, as it is of
-    the reference's."""
-    f = factorize_ydd(contract.y_dd)
-    levels = tree_levels(f, contract.src) if use_tree else None
+    """The batch's factorization of Y_dd and its kernel schedule, once per
+    batch like the reference's (sparse.py:186), so ``factorization_count``
+    counts factorizations that ran: radial feeders by their tree elimination
+    (``tree_direct``, no fill), meshed networks by SuperLU.  Nothing is
+    memoised: the host setup is part of every call, as it is of the
+    reference's."""
+    levels = radial_levels(contract) if use_tree else None  # a radial feeder: its tree elimination
+    f = None
+    if levels is None:
+        f = factorize_ydd(contract.y_dd)
+        levels = tree_levels(f, contract.src) if use_tree else None
     sub = None
     if levels is not None and contract.b >= SUBTREE_MIN_B:
         from .subtree import subtree_schedule
         sub = subtree_schedule(levels, *host_csr(contract))
-    tree = tree_schedule(f, contract.src) if levels is not None and sub is None else None
+    tree = tree_limits(levels) if levels is not None and sub is None else None
+    if f is None and sub is None and tree is None:
+        f = factorize_ydd(contract.y_dd, count=False)  # the general kernel's LU of the same matrix
     return f, tree, sub
 
 
@@ -821,8 +856,8 @@ def _solve_host_pipeline(model, loads: LoadMatrix, opts: SolveOptions, devs, chu
     resid = host_empty((tau,), np.float64)
     mask = host_empty((tau,), np.uint8)
     v_flat = complex(abs(c.v_s))
-    arrs = [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val, f.u_diag_inv,
-                                    f.perm)]
+    arrs = [] if f is None else [_nonempty(x) for x in (f.l_ptr, f.l_col, f.l_val, f.u_ptr, f.u_col, f.u_val,
+                                                        f.u_diag_inv, f.perm)]
     lib = _capi.load()
 
     def call(dev, lo, hi, slot):
