@@ -13,6 +13,7 @@
 // summary kernel and copy.  Pageable host buffers are page-locked in place for
 // the duration of the call (cudaHostRegister) so every copy is a DMA.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -333,6 +334,20 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     if (at < tau) bnd.push_back(tau);
   }
   const int64_t nchunks = int64_t(bnd.size()) - 1;
+  // TPF_PIPE_TRACE=1 (diagnostics only): per-chunk timeline on stderr
+  static const bool trace = [] {
+    const char* e = getenv("TPF_PIPE_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark(setup);
   int rc = TPF_OK;
   for (int64_t c = 0; c < nchunks && rc == TPF_OK; ++c) {
     const int k = int(c & 1);
@@ -359,6 +374,7 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
              "H2D(S chunk)");
     }
     cudaEventRecord(ss.in_done[k], sin);
+    mark(sin);
     cudaStreamWaitEvent(scomp, ss.in_done[k], 0);
     if (c >= 2) cudaStreamWaitEvent(scomp, ss.out_done[k], 0);
     rc = solver.solve_resid(n, d_S[k].as<double>(), dsn_S, dsc_S, d_V[k].as<double>(), dsn_V, dsc_V,
@@ -366,9 +382,11 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
                             d_src.as<double>(), d_res.as<double>() + lo, scomp);
     if (rc == TPF_OK) {
       cudaEventRecord(ss.comp_done[k], scomp);
+      mark(scomp);
       cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
       TPF_CK_LOOP(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
       cudaEventRecord(ss.out_done[k], sout);
+      mark(sout);
       continue;
     }
     if (rc > 0) break;  // a real error from the fused solver
@@ -380,9 +398,11 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
                            d_res.as<double>() + lo, scomp);
     if (rc != TPF_OK) break;
     cudaEventRecord(ss.comp_done[k], scomp);
+    mark(scomp);
     cudaStreamWaitEvent(sout, ss.comp_done[k], 0);
     TPF_CK_LOOP(copy_chunk(false, LV, V, d_V[k].as<double>(), b, lo, n, chunk, sout), "D2H(V chunk)");
     cudaEventRecord(ss.out_done[k], sout);
+    mark(sout);
   }
   if (rc == TPF_OK) {
     rc = tpf_batch_summary(tau, d_it.as<int32_t>(), d_res.as<double>(), residual_tol, d_mask.as<uint8_t>(),
@@ -399,7 +419,18 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     if (summary) cudaMemcpyAsync(summary, d_sum.p, 8, cudaMemcpyDeviceToHost, sout);
     cudaEventDestroy(fin);
   }
+  mark(sout);
   cudaError_t e1 = cudaStreamSynchronize(sin), e2 = cudaStreamSynchronize(scomp), e3 = cudaStreamSynchronize(sout);
+  if (trace && !tev.empty()) {  // in / compute / out completion times of each chunk, ms after the setup mark
+    fprintf(stderr, "[tpf pipe] %lld chunks, chunk %lld:", (long long)nchunks, (long long)chunk);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      fprintf(stderr, " %.2f", ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   cudaEventDestroy(setup_done);
   if (rc != TPF_OK) return rc;
   if (e1 != cudaSuccess) return set_cuda_error("pipeline(in)", e1);
