@@ -796,8 +796,8 @@ def run_e2e(model, loads, method, dev, bsd, bss, LoadMatrix, world, dtype=None, 
     return dict(value=world * tau / t, unit=UNIT, h2d_bytes_per_step=h2d, cases_per_step=tau,
                 d2h_bytes_per_step=d2h,
                 ms_per_step=t * 1e3, api=f"paper_2403_04578_b200.batch_solve_{method}(model, LoadMatrix)",
-                setup="included every call: K = -inv(Y_dd), W (dense; tree-LU solves on the device for radial "
-                      "feeders, host LAPACK otherwise) / the SuperLU factorization (sparse)",
+                setup="included every call: K = -inv(Y_dd), W (dense; tree-LU solves on the device for radial feeders with b >= 64, "
+                      "host LAPACK otherwise) / the factorization of Y_dd (sparse)",
                 iterations=int(out.iterations),
                 pageable=dict(value=world * tau / tp, ms_per_step=tp * 1e3,
                               how="the same call on an ordinary (pageable) numpy array"),

@@ -272,7 +272,7 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
   if (!LS.ok(b, tau, s_node, s_case)) return set_error(TPF_ERR_INVALID, "host S must be node-major or case-major");
   if (!LV.ok(b, tau, v_node, v_case)) return set_error(TPF_ERR_INVALID, "host V must be node-major or case-major");
   HostPin pin_s, pin_v, pin_i, pin_r, pin_m;
-  const bool stage_s = !host_pinned(S) && tau > chunk;  // one-chunk calls: registration is as cheap
+  const bool stage_s = !host_pinned(S);  // pageable loads: staged (registering costs ms even for one chunk)
   if (stage_s) {
     TPF_CK(g_staging.ensure(size_t(2) * size_t(chunk) * b * 16), "cudaHostAlloc(staging)");
   } else {

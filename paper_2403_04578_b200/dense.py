@@ -44,10 +44,12 @@ _KW_CACHE_MAX = 8
 _KW_LOCK = threading.Lock()
 
 
-# radial feeders from this size: K, W built on the device (every radial feeder:
-# the host inverse also leaves OpenBLAS's workers spinning, which starves the
-# host threads staging a pageable caller array, tools/e2e_pageable2.py)
-DEVICE_SETUP_MIN_B = 1
+# radial feeders from this size: K, W built on the device (below it the host
+# inverse is cheaper than the device setup and runs single-threaded in
+# OpenBLAS; from about b = 100 the threaded inverse also leaves OpenBLAS's
+# workers spinning, which starves the host threads staging a pageable caller
+# array, tools/e2e_pageable2.py)
+DEVICE_SETUP_MIN_B = 64
 
 
 def device_kw(contract: ModelContract, device) -> tuple[torch.Tensor, torch.Tensor] | None:

@@ -40,6 +40,7 @@ def test_meshed_network_keeps_host_setup(golden):
 def test_auto_setup_choice():
     from paper_2403_04578_b200 import DenseOperator
     assert DenseOperator(_model(101)).setup == "device"          # radial feeders: on the device
+    assert DenseOperator(_model(35)).setup == "host"             # small: LAPACK is cheaper
     assert DenseOperator(_model(101), setup="host").setup == "host"  # LAPACK, bitwise the reference's K
     with pytest.raises(ValueError):
         DenseOperator(_model(101), setup="gpu")
