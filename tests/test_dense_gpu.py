@@ -375,3 +375,22 @@ def test_two_threads_same_device_bitwise(golden):
     for w, o in zip(want, got):
         assert np.array_equal(w.values, o.values) and np.array_equal(w.residuals, o.residuals)
         assert np.array_equal(w.iterations_per_case, o.iterations_per_case)
+
+
+def test_residual_row_blocks_same_bits(monkeypatch):
+    """tpf_residual_c128 splits a small batch's rows over a second grid
+    dimension and combines the per-case maxima by atomicMax on the bits: the
+    same numbers as one thread per case (TPF_RESID_NRB forces the split)."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator, GenSpec, build_network, gen_scenarios
+    from paper_2403_04578_b200._device import residual_and_summary
+    m = build_network(GenSpec(n_buses=301, seed=4))
+    S = torch.from_numpy(gen_scenarios(m, 3000, GenSpec(n_buses=301, seed=4)).values).cuda()
+    op = DenseOperator(m)
+    V, it = op.solve(S)
+    out = {}
+    for nrb in ("1", "3", "16"):
+        monkeypatch.setenv("TPF_RESID_NRB", nrb)
+        r, _, _ = residual_and_summary(op.contract, S, V, it, 1e-8, op.device)
+        out[nrb] = r.clone()
+    assert torch.equal(out["1"], out["3"]) and torch.equal(out["1"], out["16"])

@@ -319,3 +319,37 @@ def test_subtree_schedule_emulation_bitwise(n_buses, seed):
     rng = np.random.default_rng(seed)
     rhs = rng.standard_normal(c.b) + 1j * rng.standard_normal(c.b)
     assert np.array_equal(subtree_solve_host(s, rhs), sp.tree_solve_host(t, rhs))
+
+
+@pytest.mark.parametrize("n_buses,seed", [(12, 1), (101, 0), (1001, 2)])
+def test_tree_direct_solves_like_superlu(n_buses, seed):
+    """The direct tree elimination (sparse.tree_direct, the radial feeders'
+    batch factorization) solves Y_dd x = r like the SuperLU-based layout and
+    dense LAPACK, with the same level structure."""
+    from paper_2403_04578_b200 import GenSpec, build_network
+    from paper_2403_04578_b200.sparse import ModelContract, factorize_ydd, tree_direct, tree_levels, tree_solve_host
+    c = ModelContract.of(build_network(GenSpec(n_buses=n_buses, seed=seed)))
+    td = tree_direct(c.y_dd, c.src)
+    tl = tree_levels(factorize_ydd(c.y_dd, count=False), c.src)
+    assert td is not None and td.levels == tl.levels
+    assert np.array_equal(np.diff(td.level_info[:td.levels + 1]), np.diff(tl.level_info[:tl.levels + 1]))
+    rng = np.random.default_rng(seed)
+    r = rng.standard_normal(c.b) + 1j * rng.standard_normal(c.b)
+    xe = np.linalg.solve(c.y_dd.toarray(), r)
+    assert np.abs(tree_solve_host(td, r) - xe).max() <= 1e-12 * np.abs(xe).max()
+
+
+def test_tree_direct_rejects_meshed_networks_and_counts_once():
+    from paper_2403_04578_b200 import Branch, GenSpec, NetworkModel, build_network
+    from paper_2403_04578_b200.sparse import ModelContract, factorization_count, radial_levels, tree_direct
+    base = build_network(GenSpec(n_buses=40, seed=2))
+    y0 = base.admittance.y_dd.toarray()
+    i, j = next((i, j) for i in range(1, 40) for j in range(i + 2, 40) if y0[i - 1, j - 1] == 0)
+    branches = list(base.branches) + [Branch(from_bus=i, to_bus=j, r=0.02, x=0.03)]  # a tie: one loop
+    meshed = NetworkModel.from_branches(branches, 40, slack=base.slack)
+    assert meshed.admittance.y_dd.nnz == base.admittance.y_dd.nnz + 2
+    assert tree_direct(meshed.admittance.y_dd, meshed.source_injection()) is None
+    c = ModelContract.of(base)
+    n0 = factorization_count()
+    assert radial_levels(c) is not None and factorization_count() == n0 + 1
+    assert radial_levels(c, count=False) is not None and factorization_count() == n0 + 1

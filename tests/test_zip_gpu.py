@@ -184,3 +184,37 @@ def test_zip_meshed_zero_diagonal_needs_pivoting():
     assert np.array_equal(out.converged_mask, mask)
     assert np.abs(out.iterations_per_case.astype(int) - n).max() <= 1
     assert np.abs(out.values[:, mask] - V[:, mask]).max(initial=0) <= 1e-9
+
+
+def test_zip_meshed_dense_and_fixed_pattern_kernels_agree():
+    """The two meshed ZIP kernels (dense LU with row pivoting for b <= 64, fixed
+    fill pattern without pivoting beyond) on one well-conditioned meshed
+    network: the same counts and masks, voltages to 1e-12."""
+    import torch
+    from paper_2403_04578_b200 import (Branch, GenSpec, LoadMatrix, NetworkModel, SolveOptions, ZipCoefficients,
+                                       build_network, gen_scenarios)
+    from paper_2403_04578_b200 import dense as dense_mod
+    from paper_2403_04578_b200._device import ModelContract
+    spec = GenSpec(n_buses=30, seed=5, load_scale=1.5)
+    base = build_network(spec)
+    rng = np.random.default_rng(5)
+    branches = list(base.branches) + [Branch(from_bus=3, to_bus=20, r=0.02, x=0.03),
+                                      Branch(from_bus=7, to_bus=25, r=0.03, x=0.02)]
+    b = base.n_demand
+    w = rng.dirichlet([1.0, 1.0, 2.0], size=b)
+    z = ZipCoefficients(alpha_z=w[:, 0], alpha_i=w[:, 1], alpha_p=1.0 - w[:, 0] - w[:, 1])
+    model = NetworkModel.from_branches(branches, 30, slack=base.slack, zip_coeffs=z)
+    L = LoadMatrix(gen_scenarios(model, 200, spec).values)
+    opts = SolveOptions(max_iterations=50)
+    c = ModelContract.of(model)
+    a = dense_mod._solve_zip_dense(model, c, L, opts, torch.device("cuda", 0), False)
+    lib = dense_mod._capi.load()  # force the fixed-pattern kernel: no dense route for any b
+    orig = lib.tpf_sparse_zip_dense_max_nodes
+    try:
+        lib.tpf_sparse_zip_dense_max_nodes = lambda: 0
+        f = dense_mod._solve_zip_lu(model, c, L, opts, torch.device("cuda", 0), False)
+    finally:
+        lib.tpf_sparse_zip_dense_max_nodes = orig
+    assert np.array_equal(a.iterations_per_case, f.iterations_per_case)
+    assert np.array_equal(a.converged_mask, f.converged_mask)
+    assert np.abs(a.values - f.values).max() <= 1e-12
