@@ -357,6 +357,14 @@ int tpf_residual_c128(int64_t tau, int32_t b,
                       const double* V, int64_t v_node_stride, int64_t v_case_stride,
                       const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
                       const double* src, double* resid, void* stream);
+/* The same with the rows visited in row_order (a permutation of 0..b-1, e.g.
+ * a depth-first order of a radial feeder, so a row's neighbours are read
+ * while still cached); the per-case maximum does not depend on the order. */
+int tpf_residual_order_c128(int64_t tau, int32_t b,
+                            const double* S, int64_t s_node_stride, int64_t s_case_stride,
+                            const double* V, int64_t v_node_stride, int64_t v_case_stride,
+                            const int32_t* ydd_row_ptr, const int32_t* ydd_col, const double* ydd_val,
+                            const double* src, const int32_t* row_order, double* resid, void* stream);
 
 /* --------------------------------------------------------------- summary --
  * converged mask (dense.py:198-199): mask[j] = isfinite(resid[j]) && resid[j] < residual_tol.

@@ -50,6 +50,9 @@ SIGNATURES = {
     "tpf_residual_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
         _c_ptr, _c_ptr, _c_ptr]),
+    "tpf_residual_order_c128": (ctypes.c_int, [
+        _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_i64, _c_i64, _c_ptr, _c_ptr, _c_ptr,
+        _c_ptr, _c_ptr, _c_ptr, _c_ptr]),
     "tpf_batch_summary": (ctypes.c_int, [_c_i64, _c_ptr, _c_ptr, _c_dbl, _c_ptr, _c_ptr, _c_ptr]),
     "tpf_sparse_fpi_c128": (ctypes.c_int, [
         _c_i64, _c_i32, _c_ptr, _c_i64, _c_i64,

@@ -59,12 +59,30 @@ class ModelContract:
             h.update(np.ascontiguousarray(a).tobytes())
         return h.digest()
 
+    def row_order(self) -> np.ndarray:
+        """A depth-first order of Y_dd's graph (every component): the residual
+        kernel visits rows in it, so a row's neighbours were read moments
+        before and still sit in L1 (C2: 0.50 -> 0.42 ms, tools/resid_order_probe.py)."""
+        from scipy.sparse import csgraph
+        y = self.y_dd
+        pat = sparse.csr_matrix((np.ones(y.indices.size), y.indices, y.indptr), shape=y.shape)
+        seen = np.zeros(self.b, dtype=bool)
+        parts = []
+        for r in range(self.b):
+            if not seen[r]:
+                part = csgraph.depth_first_order(pat, r, directed=False, return_predecessors=False)
+                seen[part] = True
+                parts.append(part)
+        return np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, dtype=np.int32)
+
     def csr_on(self, device: torch.device):
+        """Y_dd (CSR), src and the residual's row order on ``device``."""
         rp = torch.from_numpy(self.y_dd.indptr.astype(np.int32)).to(device)
         ci = torch.from_numpy(self.y_dd.indices.astype(np.int32)).to(device)
         val = torch.from_numpy(np.ascontiguousarray(self.y_dd.data)).to(device)
         src = torch.from_numpy(self.src).to(device)
-        return rp, ci, val, src
+        order = torch.from_numpy(self.row_order()).to(device)
+        return rp, ci, val, src, order
 
 
 def complex_strides(t: torch.Tensor) -> tuple[int, int]:
@@ -108,10 +126,14 @@ def residual_and_summary(contract: ModelContract, S: torch.Tensor, V: torch.Tens
     sn, sc = complex_strides(S)
     vn, vc = complex_strides(V)
     if not have_resid:
-        rp, ci, val, src = csr if csr is not None else contract.csr_on(device)
-        fn = "tpf_residual_c64" if V.dtype == torch.complex64 else "tpf_residual_c128"
-        _capi.call(fn, tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
-                   rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
+        rp, ci, val, src, order = csr if csr is not None else contract.csr_on(device)
+        if V.dtype == torch.complex64:
+            _capi.call("tpf_residual_c64", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                       rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(), st)
+        else:
+            _capi.call("tpf_residual_order_c128", tau, contract.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                       rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), order.data_ptr(),
+                       resid.data_ptr(), st)
     _capi.call("tpf_batch_summary", tau, iters.data_ptr(), resid.data_ptr(), float(residual_tol),
                mask.data_ptr(), summ.data_ptr(), st)
     return resid, mask, summ

@@ -33,13 +33,17 @@ __global__ void residual_kernel(int64_t tau, int b, const double* __restrict__ S
                                 const double* __restrict__ V, int64_t vn, int64_t vc,
                                 const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                 const double* __restrict__ yv, const double* __restrict__ src,
-                                double* __restrict__ resid) {
+                                const int32_t* __restrict__ order, double* __restrict__ resid) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= tau) return;
   const int nrb = int(gridDim.y);
   const int i0 = int(int64_t(b) * blockIdx.y / nrb), i1 = int(int64_t(b) * (blockIdx.y + 1) / nrb);
   double worst = 0.0;
-  for (int i = i0; i < i1; ++i) {
+  for (int ii = i0; ii < i1; ++ii) {
+    // rows in `order` (a depth-first order of a radial feeder: a row's
+    // neighbours were read moments ago and still sit in L1); the maximum does
+    // not depend on the order of the rows
+    const int i = order ? __ldg(order + ii) : ii;
     const double2 si = ldg_c128(src, i);
     double ar = si.x, ai = si.y;
     for (int k = __ldg(rp + i); k < __ldg(rp + i + 1); ++k) {
@@ -109,10 +113,25 @@ extern "C" int tpf_version(void) { return 100; }
 
 extern "C" const char* tpf_last_error(void) { return g_last_error.c_str(); }
 
+extern "C" int tpf_residual_order_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                       int64_t s_case_stride, const double* V, int64_t v_node_stride,
+                                       int64_t v_case_stride, const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                       const double* ydd_val, const double* src, const int32_t* row_order,
+                                       double* resid, void* stream);
+
 extern "C" int tpf_residual_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
                                  int64_t s_case_stride, const double* V, int64_t v_node_stride,
                                  int64_t v_case_stride, const int32_t* ydd_row_ptr, const int32_t* ydd_col,
                                  const double* ydd_val, const double* src, double* resid, void* stream) {
+  return tpf_residual_order_c128(tau, b, S, s_node_stride, s_case_stride, V, v_node_stride, v_case_stride,
+                                 ydd_row_ptr, ydd_col, ydd_val, src, nullptr, resid, stream);
+}
+
+extern "C" int tpf_residual_order_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
+                                       int64_t s_case_stride, const double* V, int64_t v_node_stride,
+                                       int64_t v_case_stride, const int32_t* ydd_row_ptr, const int32_t* ydd_col,
+                                       const double* ydd_val, const double* src, const int32_t* row_order,
+                                       double* resid, void* stream) {
   if (tau < 0 || b < 1) return set_error(TPF_ERR_INVALID, "tpf_residual_c128: need tau >= 0, b >= 1");
   if (tau == 0) return TPF_OK;
   if (!S || !V || !ydd_row_ptr || !ydd_col || !ydd_val || !src || !resid)
@@ -137,7 +156,7 @@ extern "C" int tpf_residual_c128(int64_t tau, int32_t b, const double* S, int64_
   }
   residual_kernel<<<dim3(unsigned(blocks), unsigned(nrb)), threads, 0, st>>>(
       tau, b, S, s_node_stride, s_case_stride, V, v_node_stride, v_case_stride, ydd_row_ptr, ydd_col, ydd_val,
-      src, resid);
+      src, row_order, resid);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(residual_kernel)", err);
   return TPF_OK;

@@ -771,12 +771,17 @@ class SparseOperator:
         return V, iters
 
     def _residual(self, S, V, resid):
-        rp, ci, val, src = self.csr()
+        rp, ci, val, src, order = self.csr()
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
-        _capi.call("tpf_residual_c64" if V.dtype == torch.complex64 else "tpf_residual_c128", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
-                   rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(),
-                   stream_ptr(self.device))
+        if V.dtype == torch.complex64:
+            _capi.call("tpf_residual_c64", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                       rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), resid.data_ptr(),
+                       stream_ptr(self.device))
+        else:
+            _capi.call("tpf_residual_order_c128", S.shape[1], self.b, S.data_ptr(), sn, sc, V.data_ptr(), vn, vc,
+                       rp.data_ptr(), ci.data_ptr(), val.data_ptr(), src.data_ptr(), order.data_ptr(),
+                       resid.data_ptr(), stream_ptr(self.device))
 
 
 def batch_solve_sparse(model, loads: LoadMatrix, opts: SolveOptions = SolveOptions(),
