@@ -343,9 +343,9 @@ def run_ours():
         one_step = step
 
         def sharded_fn(_model, Sk, _opts):
-            resid_k, mask_k, summ_k = one_step(None, S_list.index(Sk) if len(S_list) > 1 else 0)
-            itk = iters_list[S_list.index(Sk) if len(S_list) > 1 else 0]
-            return finish(V, itk, resid_k, mask_k, summ_k, True)
+            k = next(i for i, x in enumerate(S_list) if x is Sk)  # by identity (tensor == is elementwise)
+            resid_k, mask_k, summ_k = one_step(None, k)
+            return finish(V, iters_list[k], resid_k, mask_k, summ_k, True)
 
         def step(ev=None, k=0):  # noqa: F811 -- the sharded step
             Sk = S_list[k % len(S_list)]
