@@ -3,18 +3,21 @@
 The sparse fixed point (sparse.py:186-197 restated as ``Y_dd v' = -(s*/conj(v)
 + src)``, one LU of Y_dd for every case) on a radial feeder is an up-sweep
 (children before parents) and a down-sweep (parents before children) of the
-tree LU per iteration (``sparse.tree_levels``).  The level kernel
-synchronises the whole CTA at every depth level (14 barriers per iteration
-at C3).  This schedule cuts the tree at depth ``D``:
+tree LU per iteration (``sparse.tree_levels`` / ``sparse.tree_direct``).  The
+level kernel synchronises the whole CTA at every depth level (14 barriers per
+iteration at C3).  This schedule cuts the tree at depth ``D``:
 
 * the nodes of depth < D form the *top* (21 nodes at C3), swept redundantly
   by every warp on its own private copy (shared memory);
 * every node of depth D roots a *subtree*; subtrees are packed onto the W
   warps of the CTA (largest first onto the least loaded warp), and each
-  warp's nodes are list-scheduled into *super-slots* of 64 mutually
-  independent nodes (a node goes to the first super-slot after all of its
-  children's), so a warp sweeps its subtrees two slots at a time with one
-  ``__syncwarp`` per super-slot and no CTA barrier.
+  warp's nodes are list-scheduled into *slots* of 32 mutually independent
+  nodes by Hu's rule (a node goes to the first slot after all of its
+  children's; the deepest ready nodes first), so a warp sweeps its subtrees
+  with one ``__syncwarp`` per step and no CTA barrier; consecutive slots with
+  no parent-child pair between them are marked and swept two at a time.
+  The cut depth is the one with the fewest slots (subtree + top); a cut whose
+  Hu lower bound max_w max(ceil(n_w / 32), height_w) cannot win is skipped.
 
 One iteration is then: every warp's subtree up-sweep, ONE CTA barrier (the
 subtree roots' child products cross warps through ``Proot``, double-buffered
@@ -24,10 +27,11 @@ subtree down-sweep.
 
 Slots: thread ``lane`` of warp ``w`` owns, in slot ``j`` (0 <= j < NSL), the
 node at position ``p = (w * NSL + j) * 32 + lane`` (or nothing).  Slots
-``0 .. NS-1`` are subtree slots (super-slot k = slots 2k, 2k+1; iterate, load
-and z / U_mm in Tensor Memory), slots ``NS ..`` the top (depth D-1 first).
-Arithmetic per node is that of the level kernel (same coefficients, same
-child order), so both kernels give the same bits.
+``0 .. NS-1`` are subtree slots (iterate and load in Tensor Memory, plus
+z / U_mm for slots with an internal node; leaf-only slots recompute it),
+slots ``NS ..`` the top (depth D-1 first).  Arithmetic per node is that of
+the level kernel (same coefficients, same child order), so both kernels give
+the same bits.
 """
 
 from __future__ import annotations
@@ -51,7 +55,7 @@ SUB_SMEM_MAX = 227 * 1024
 class SubtreeSchedule:
     b: int
     W: int
-    NS: int           # subtree slots per thread (even: NS / 2 super-slots)
+    NS: int           # subtree slots per thread
     NT: int           # top slots
     NSL: int          # NS + NT
     D: int            # cut depth
@@ -87,11 +91,11 @@ def _pack(lo16: int, hi16: int) -> int:
     return v - (1 << 32) if v >= (1 << 31) else v
 
 
-def _superslots(nodes: np.ndarray, kids_of, parent, prio, width: int = 64) -> list[list[int]]:
+def _superslots(nodes: np.ndarray, kids_of, parent, prio, width: int = 32) -> list[list[int]]:
     """List-schedule ``nodes`` (a union of subtrees; the up-sweep DAG is an
-    in-forest, child -> parent) into super-slots of ``width`` mutually
+    in-forest, child -> parent) into slots of ``width`` mutually
     independent nodes: at each step the ready nodes (all children in earlier
-    super-slots) farthest from their root go first (Hu's rule, optimal for
+    slots) farthest from their root go first (Hu's rule, optimal for
     unit tasks on an in-forest)."""
     nodes = [int(m) for m in nodes]
     member = set(nodes)
@@ -296,7 +300,7 @@ def subtree_schedule(t, rp: np.ndarray, ci: np.ndarray, yv: np.ndarray, W: int =
 def subtree_solve_host(s: SubtreeSchedule, rhs: np.ndarray) -> np.ndarray:
     """Numpy emulation of one solve ``Y_dd x = rhs`` in the kernel's order and
     storage (X index space with Proot and private top copies, child lists,
-    parents, super-slots); host tests compare it bit for bit with
+    parents, slots); host tests compare it bit for bit with
     ``sparse.tree_solve_host``."""
     W, NSL, NS = s.W, s.NSL, s.NS
     xcap, RR = s.xcap, s.RR
