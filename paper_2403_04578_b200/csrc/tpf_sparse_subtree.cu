@@ -21,14 +21,17 @@
 //
 // One case per CTA (one CTA per SM), persistent over cases.  Per thread and
 // slot: the iterate v and the load s in Tensor Memory (8 columns per slot),
-// the up-sweep value z in registers (compile-time slot index).  Shared
-// memory: the sweep exchange vector X (by position), the per-position
-// structure, the child lists and Proot.  Per case the loads arrive by TMA
-// (2-D tensor copy of one column of the node-major S, or a 1-D bulk copy of a
-// case-major column) into X in original node order, the next case's column is
+// plus z / U_mm (4 columns) for slots that hold an internal node (leaf-only
+// slots recompute it in the down-sweep with the same operations); the slot
+// loops are rolled.  Shared memory: the sweep exchange vector X (by
+// position), the per-position structure, the child lists, Proot and the
+// warps' private top copies.  Per case the loads arrive by TMA (2-D tensor
+// copy of one column of the node-major S, or a 1-D bulk copy of a case-major
+// column) into X in original node order, the next case's column is
 // prefetched into L2 by TMA while this one iterates, and V leaves the same way
 // (TMA store from X).  The residual post-check (fpi.py:221-240) is fused: the
-// final V is in X in original node order, Y_dd's rows come as ELL per position.
+// final V is in X in original node order, Y_dd's rows come as ELL blocks per
+// slot (see the residual below).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
