@@ -7,7 +7,8 @@
 // (C5: batch 58 iterations, per-case mean 10.4): every iteration only the
 // still-unconverged cases enter the GEMM.
 //
-// Per iteration (three launches, all early-exit when the active set is empty):
+// Per iteration (launches that early-exit when the active set is empty or
+// outside their range):
 //   prep    U[k, a] = S*_{k,c} / conj(v_{k,c}) for active case c = act[a]
 //           (zero-voltage guard), node-major so the writes coalesce over a;
 //   gemm    V'[a, n] = W[n] + sum_k U[k, a] K[n, k] on FP64 tensor cores:
@@ -17,9 +18,14 @@
 //           epilogue reads the old iterate, writes the new one in place and
 //           flags the case if any |dv|^2 >= tol^2 (or non-finite);
 //   compact count the update, keep flagged cases below max_iter.
+// Once at most kPtMax cases remain, tail_persistent_kernel runs every
+// remaining iteration in one cooperative launch (below); tail_kernel is the
+// per-iteration fallback when its CTAs cannot all be resident.
 // The k-order of every dot product is fixed, so a case's bits do not depend
 // on its position in the active set (permutation / shard invariance).
 #include <climits>
+#include <algorithm>
+#include <cstdlib>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -33,6 +39,7 @@ constexpr int TK = 16;   // input nodes per k-slab (4 k-steps)
 constexpr int KSTEPS = TK / 4;
 constexpr int MF = TM / 8, NF = TN / 8;
 constexpr int LTHREADS = 256;
+constexpr int kPtMax = 256;  // persistent hand-off: active cases at most this (tail_persistent_kernel)
 
 struct LargeArgs {
   int64_t tau;
@@ -52,6 +59,11 @@ struct LargeArgs {
   int32_t* count;  // [2]: active counts of the two lists
   int32_t* bad;    // per active position
   double2* U;      // b x tau, node-major, ld = tau
+  // persistent tail (tail_persistent_kernel)
+  double2* U2;       // [2][kPtMax][b]: slot-major U, double-buffered across iterations
+  int32_t* stamp;    // [kPtMax]: iteration + 1 at which the slot's case last moved >= tol
+  int handoff;       // gemm_kernel runs while more than this many cases are active
+  uint32_t* gbar;    // grid-barrier arrivals
 };
 
 __global__ void init_kernel(LargeArgs a) {
@@ -59,7 +71,9 @@ __global__ void init_kernel(LargeArgs a) {
   if (j == 0) {
     a.count[0] = int(a.tau);
     a.count[1] = 0;
+    *a.gbar = 0u;
   }
+  for (int64_t i = j; i < kPtMax; i += int64_t(gridDim.x) * blockDim.x) a.stamp[i] = 0;
   if (j >= a.tau) return;
   a.act[0][j] = int(j);
   a.iters[j] = 0;
@@ -115,7 +129,7 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
   constexpr int MFR = TMV / WM / 8, NFR = TN / WN / 8;  // fragments per warp tile
   constexpr int MFT = TMV / 8;                         // m-fragments per CTA tile
   const int n_act = a.count[cur];
-  if (TMV == 8 ? n_act > kTailM : n_act <= kTailM) return;
+  if (n_act <= a.handoff) return;
   const int m0 = blockIdx.x * TMV;
   if (m0 >= n_act) return;
   const int n0 = blockIdx.y * TN;
@@ -347,6 +361,313 @@ __global__ void __launch_bounds__(32 * kTailWarps) tail_kernel(LargeArgs a, int 
   if (row_bad && mok && (lane & 3) == 0) atomicOr(a.bad + m, 1);
 }
 
+// ---- Small active sets as ONE persistent launch -----------------------------
+// Once at most kPtMax cases are active (C5: from iteration 14 of 58, 171
+// cases falling to 1 over the last 44), an iteration is too little work for
+// 64x64 GEMM tiles (few CTAs, each latency-bound) and the remaining
+// iterations are mostly launch and latency overhead.  One cooperative launch
+// of ceil(b / 8) CTAs runs them all.  CTA x owns output nodes [8x, 8x + 8) for
+// every iteration and keeps those 8 rows of K resident in shared memory (one
+// bulk copy per row at entry).  The active cases go in groups of 8 (each CTA
+// starts at a different group); per group a producer warp streams the
+// group's U rows in kPtSK-node slabs through a kPtStages-deep ring
+// (cp.async.bulk + mbarriers) and three consumer warps each run ONE of the 3M
+// product chains (P1, P2, P3) over the whole k range, so the chain latency
+// (26 cycles per dependent DMMA; P3's operand sums make it ~40) rather than
+// one warp's issue rate sets the pace.  The first consumer warp finishes the
+// fragment exactly as gemm_kernel's epilogue does (same DMMAs, same k-order,
+// same zero padding of k to a multiple of TK: a case's bits do not depend on
+// which kernel ran an iteration), forms the next iteration's U for its nodes
+// (slot-major, double-buffered; a generic -> async proxy fence before the
+// other CTAs' bulk reads) and stamps cases that moved >= tol.  A grid barrier
+// then lets every CTA rebuild the same ordered active list.  kPtTeams > 1
+// runs several groups per CTA at once; measured slower at b = 1,000 (four
+// teams: shared-memory operand traffic of unblocked 8x8 fragments, ~60k
+// cycles per round of four groups against ~19k per group for one team).
+constexpr int kPtSK = 64;                  // k per ring slab (16 k-steps)
+constexpr int kPtStages = 8;               // ring depth per team
+constexpr int kPtTeams = 1;
+constexpr int kPtRow = kPtSK * 16 + 64;    // bytes per slab row; +64 B puts the two rows a quarter-warp reads in different banks
+constexpr int kPtStage = 8 * kPtRow;       // the U rows of one group of 8 cases
+constexpr int kPtThreads = 32 * 4 * kPtTeams;  // per team: 3 consumer warps + 1 producer warp
+static_assert(kPtSK % 4 == 0 && (TK * 4) % kPtSK == 0, "slabs tile the k-slabs of TK");
+static_assert(kPtStages <= 32, "parities");
+// resident K row stride: nks * 64 bytes rounded to 128, + 64 (bank offset as above)
+__host__ __device__ constexpr int pt_krow(int nks) { return (nks * 64 + 127) / 128 * 128 + 64; }
+
+struct PtShared {
+  uint64_t full[kPtTeams][kPtStages], empty[kPtTeams][kPtStages], kbar;
+  double hand[kPtTeams][2][32][2];
+  int warp_sum[kPtThreads / 32];
+  int list[kPtMax];
+  int n;
+};
+__host__ __device__ constexpr size_t pt_smem_bytes(int nks) {
+  return size_t(8) * pt_krow(nks) + size_t(kPtTeams) * kPtStages * kPtStage + sizeof(PtShared);
+}
+
+__device__ __forceinline__ void pt_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pt_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// all CTAs of the (cooperative) grid; `target` = barriers so far x gridDim.x
+__device__ __forceinline__ void pt_grid_sync(uint32_t* gbar, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(gbar, 1u);
+    uint32_t v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// U = conj(s) v / |v|^2 with the zero-voltage guard, bit-identical to prep_kernel
+__device__ __forceinline__ double2 pt_u(double2 v, double2 s) {
+  double m2 = __fma_rn(v.x, v.x, v.y * v.y);
+  if (m2 < kZeroGuard2) {
+    v = make_double2(kZeroGuard, 0.0);
+    m2 = kZeroGuard * kZeroGuard;
+  }
+  const double r = 1.0 / m2;
+  return make_double2(__fma_rn(s.x, v.x, s.y * v.y) * r, __fma_rn(s.x, v.y, -(s.y * v.x)) * r);
+}
+
+template <int W>
+__device__ __forceinline__ double pt_operand(double2 v) {
+  return W == 0 ? v.x : W == 1 ? v.y : v.x + v.y;
+}
+
+// Product chain W of one fragment over all nks k-steps: per slab the operand
+// loads issue ahead of its dependent DMMAs; the last slab zeroes operands past
+// b (gemm_kernel's zero padding up to a multiple of TK).
+template <int W>
+__device__ __forceinline__ void pt_chain(const unsigned char* ring, const unsigned char* kres, int krow,
+                                         uint64_t* full, uint64_t* empty, uint32_t q, int nslab, int nks, int b,
+                                         int lane, double& p0, double& p1) {
+  constexpr int KS = kPtSK / 4;
+  const int rowa = (lane >> 2) * kPtRow + (lane & 3) * 16;
+  const unsigned char* kb0 = kres + (lane >> 2) * krow + (lane & 3) * 16;
+  for (int sl = 0; sl < nslab; ++sl, ++q) {
+    const int st = q % kPtStages;
+    mbar_wait(&full[st], (q / kPtStages) & 1);
+    const unsigned char* sa = ring + size_t(st) * kPtStage + rowa;
+    const unsigned char* sb = kb0 + sl * kPtSK * 16;
+    const int kse = min(KS, nks - sl * KS);
+    if (kse == KS && (sl + 1) * kPtSK <= b) {
+      double x[KS], y[KS];
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        x[ks] = pt_operand<W>(*reinterpret_cast<const double2*>(sa + ks * 64));
+        y[ks] = pt_operand<W>(*reinterpret_cast<const double2*>(sb + ks * 64));
+      }
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma884(p0, p1, x[ks], y[ks]);
+    } else {
+#pragma unroll 1
+      for (int ks = 0; ks < kse; ++ks) {
+        const bool kok = sl * kPtSK + 4 * ks + (lane & 3) < b;
+        double2 av = *reinterpret_cast<const double2*>(sa + ks * 64);
+        double2 bv = *reinterpret_cast<const double2*>(sb + ks * 64);
+        if (!kok) av = bv = make_double2(0.0, 0.0);
+        dmma884(p0, p1, pt_operand<W>(av), pt_operand<W>(bv));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
+__global__ void __launch_bounds__(kPtThreads, 1) tail_persistent_kernel(LargeArgs a, int cur, int it0) {
+  const int n_entry = a.count[cur];
+  if (n_entry == 0 || n_entry > kPtMax) return;
+  const int b = a.b;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int team = warp < 3 * kPtTeams ? warp / 3 : warp - 3 * kPtTeams, role = warp < 3 * kPtTeams ? warp % 3 : 3;
+  const int n0 = blockIdx.x * 8;
+  const int nks = (b + TK - 1) / TK * KSTEPS;  // k-steps of 4, padded like gemm_kernel's slabs
+  const int nslab = (nks * 4 + kPtSK - 1) / kPtSK;
+  const int nrows = min(8, b - n0);
+  const int krow = pt_krow(nks);
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  unsigned char* kres = pt_smem;                                    // [8][krow]: this CTA's K rows
+  unsigned char* rings = pt_smem + 8 * krow;                        // [team][stage][8][kPtRow]: U slabs
+  PtShared& sh = *reinterpret_cast<PtShared*>(rings + size_t(kPtTeams) * kPtStages * kPtStage);
+  unsigned char* ring = rings + size_t(team) * kPtStages * kPtStage;
+  const int* act = a.act[cur];  // slot -> case, fixed for the whole launch
+  const size_t uplane = size_t(kPtMax) * b;
+
+  if (tid == 0) {
+    for (int t = 0; t < kPtTeams; ++t)
+      for (int i = 0; i < kPtStages; ++i) {
+        mbar_init(&sh.full[t][i], 1);
+        mbar_init(&sh.empty[t][i], 3);
+      }
+    mbar_init(&sh.kbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    sh.n = n_entry;
+    pt_expect_tx(&sh.kbar, uint32_t(nrows) * b * 16u);
+    for (int r = 0; r < nrows; ++r) pt_bulk(kres + r * krow, a.K + int64_t(n0 + r) * b, uint32_t(b) * 16u, &sh.kbar);
+  }
+  for (int q = tid; q < n_entry; q += kPtThreads) sh.list[q] = q;
+  // zero K past b and the rows past the feeder's last node (gemm_kernel's zero fill)
+  for (int e = tid; e < 8 * (krow / 16); e += kPtThreads) {
+    const int r = e / (krow / 16), k = e - r * (krow / 16);
+    if (r >= nrows || k >= b) *reinterpret_cast<double2*>(kres + r * krow + k * 16) = make_double2(0.0, 0.0);
+  }
+  // U of the entry iteration for this CTA's nodes (prep_kernel's values, slot-major)
+  for (int e = tid; e < nrows * n_entry; e += kPtThreads) {
+    const int r = e / n_entry, q = e - r * n_entry, n = n0 + r, c = act[q];
+    a.U2[size_t(q) * b + n] =
+        pt_u(a.V[n * a.v_node + int64_t(c) * a.v_case], __ldg(a.S + n * a.s_node + int64_t(c) * a.s_case));
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  uint32_t nbar = 1;
+  pt_grid_sync(a.gbar, nbar * gridDim.x);
+
+  uint32_t q_ring = 0;  // this team's ring slabs issued (producer) / consumed (consumers)
+  bool k_ready = false;
+  for (int it = it0;; ++it) {
+    const int n = sh.n;
+    const int par = (it - it0) & 1;
+    const double2* usrc = a.U2 + par * uplane;
+    const int ngroups = (n + 7) / 8;
+    if (role == 3) {
+      // producer of this team: its groups' U rows, slab by slab.  cp.async
+      // (generic proxy) because other CTAs wrote U with plain stores.
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // other CTAs' U stores -> bulk reads
+        for (int gi = team; gi < ngroups; gi += kPtTeams) {
+          // CTAs walk the groups from different starting points, so that the
+          // 125 CTAs do not all read the same U rows at the same time
+          const int g = (gi + blockIdx.x) % ngroups;
+          const int g0 = g * 8, gcnt = min(8, n - g0);
+          for (int sl = 0; sl < nslab; ++sl, ++q_ring) {
+            const int st = q_ring % kPtStages;
+            mbar_wait(&sh.empty[team][st], ((q_ring / kPtStages) & 1) ^ 1);
+            const int k0 = sl * kPtSK;
+            const uint32_t bytes = uint32_t(min(kPtSK, b - k0)) * 16u;
+            unsigned char* stage = ring + size_t(st) * kPtStage;
+            pt_expect_tx(&sh.full[team][st], bytes * uint32_t(gcnt));
+            for (int m = 0; m < gcnt; ++m)
+              pt_bulk(stage + m * kPtRow, usrc + size_t(sh.list[g0 + m]) * b + k0, bytes, &sh.full[team][st]);
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+      if (!k_ready) {
+        mbar_wait(&sh.kbar, 0);
+        k_ready = true;
+      }
+      for (int gi = team; gi < ngroups; gi += kPtTeams) {
+        // CTAs walk the groups from different starting points, so that the
+        // 125 CTAs do not all read the same U rows at the same time
+        const int g = (gi + blockIdx.x) % ngroups;
+        const int g0 = g * 8, gcnt = min(8, n - g0);
+        // the epilogue's operands, loaded ahead of the chain
+        const int m = lane >> 2;
+        const bool mok = m < gcnt;
+        const int slot = mok ? sh.list[g0 + m] : 0;
+        const int c = act[slot];
+        double2 vold[2], wv[2], sv[2];
+        if (role == 0) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int nn = 2 * (lane & 3) + e, nd = n0 + nn;
+            if (mok && nn < nrows) {
+              vold[e] = a.V[nd * a.v_node + int64_t(c) * a.v_case];
+              wv[e] = __ldg(a.W + nd);
+              sv[e] = __ldg(a.S + nd * a.s_node + int64_t(c) * a.s_case);
+            }
+          }
+        }
+        double p0 = 0.0, p1 = 0.0;
+        if (role == 0)
+          pt_chain<0>(ring, kres, krow, sh.full[team], sh.empty[team], q_ring, nslab, nks, b, lane, p0, p1);
+        else if (role == 1)
+          pt_chain<1>(ring, kres, krow, sh.full[team], sh.empty[team], q_ring, nslab, nks, b, lane, p0, p1);
+        else
+          pt_chain<2>(ring, kres, krow, sh.full[team], sh.empty[team], q_ring, nslab, nks, b, lane, p0, p1);
+        q_ring += nslab;
+        if (role > 0) {
+          sh.hand[team][role - 1][lane][0] = p0;
+          sh.hand[team][role - 1][lane][1] = p1;
+        }
+        named_bar(1 + team, 96);
+        if (role == 0) {
+          // gemm_kernel's epilogue for this fragment, plus the next U and the stamp
+          bool row_bad = false;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int nn = 2 * (lane & 3) + e, nd = n0 + nn;
+            if (mok && nn < nrows) {
+              const double q2 = sh.hand[team][0][lane][e], q3 = sh.hand[team][1][lane][e];
+              const double q1 = e == 0 ? p0 : p1;
+              const double cr = q1 - q2;
+              const double ci = (q3 - q1) - q2;
+              double2 old = vold[e];
+              if (__fma_rn(old.x, old.x, old.y * old.y) < kZeroGuard2) old = make_double2(kZeroGuard, 0.0);
+              const double2 nv = make_double2(cr + wv[e].x, ci + wv[e].y);
+              const double dr = nv.x - old.x, di = nv.y - old.y;
+              if (!(__fma_rn(dr, dr, di * di) < a.tol2)) row_bad = true;
+              a.V[nd * a.v_node + int64_t(c) * a.v_case] = nv;
+              a.U2[(par ^ 1) * uplane + size_t(slot) * b + nd] = pt_u(nv, sv[e]);
+            }
+          }
+          row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 1);
+          row_bad |= __shfl_xor_sync(0xffffffffu, row_bad, 2);
+          if (row_bad && mok && (lane & 3) == 0) a.stamp[slot] = it + 1;
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // U stores -> other CTAs' bulk reads
+        }
+        named_bar(1 + team, 96);  // hand[] free for the team's next group
+      }
+    }
+    ++nbar;
+    pt_grid_sync(a.gbar, nbar * gridDim.x);
+    // every CTA rebuilds the same ordered list from the stamps (CTA 0 counts the update)
+    int nn = 0;
+    for (int base = 0; base < n; base += kPtThreads) {
+      const int q = base + tid;
+      int slot = 0;
+      bool keep = false;
+      if (q < n) {
+        slot = sh.list[q];
+        if (blockIdx.x == 0) a.iters[act[slot]] = it + 1;
+        keep = __ldcg(a.stamp + slot) == it + 1 && it + 1 < a.max_iter;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) sh.warp_sum[warp] = __popc(bal);
+      __syncthreads();  // warp counts ready; every read of this round's slots done
+      int before = nn;
+      for (int w = 0; w < warp; ++w) before += sh.warp_sum[w];
+      int total = nn;
+      for (int w = 0; w < kPtThreads / 32; ++w) total += sh.warp_sum[w];
+      if (keep) sh.list[before + __popc(bal & ((1u << lane) - 1u))] = slot;
+      nn = total;
+      __syncthreads();  // warp_sum reusable
+    }
+    if (nn == 0) break;
+    if (tid == 0) sh.n = nn;
+    __syncthreads();
+  }
+  // nothing is in flight (every issued slab was consumed); retire the host loop
+  if (blockIdx.x == 0 && tid == 0) {
+    a.count[0] = 0;
+    a.count[1] = 0;
+  }
+}
+
 __global__ void compact_kernel(LargeArgs a, int cur) {
   const int n_act = a.count[cur];
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -367,7 +688,7 @@ using namespace tpf;
 
 extern "C" size_t tpf_dense_large_workspace_bytes(int64_t tau, int32_t b) {
   const size_t t = size_t(tau > 0 ? tau : 1);
-  return 256 + 3 * t * 4 + 64 + t * size_t(b) * 16 + 1024;
+  return 256 + 3 * t * 4 + 64 + t * size_t(b) * 16 + 2 * size_t(kPtMax) * b * 16 + size_t(kPtMax) * 4 + 2048;
 }
 
 extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S, int64_t s_node_stride,
@@ -411,6 +732,10 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   a.act[1] = reinterpret_cast<int32_t*>(take(size_t(tau) * 4));
   a.bad = reinterpret_cast<int32_t*>(take(size_t(tau) * 4));
   a.U = reinterpret_cast<double2*>(take(size_t(tau) * b * 16));
+  a.handoff = kTailM;
+  a.U2 = reinterpret_cast<double2*>(take(2 * size_t(kPtMax) * b * 16));
+  a.stamp = reinterpret_cast<int32_t*>(take(kPtMax * 4));
+  a.gbar = reinterpret_cast<uint32_t*>(a.count + 8);
   if (size_t(w - static_cast<char*>(workspace)) > workspace_bytes)
     return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: workspace too small");
 
@@ -432,11 +757,35 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   const int tsmem = int(kTailWarps * kTailDepth * 64 * sizeof(double2));
   aerr = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
   if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tail_kernel)", aerr);
+  // the persistent kernel needs its ceil(b / 8) CTAs co-resident (one per SM:
+  // b <= 1,184 on a B200) and its shared memory; otherwise gemm_kernel runs
+  // down to kTailM active cases and tail_kernel each iteration below that
+  const int pt_ctas = (b + 7) / 8;
+  const size_t ptsmem = pt_smem_bytes((b + TK - 1) / TK * KSTEPS);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  bool persistent = std::getenv("TPF_LARGE_TAIL_LAUNCHES") == nullptr && ptsmem <= size_t(smem_optin);
+  if (persistent) {
+    aerr = cudaFuncSetAttribute(tail_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ptsmem));
+    if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(tail_persistent_kernel)", aerr);
+    int per_sm = 0, coop = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_persistent_kernel, kPtThreads, ptsmem);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    persistent = coop && per_sm >= 1 && pt_ctas <= per_sm * sms;
+  }
+  a.handoff = persistent ? kPtMax : kTailM;
   for (int it = 0; it < max_iter; ++it) {
-    const int cur = it & 1;
+    int cur = it & 1;
     prep_kernel<<<pgrid, 256, 0, st>>>(a, cur);
     gemm_kernel<TM, 2, kBulkStages><<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
-    tail_kernel<<<tgrid, 32 * kTailWarps, tsmem, st>>>(a, cur);
+    if (persistent) {
+      void* args[] = {&a, &cur, &it};
+      aerr = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tail_persistent_kernel), dim3(pt_ctas),
+                                         dim3(kPtThreads), args, ptsmem, st);
+      if (aerr != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(tail_persistent_kernel)", aerr);
+    } else {
+      tail_kernel<<<tgrid, 32 * kTailWarps, tsmem, st>>>(a, cur);
+    }
     compact_kernel<<<tb, 256, 0, st>>>(a, cur);
   }
   cudaError_t err = cudaGetLastError();

@@ -188,6 +188,45 @@ def test_large_b_permutation_invariance_bitwise(golden):
     assert np.array_equal(b.values, a.values[:, perm])
 
 
+def _large_solve_both_tails(monkeypatch, model, S):
+    """(V, iterations) from the persistent tail kernel and from the
+    per-iteration launches (TPF_LARGE_TAIL_LAUNCHES=1)."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator
+    op = DenseOperator(model)
+    assert op.large
+    St = torch.from_numpy(np.ascontiguousarray(S)).cuda()
+    monkeypatch.delenv("TPF_LARGE_TAIL_LAUNCHES", raising=False)
+    V1, it1 = op.solve(St)
+    monkeypatch.setenv("TPF_LARGE_TAIL_LAUNCHES", "1")
+    V2, it2 = op.solve(St)
+    return (V1.cpu().numpy(), it1.cpu().numpy()), (V2.cpu().numpy(), it2.cpu().numpy())
+
+
+def test_large_b_persistent_tail_same_bits_c5_slice(golden, monkeypatch):
+    """32 cases near collapse: the persistent kernel runs all 58 iterations;
+    the per-iteration launches (GEMM tiles, then tail_kernel) give the same bits."""
+    g = golden("c5_slice32")
+    (V1, it1), (V2, it2) = _large_solve_both_tails(monkeypatch, g.model, g.S)
+    assert int(it1.max()) == 58
+    assert np.array_equal(it1, it2)
+    assert np.array_equal(V1.view(np.int64), V2.view(np.int64))
+
+
+def test_large_b_persistent_hand_off_same_bits(monkeypatch):
+    """600 cases of the C5 feeder: GEMM tiles while more than 256 are active,
+    then the persistent kernel; bitwise the per-iteration path, and the
+    heavy tail (a few cases to 50+ iterations) is exercised."""
+    from paper_2403_04578_b200 import GenSpec, build_network, gen_scenarios
+    spec = GenSpec(n_buses=1001, seed=0, load_scale=21.0)
+    m = build_network(spec)
+    S = gen_scenarios(m, 600, GenSpec(n_buses=1001, seed=3, load_scale=21.0)).values
+    (V1, it1), (V2, it2) = _large_solve_both_tails(monkeypatch, m, S)
+    assert np.array_equal(it1, it2)
+    assert np.array_equal(V1.view(np.int64), V2.view(np.int64))
+    assert (it1 > 16).sum() >= 1 and int(it1.max()) >= 30
+
+
 @pytest.mark.parametrize("kernel", ["pairs"])
 @pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
                                   "nine_zero_batch"])
