@@ -18,14 +18,19 @@
 //           epilogue reads the old iterate, writes the new one in place and
 //           flags the case if any |dv|^2 >= tol^2 (or non-finite);
 //   compact count the update, keep flagged cases below max_iter.
-// Once at most kPtMax cases remain, tail_persistent_kernel runs every
-// remaining iteration in one cooperative launch (below); tail_kernel is the
-// per-iteration fallback when its CTAs cannot all be resident.
+//   step    advance the device-resident iteration and set the loop condition.
+// The loop itself runs on the device: a CUDA graph WHILE node around these
+// launches (joined to the caller's stream capture, or built and launched per
+// call), so no launch is spent on iterations past the hand-off.  Once at most
+// kPtMax cases remain, tail_persistent_kernel runs every remaining iteration
+// in one cooperative launch (below); tail_kernel is the per-iteration
+// fallback when its CTAs cannot all be resident.
 // The k-order of every dot product is fixed, so a case's bits do not depend
 // on its position in the active set (permutation / shard invariance).
 #include <climits>
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "tpf_common.cuh"
 #include "tpf_internal.h"
@@ -63,15 +68,19 @@ struct LargeArgs {
   double2* U2;       // [2][kPtMax][b]: slot-major U, double-buffered across iterations
   int32_t* stamp;    // [kPtMax]: iteration + 1 at which the slot's case last moved >= tol
   int handoff;       // gemm_kernel runs while more than this many cases are active
+  int32_t* iter;     // the iteration in flight (device-resident: the loop may run on the device)
+  int loop_min;      // the iteration loop continues while more than this many cases are active
   uint32_t* gbar;    // grid-barrier arrivals
 };
 
-__global__ void init_kernel(LargeArgs a) {
+__global__ void init_kernel(LargeArgs a, cudaGraphConditionalHandle loop) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j == 0) {
     a.count[0] = int(a.tau);
     a.count[1] = 0;
+    *a.iter = 0;
     *a.gbar = 0u;
+    if (loop) cudaGraphSetConditional(loop, a.tau > a.loop_min ? 1u : 0u);
   }
   for (int64_t i = j; i < kPtMax; i += int64_t(gridDim.x) * blockDim.x) a.stamp[i] = 0;
   if (j >= a.tau) return;
@@ -80,7 +89,8 @@ __global__ void init_kernel(LargeArgs a) {
   for (int i = 0; i < a.b; ++i) a.V[i * a.v_node + j * a.v_case] = a.v_flat;
 }
 
-__global__ void prep_kernel(LargeArgs a, int cur) {
+__global__ void prep_kernel(LargeArgs a) {
+  const int cur = *a.iter & 1;
   const int n_act = a.count[cur];
   const int* act = a.act[cur];
   // the output list of this iteration's compaction was the input of the previous one
@@ -124,7 +134,8 @@ constexpr int kTailM = 64;
 // keeps NST - 1 slabs in flight to cover the L2 latency.  The stage count does
 // not change the k-order.
 template <int TMV, int WM, int NST>
-__global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a, int cur) {
+__global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a) {
+  const int cur = *a.iter & 1;
   constexpr int WN = 8 / WM;
   constexpr int MFR = TMV / WM / 8, NFR = TN / WN / 8;  // fragments per warp tile
   constexpr int MFT = TMV / 8;                         // m-fragments per CTA tile
@@ -273,7 +284,8 @@ constexpr int kTailDepth = 16;
 
 constexpr int kTailWarps = 4;  // one fragment per SM sub-partition: the DMMA pipe is per SMSP
 
-__global__ void __launch_bounds__(32 * kTailWarps) tail_kernel(LargeArgs a, int cur) {
+__global__ void __launch_bounds__(32 * kTailWarps) tail_kernel(LargeArgs a) {
+  const int cur = *a.iter & 1;
   const int n_act = a.count[cur];
   if (n_act > kTailM) return;
   const int m0 = blockIdx.y * 8;
@@ -488,7 +500,8 @@ __device__ __forceinline__ void pt_chain(const unsigned char* ring, const unsign
   }
 }
 
-__global__ void __launch_bounds__(kPtThreads, 1) tail_persistent_kernel(LargeArgs a, int cur, int it0) {
+__global__ void __launch_bounds__(kPtThreads, 1) tail_persistent_kernel(LargeArgs a) {
+  const int it0 = *a.iter, cur = it0 & 1;
   const int n_entry = a.count[cur];
   if (n_entry == 0 || n_entry > kPtMax) return;
   const int b = a.b;
@@ -668,7 +681,8 @@ __global__ void __launch_bounds__(kPtThreads, 1) tail_persistent_kernel(LargeArg
   }
 }
 
-__global__ void compact_kernel(LargeArgs a, int cur) {
+__global__ void compact_kernel(LargeArgs a) {
+  const int cur = *a.iter & 1;
   const int n_act = a.count[cur];
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_act) return;
@@ -679,6 +693,14 @@ __global__ void compact_kernel(LargeArgs a, int cur) {
     const int q = atomicAdd(a.count + (cur ^ 1), 1);
     a.act[cur ^ 1][q] = c;
   }
+}
+
+// Advance the device-resident iteration; with a device-side loop, decide
+// whether its body (prep, gemm, [tail,] compact, step) runs again.
+__global__ void step_kernel(LargeArgs a, cudaGraphConditionalHandle loop) {
+  const int it = *a.iter;
+  *a.iter = it + 1;
+  if (loop) cudaGraphSetConditional(loop, (a.count[(it & 1) ^ 1] > a.loop_min && it + 1 < a.max_iter) ? 1u : 0u);
 }
 
 }  // namespace
@@ -736,11 +758,11 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   a.U2 = reinterpret_cast<double2*>(take(2 * size_t(kPtMax) * b * 16));
   a.stamp = reinterpret_cast<int32_t*>(take(kPtMax * 4));
   a.gbar = reinterpret_cast<uint32_t*>(a.count + 8);
+  a.iter = a.count + 2;
   if (size_t(w - static_cast<char*>(workspace)) > workspace_bytes)
     return set_error(TPF_ERR_INVALID, "tpf_dense_fpi_large_c128: workspace too small");
 
   const unsigned tb = unsigned((tau + 255) / 256);
-  init_kernel<<<tb, 256, 0, st>>>(a);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -774,19 +796,119 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
     persistent = coop && per_sm >= 1 && pt_ctas <= per_sm * sms;
   }
   a.handoff = persistent ? kPtMax : kTailM;
-  for (int it = 0; it < max_iter; ++it) {
-    int cur = it & 1;
-    prep_kernel<<<pgrid, 256, 0, st>>>(a, cur);
-    gemm_kernel<TM, 2, kBulkStages><<<ggrid, LTHREADS, gsmem, st>>>(a, cur);
+  a.loop_min = persistent ? kPtMax : 0;
+
+  // The iteration loop runs on the device: a CUDA graph WHILE node around
+  // prep -> gemm -> [tail ->] compact -> step, whose condition step_kernel
+  // sets (more than loop_min cases active, iterations left), then the
+  // persistent kernel once.  Inside a stream capture the nodes join the
+  // captured graph; otherwise a graph is built, launched and released.
+  // TPF_LARGE_HOST_LOOP=1 (or a graph API failure before anything was
+  // enqueued) launches the max_iter iterations from the host instead, each
+  // kernel exiting early once its range is empty.
+  const bool want_graph = std::getenv("TPF_LARGE_HOST_LOOP") == nullptr;
+  if (want_graph) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* cdeps = nullptr;
+    size_t ncdeps = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &cdeps, &ncdeps);
+    if (e != cudaSuccess) return set_cuda_error("cudaStreamGetCaptureInfo", e);
+    const bool captured = cs == cudaStreamCaptureStatusActive;
+    std::vector<cudaGraphNode_t> deps(cdeps, cdeps + (captured ? ncdeps : 0));
+    if (!captured) {
+      e = cudaGraphCreate(&g, 0);
+      if (e != cudaSuccess) return set_cuda_error("cudaGraphCreate", e);
+    }
+    cudaGraphConditionalHandle loop = 0;
+    auto fail = [&](const char* what, cudaError_t err) {
+      if (!captured && g) cudaGraphDestroy(g);
+      return set_cuda_error(what, err);
+    };
+    e = cudaGraphConditionalHandleCreate(&loop, g, 0, 0);
+    if (e != cudaSuccess) return fail("cudaGraphConditionalHandleCreate", e);
+    auto add_kernel = [&](cudaGraph_t graph, std::vector<cudaGraphNode_t>& after, const void* fn, dim3 grid,
+                          dim3 block, size_t smem, void** args, bool coop, cudaGraphNode_t* out) {
+      cudaKernelNodeParams kp = {};
+      kp.func = const_cast<void*>(fn);
+      kp.gridDim = grid;
+      kp.blockDim = block;
+      kp.sharedMemBytes = unsigned(smem);
+      kp.kernelParams = args;
+      cudaError_t r = cudaGraphAddKernelNode(out, graph, after.data(), after.size(), &kp);
+      if (r == cudaSuccess && coop) {
+        cudaLaunchAttributeValue v = {};
+        v.cooperative = 1;
+        r = cudaGraphKernelNodeSetAttribute(*out, cudaLaunchAttributeCooperative, &v);
+      }
+      if (r == cudaSuccess) after.assign(1, *out);
+      return r;
+    };
+    cudaGraphNode_t node = nullptr;
+    void* init_args[] = {&a, &loop};
+    e = add_kernel(g, deps, reinterpret_cast<const void*>(init_kernel), dim3(tb), dim3(256), 0, init_args, false, &node);
+    if (e != cudaSuccess) return fail("graph: init_kernel", e);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = loop;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, deps.data(), deps.size(), &cp);
+    if (e != cudaSuccess) return fail("graph: while node", e);
+    deps.assign(1, node);
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    std::vector<cudaGraphNode_t> bdeps;
+    cudaGraphNode_t bn = nullptr;
+    void* a_args[] = {&a};
+    void* step_args[] = {&a, &loop};
+    e = add_kernel(body, bdeps, reinterpret_cast<const void*>(prep_kernel), dim3(pgrid), dim3(256), 0, a_args, false, &bn);
+    if (e == cudaSuccess)
+      e = add_kernel(body, bdeps, reinterpret_cast<const void*>(gemm_kernel<TM, 2, kBulkStages>), ggrid,
+                     dim3(LTHREADS), size_t(gsmem), a_args, false, &bn);
+    if (e == cudaSuccess && !persistent)
+      e = add_kernel(body, bdeps, reinterpret_cast<const void*>(tail_kernel), tgrid, dim3(32 * kTailWarps),
+                     size_t(tsmem), a_args, false, &bn);
+    if (e == cudaSuccess)
+      e = add_kernel(body, bdeps, reinterpret_cast<const void*>(compact_kernel), dim3(tb), dim3(256), 0, a_args, false, &bn);
+    if (e == cudaSuccess)
+      e = add_kernel(body, bdeps, reinterpret_cast<const void*>(step_kernel), dim3(1), dim3(1), 0, step_args, false, &bn);
+    if (e != cudaSuccess) return fail("graph: loop body", e);
     if (persistent) {
-      void* args[] = {&a, &cur, &it};
+      e = add_kernel(g, deps, reinterpret_cast<const void*>(tail_persistent_kernel), dim3(pt_ctas), dim3(kPtThreads),
+                     ptsmem, a_args, true, &node);
+      if (e != cudaSuccess) return fail("graph: tail_persistent_kernel", e);
+    }
+    if (captured) {
+      e = cudaStreamUpdateCaptureDependencies(st, deps.data(), deps.size(), cudaStreamSetCaptureDependencies);
+      if (e != cudaSuccess) return set_cuda_error("cudaStreamUpdateCaptureDependencies", e);
+      return TPF_OK;
+    }
+    cudaGraphExec_t ge = nullptr;
+    e = cudaGraphInstantiate(&ge, g, 0);
+    if (e != cudaSuccess) return fail("cudaGraphInstantiate", e);
+    e = cudaGraphLaunch(ge, st);
+    // an executable graph destroyed while in flight is freed on completion
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return set_cuda_error("cudaGraphLaunch", e);
+    return TPF_OK;
+  }
+
+  cudaGraphConditionalHandle none = 0;
+  init_kernel<<<tb, 256, 0, st>>>(a, none);
+  for (int it = 0; it < max_iter; ++it) {
+    prep_kernel<<<pgrid, 256, 0, st>>>(a);
+    gemm_kernel<TM, 2, kBulkStages><<<ggrid, LTHREADS, gsmem, st>>>(a);
+    if (persistent) {
+      void* args[] = {&a};
       aerr = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tail_persistent_kernel), dim3(pt_ctas),
                                          dim3(kPtThreads), args, ptsmem, st);
       if (aerr != cudaSuccess) return set_cuda_error("cudaLaunchCooperativeKernel(tail_persistent_kernel)", aerr);
     } else {
-      tail_kernel<<<tgrid, 32 * kTailWarps, tsmem, st>>>(a, cur);
+      tail_kernel<<<tgrid, 32 * kTailWarps, tsmem, st>>>(a);
     }
-    compact_kernel<<<tb, 256, 0, st>>>(a, cur);
+    compact_kernel<<<tb, 256, 0, st>>>(a);
+    step_kernel<<<1, 1, 0, st>>>(a, none);
   }
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_cuda_error("launch(dense large)", err);

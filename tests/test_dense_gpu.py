@@ -227,6 +227,44 @@ def test_large_b_persistent_hand_off_same_bits(monkeypatch):
     assert (it1 > 16).sum() >= 1 and int(it1.max()) >= 30
 
 
+def test_large_b_device_loop_matches_host_loop(golden, monkeypatch):
+    """The iteration loop as a CUDA graph WHILE node (default) and as
+    max_iter host launches (TPF_LARGE_HOST_LOOP=1) give the same bits."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator
+    g = golden("c5_slice32")
+    op = DenseOperator(g.model)
+    S = torch.from_numpy(g.S).cuda()
+    monkeypatch.delenv("TPF_LARGE_HOST_LOOP", raising=False)
+    V1, it1 = op.solve(S)
+    monkeypatch.setenv("TPF_LARGE_HOST_LOOP", "1")
+    V2, it2 = op.solve(S)
+    assert torch.equal(it1, it2) and int(it1.max()) == 58
+    assert torch.equal(V1.view(torch.int64), V2.view(torch.int64))
+
+
+def test_large_b_solve_inside_stream_capture(golden):
+    """Captured into a torch CUDA graph (the loop's WHILE node joins the
+    captured graph) and replayed twice: the eager result, bitwise."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator
+    g = golden("c5_slice32")
+    op = DenseOperator(g.model)
+    S = torch.from_numpy(g.S).cuda()
+    V0, it0 = op.solve(S)
+    op.solve(S)  # workspace and memos allocated outside the capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        Vg, itg = op.solve(S)
+    for _ in range(2):
+        Vg.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(itg, it0)
+        assert torch.equal(Vg.view(torch.int64), V0.view(torch.int64))
+
+
 @pytest.mark.parametrize("kernel", ["pairs"])
 @pytest.mark.parametrize("name", ["c2_slice192", "c1_slice512", "nine_t500", "twobus_infeasible", "asym6",
                                   "nine_zero_batch"])
