@@ -499,7 +499,8 @@ def run_ours():
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
                     **({"sparse": sparse} if sparse is not None else {}),
                     **({"shard_gather": shard_gather} if shard_gather is not None else {}),
-                    gpu_launches=launches_per_step(method, op, tau) * ARGS.steps,
+                    gpu_launches=sum(launches_per_step(method, op, tau, iters_list[k % len(S_list)])
+                                     for k in range(ARGS.steps)),
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -679,14 +680,24 @@ def dense_kernel_name(b, tau):
     return "dense_fpi_kernel" if tau <= 2 * sms * 64 else "dense_ws_kernel"
 
 
-def launches_per_step(method, op, tau):
+LARGE_HANDOFF = 256  # tpf_dense_large.cu kPtMax: active cases at the persistent hand-off
+
+
+def launches_per_step(method, op, tau, iters=None):
     """Our kernels per timed step: dense = solve + residual + summary; sparse =
     one tree launch per compact chunk (SparseOperator) + summary, or the
     general kernel + residual + summary."""
     if method == "dense":
-        # b > 104: init + (prep, bulk GEMM, tail GEMM, compact) per iteration up to the
-        # cap (early-exit launches once every case froze), then residual + summary
-        return 1 + 4 * 100 + 2 if op.b > 104 else 3
+        if op.b <= 104:
+            return 3
+        # b > 104: init, then (prep, GEMM, compact, step) per iteration of the
+        # device-side WHILE loop (while more than LARGE_HANDOFF cases are
+        # active), the persistent kernel once, residual + summary
+        it = iters.cpu().numpy() if hasattr(iters, "cpu") else np.asarray(iters)
+        loop = 0
+        while loop < int(it.max()) and int((it > loop).sum()) > LARGE_HANDOFF:
+            loop += 1
+        return 1 + 4 * loop + 1 + 2
     from paper_2403_04578_b200.sparse import TREE_CHUNK
     if op.sub is not None:  # per 65,536-case chunk: transpose in, subtree kernel, transpose out; + summary
         return 3 * -(-tau // 65536) + 1
