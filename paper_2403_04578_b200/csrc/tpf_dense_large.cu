@@ -45,6 +45,7 @@ constexpr int KSTEPS = TK / 4;
 constexpr int MF = TM / 8, NF = TN / 8;
 constexpr int LTHREADS = 256;
 constexpr int kPtMax = 256;  // persistent hand-off: active cases at most this (tail_persistent_kernel)
+constexpr int kMidM = 1184;  // 32-case GEMM tiles at most this many active cases (more CTAs per iteration)
 
 struct LargeArgs {
   int64_t tau;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(LTHREADS) gemm_kernel(LargeArgs a) {
   constexpr int MFR = TMV / WM / 8, NFR = TN / WN / 8;  // fragments per warp tile
   constexpr int MFT = TMV / 8;                         // m-fragments per CTA tile
   const int n_act = a.count[cur];
-  if (n_act <= a.handoff) return;
+  if (TMV == 32 ? (n_act <= a.handoff || n_act > kMidM) : n_act <= max(a.handoff, kMidM)) return;
   const int m0 = blockIdx.x * TMV;
   if (m0 >= n_act) return;
   const int n0 = blockIdx.y * TN;
@@ -773,6 +774,11 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   cudaError_t aerr = cudaFuncSetAttribute(gemm_kernel<TM, 2, kBulkStages>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem);
   if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(gemm_kernel)", aerr);
+  // partial active sets (kMidM or fewer cases): 32-case tiles, twice the CTAs
+  const int msmem = int(kBulkStages * KSTEPS * (32 / 8 + NF) * 32 * sizeof(double2));
+  aerr = cudaFuncSetAttribute(gemm_kernel<32, 2, kBulkStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
+  if (aerr != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(gemm_kernel<32>)", aerr);
+  const dim3 mgrid(unsigned((std::min<int64_t>(tau, kMidM) + 31) / 32), unsigned((b + TN - 1) / TN));
   // node groups fastest: the active fragments (cases m0 < n_act) of one
   // iteration spread over the SMs
   const dim3 tgrid(unsigned((b + 8 * kTailWarps - 1) / (8 * kTailWarps)), unsigned(kTailM / 8));
@@ -865,6 +871,9 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
     if (e == cudaSuccess)
       e = add_kernel(body, bdeps, reinterpret_cast<const void*>(gemm_kernel<TM, 2, kBulkStages>), ggrid,
                      dim3(LTHREADS), size_t(gsmem), a_args, false, &bn);
+    if (e == cudaSuccess)
+      e = add_kernel(body, bdeps, reinterpret_cast<const void*>(gemm_kernel<32, 2, kBulkStages>), mgrid,
+                     dim3(LTHREADS), size_t(msmem), a_args, false, &bn);
     if (e == cudaSuccess && !persistent)
       e = add_kernel(body, bdeps, reinterpret_cast<const void*>(tail_kernel), tgrid, dim3(32 * kTailWarps),
                      size_t(tsmem), a_args, false, &bn);
@@ -899,6 +908,7 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
   for (int it = 0; it < max_iter; ++it) {
     prep_kernel<<<pgrid, 256, 0, st>>>(a);
     gemm_kernel<TM, 2, kBulkStages><<<ggrid, LTHREADS, gsmem, st>>>(a);
+    gemm_kernel<32, 2, kBulkStages><<<mgrid, LTHREADS, msmem, st>>>(a);
     if (persistent) {
       void* args[] = {&a};
       aerr = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tail_persistent_kernel), dim3(pt_ctas),
