@@ -690,14 +690,15 @@ def launches_per_step(method, op, tau, iters=None):
     if method == "dense":
         if op.b <= 104:
             return 3
-        # b > 104: init, then (prep, GEMM, compact, step) per iteration of the
-        # device-side WHILE loop (while more than LARGE_HANDOFF cases are
-        # active), the persistent kernel once, residual + summary
+        # b > 104: init, then (prep, 64-case GEMM, 32-case GEMM, compact,
+        # step) per iteration of the device-side WHILE loop (while more than
+        # LARGE_HANDOFF cases are active), the persistent kernel once,
+        # residual + summary
         it = iters.cpu().numpy() if hasattr(iters, "cpu") else np.asarray(iters)
         loop = 0
         while loop < int(it.max()) and int((it > loop).sum()) > LARGE_HANDOFF:
             loop += 1
-        return 1 + 4 * loop + 1 + 2
+        return 1 + 5 * loop + 1 + 2
     from paper_2403_04578_b200.sparse import TREE_CHUNK
     if op.sub is not None:  # per 65,536-case chunk: transpose in, subtree kernel, transpose out; + summary
         return 3 * -(-tau // 65536) + 1
