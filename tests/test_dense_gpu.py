@@ -302,6 +302,28 @@ def test_ws_kernel_full_c2_counts():
     assert (V1 - V2).abs().max().item() <= 1e-13
 
 
+def test_large_b_beyond_persistent_limit(monkeypatch):
+    """b = 1,300: 163 CTAs of 8 nodes cannot all be resident, so the device
+    loop runs GEMM tiles and tail_kernel every iteration down to zero active
+    cases; counts exact vs the oracle, bitwise the host loop."""
+    import torch
+    from paper_2403_04578_b200 import DenseOperator, GenSpec, build_network, gen_scenarios
+    spec = GenSpec(n_buses=1301, seed=7, load_scale=4.0)
+    model = build_network(spec)
+    loads = gen_scenarios(model, 96, spec)
+    op = DenseOperator(model)
+    S = torch.from_numpy(np.ascontiguousarray(loads.values)).cuda()
+    monkeypatch.delenv("TPF_LARGE_HOST_LOOP", raising=False)
+    V1, it1 = op.solve(S)
+    monkeypatch.setenv("TPF_LARGE_HOST_LOOP", "1")
+    V2, it2 = op.solve(S)
+    assert torch.equal(it1, it2) and torch.equal(V1.view(torch.int64), V2.view(torch.int64))
+    V, n, mask, _ = orc.dense_per_case(model.admittance.y_dd, model.source_injection(), model.slack.v_s,
+                                       loads.values)
+    assert np.array_equal(it1.cpu().numpy(), n)
+    assert np.abs(V1.cpu().numpy() - V).max() < 1e-11
+
+
 @pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 50, 56, 64, 72, 80, 88, 96, 100, 101, 104, 105, 128])
 def test_feeder_sizes_across_kernel_boundaries(b):
     """Every node-block count of the shared-memory kernels (b <= 104) and the
