@@ -13,6 +13,7 @@
 // summary kernel and copy.  Pageable host buffers are page-locked in place for
 // the duration of the call (cudaHostRegister) so every copy is a DMA.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -268,6 +269,9 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
                  const int32_t* rp, const int32_t* ci, const double* yv, const double* src, double residual_tol,
                  double* V, int64_t v_node, int64_t v_case, int32_t* iters, double* resid, uint8_t* mask,
                  int32_t* summary, int64_t chunk, const Streams& ss, cudaStream_t setup) {
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
+  double h_mark = 0, h_loop = 0;
   HostLayout LS, LV;
   if (!LS.ok(b, tau, s_node, s_case)) return set_error(TPF_ERR_INVALID, "host S must be node-major or case-major");
   if (!LV.ok(b, tau, v_node, v_case)) return set_error(TPF_ERR_INVALID, "host V must be node-major or case-major");
@@ -348,10 +352,13 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     tev.push_back(e);
   };
   mark(setup);
+  h_mark = hms();
+  std::vector<double> h_chunk;
   int rc = TPF_OK;
   for (int64_t c = 0; c < nchunks && rc == TPF_OK; ++c) {
     const int k = int(c & 1);
     const int64_t lo = bnd[c], n = bnd[c + 1] - bnd[c];
+    if (trace) h_chunk.push_back(hms());
     if (c >= 2) cudaStreamWaitEvent(sin, ss.comp_done[k], 0);
     if (stage_s) {
       // staging slot k was last read by the H2D of chunk c - 2
@@ -420,7 +427,13 @@ int run_pipeline(ChunkSolver& solver, int64_t tau, int b, const double* S, int64
     cudaEventDestroy(fin);
   }
   mark(sout);
+  h_loop = hms();
   cudaError_t e1 = cudaStreamSynchronize(sin), e2 = cudaStreamSynchronize(scomp), e3 = cudaStreamSynchronize(sout);
+  if (trace) {
+    fprintf(stderr, "[tpf pipe] host: setup mark enqueued %.2f ms, loop enqueued %.2f ms, synced %.2f ms; chunk starts:", h_mark, h_loop, hms());
+    for (double t : h_chunk) fprintf(stderr, " %.2f", t);
+    fprintf(stderr, "\n");
+  }
   if (trace && !tev.empty()) {  // in / compute / out completion times of each chunk, ms after the setup mark
     fprintf(stderr, "[tpf pipe] %lld chunks, chunk %lld:", (long long)nchunks, (long long)chunk);
     for (size_t i = 1; i < tev.size(); ++i) {

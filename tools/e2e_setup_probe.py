@@ -37,3 +37,18 @@ for _ in range(20):
     dm.dense_kw(dm.ModelContract.of(m))
 print("dense_kw alone %.2f ms" % ((time.perf_counter() - t0) / 20 * 1e3))
 print("memo kept again %.1f ms" % run(False))
+t0 = time.perf_counter()
+for _ in range(20):
+    dm._KW_CACHE.clear()
+    dm.device_kw(dm.ModelContract.of(m), torch.device("cuda", 0))
+torch.cuda.synchronize()
+print("device_kw alone %.2f ms" % ((time.perf_counter() - t0) / 20 * 1e3))
+import cProfile, pstats  # noqa: E402
+dm._KW_CACHE.clear()
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(3):
+    dm._KW_CACHE.clear()
+    batch_solve_dense(m, host)
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
