@@ -709,6 +709,34 @@ __global__ void step_kernel(LargeArgs a, cudaGraphConditionalHandle loop) {
 
 using namespace tpf;
 
+namespace {
+// Executable graphs of eager calls, released once their launch has completed
+// (checked at this thread's next call; the rest at thread exit).
+struct LaunchedGraph {
+  cudaGraphExec_t exec;
+  cudaEvent_t done;
+};
+struct GraphReaper {
+  std::vector<LaunchedGraph> items;
+  void reap(bool all) {
+    size_t keep = 0;
+    for (auto& x : items) {
+      cudaError_t q = all ? cudaEventSynchronize(x.done) : cudaEventQuery(x.done);
+      if (q == cudaErrorNotReady) {
+        cudaGetLastError();  // not an error: still running
+        items[keep++] = x;
+        continue;
+      }
+      cudaGraphExecDestroy(x.exec);
+      cudaEventDestroy(x.done);
+    }
+    items.resize(keep);
+  }
+  ~GraphReaper() { reap(true); }
+};
+thread_local GraphReaper g_reaper;
+}  // namespace
+
 extern "C" size_t tpf_dense_large_workspace_bytes(int64_t tau, int32_t b) {
   const size_t t = size_t(tau > 0 ? tau : 1);
   return 256 + 3 * t * 4 + 64 + t * size_t(b) * 16 + 2 * size_t(kPtMax) * b * 16 + size_t(kPtMax) * 4 + 2048;
@@ -892,14 +920,22 @@ extern "C" int tpf_dense_fpi_large_c128(int64_t tau, int32_t b, const double* S,
       if (e != cudaSuccess) return set_cuda_error("cudaStreamUpdateCaptureDependencies", e);
       return TPF_OK;
     }
+    g_reaper.reap(false);
     cudaGraphExec_t ge = nullptr;
     e = cudaGraphInstantiate(&ge, g, 0);
-    if (e != cudaSuccess) return fail("cudaGraphInstantiate", e);
+    cudaGraphDestroy(g);  // the executable graph does not depend on it
+    if (e != cudaSuccess) return set_cuda_error("cudaGraphInstantiate", e);
     e = cudaGraphLaunch(ge, st);
-    // an executable graph destroyed while in flight is freed on completion
-    cudaGraphExecDestroy(ge);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return set_cuda_error("cudaGraphLaunch", e);
+    cudaEvent_t done = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(done, st);
+    if (e != cudaSuccess) {
+      if (done) cudaEventDestroy(done);
+      cudaStreamSynchronize(st);
+      cudaGraphExecDestroy(ge);
+      return set_cuda_error("cudaGraphLaunch", e);
+    }
+    g_reaper.items.push_back({ge, done});  // released after the launch completes
     return TPF_OK;
   }
 
