@@ -401,6 +401,7 @@ def run_ours():
     kms = float(np.mean([a.elapsed_time(c) for a, c in kev]))
     # algorithmic work per launch: mean over the timed steps of sum_j n_j
     sum_n = int(round(sum(int(iters_list[k % len(S_list)].sum().item()) for k in range(ARGS.steps)) / ARGS.steps))
+    launches = sum(launches_per_step(method, op, tau, iters_list[k % len(S_list)]) for k in range(ARGS.steps))
     summ = out[2].cpu().numpy()
     if world > 1:
         t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
@@ -499,8 +500,7 @@ def run_ours():
                     roofline=roofline, cpu_baseline=cpu, e2e=e2e,
                     **({"sparse": sparse} if sparse is not None else {}),
                     **({"shard_gather": shard_gather} if shard_gather is not None else {}),
-                    gpu_launches=sum(launches_per_step(method, op, tau, iters_list[k % len(S_list)])
-                                     for k in range(ARGS.steps)),
+                    gpu_launches=launches,
                     clocks=clk.summary())
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -72,3 +72,26 @@ def test_bench_c64_line():
     assert d["roofline"]["kernel"] == "dense_c64_kernel" and 0 < d["roofline"]["frac"] < 1
     assert d["config"]["converged"] == d["config"]["tau_per_gpu"]
     assert d["e2e"]["h2d_bytes_per_step"] == 34 * 8760 * 8
+
+
+def test_bench_default_line_with_sparse_half():
+    """The driver's default invocation: C2 dense plus the nested C3 sparse object (full size; ~1 min)."""
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "3", "--cpu-seconds", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["value"] > 0 and d["gpu_launches"] == 2 * 3
+    sp = d["sparse"]
+    assert sp["value"] > 0 and sp["roofline"]["bound"] == "hbm" and 0 < sp["roofline"]["frac"] < 1
+
+
+def test_bench_c5_line():
+    """Config C5 (b = 1,000, the device-side loop + persistent tail) at a small tau."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "c5", "--tau", "2000", "--steps", "2", "--warmup",
+                        "3", "--cpu-seconds", "1"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["value"] > 0 and d["gpu_launches"] >= 2 * 4
+    assert d["roofline"]["bound"] == "tensor" and 0 < d["roofline"]["frac"] < 1
