@@ -252,6 +252,26 @@ def run_sliced(devices: list[torch.device], tau: int, call, arrays) -> list:
     return results
 
 
+_STREAM_WS_LOCK = threading.Lock()
+
+
+def stream_scratch(cache: dict, device: torch.device, nbytes: int) -> torch.Tensor:
+    """Grow-only device scratch of an operator, one buffer per CUDA stream:
+    solves queued on different streams (threads, or one thread alternating
+    streams) never share scratch, and a buffer is reused only by work that its
+    stream orders after the previous use.  A grown buffer replaces the old one
+    on the same stream (torch's allocator keeps the freed block for that
+    stream's later work)."""
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    with _STREAM_WS_LOCK:
+        ws = cache.get(key)
+        if ws is None or ws.numel() < nbytes:
+            cache.pop(key, None)
+            ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cache[key] = ws
+    return ws
+
+
 def device_workspace_slot(device: torch.device, nbytes: int, slot: int) -> torch.Tensor:
     """Grow-only scratch for one host-pipeline call: one buffer per (calling
     thread, device, slot), so concurrent calls (the per-device threads of

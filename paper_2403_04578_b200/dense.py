@@ -32,7 +32,7 @@ import torch
 
 from . import _capi
 from ._device import (ModelContract, complex_strides, engine_dtype, host_csr, host_empty, host_loads,
-                      device_workspace_slot,
+                      device_workspace_slot, stream_scratch,
                       loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
                       stream_ptr)
 from ._types import LoadMatrix, SolveOptions, VoltageBatch
@@ -151,7 +151,7 @@ class DenseOperator:
             self.W = torch.from_numpy(np.array(W, dtype=self.dtype)).to(self.device)
         self.large = b > _capi.load().tpf_dense_max_nodes()
         self.v_flat = complex(abs(self.contract.v_s))
-        self._ws = None
+        self._ws: dict = {}  # per-stream scratch (_device.stream_scratch)
 
     @property
     def b(self) -> int:
@@ -161,9 +161,7 @@ class DenseOperator:
         lib = _capi.load()
         n = (lib.tpf_dense_large_workspace_bytes(tau, self.b) if self.large
              else lib.tpf_dense_workspace_bytes(self.b))
-        if self._ws is None or self._ws.numel() < n:
-            self._ws = torch.empty(max(int(n), 256), dtype=torch.uint8, device=self.device)
-        return self._ws
+        return stream_scratch(self._ws, self.device, int(n))
 
     def solve(self, S: torch.Tensor, opts: SolveOptions = SolveOptions(), V: torch.Tensor | None = None,
               iters: torch.Tensor | None = None, kernel: str | None = None):
@@ -182,14 +180,12 @@ class DenseOperator:
         if iters is None:
             iters = torch.empty(tau, dtype=torch.int32, device=self.device)
         if self.dtype == np.complex64:  # the c64 twin (include/tpf.h)
-            need = int(_capi.load().tpf_dense_c64_workspace_bytes(tau, b))
-            if self._ws is None or self._ws.numel() < need:
-                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            ws = stream_scratch(self._ws, self.device, int(_capi.load().tpf_dense_c64_workspace_bytes(tau, b)))
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
             _capi.call("tpf_dense_fpi_c64", tau, b, S.data_ptr(), sn, sc, self.K.data_ptr(), self.W.data_ptr(),
                        self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
-                       V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                       V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),
                        stream_ptr(self.device))
             return V, iters
         ws = self.workspace(tau)

@@ -32,7 +32,7 @@ from scipy import sparse
 from scipy.sparse.linalg import splu
 
 from . import _capi
-from ._device import (ModelContract, complex_strides, engine_dtype, host_csr, host_empty, host_loads,
+from ._device import (ModelContract, complex_strides, stream_scratch, engine_dtype, host_csr, host_empty, host_loads,
                       device_workspace_slot,
                       loads_to_device, ptr, require_cuda, residual_and_summary, resolve_devices, run_sliced,
                       stream_ptr)
@@ -615,7 +615,7 @@ class SparseOperator:
         self.lu = None if levels is not None else factorize_ydd(self.contract.y_dd)
         self._dev = None
         self.v_flat = complex(abs(self.contract.v_s))
-        self._ws = None
+        self._ws: dict = {}  # per-stream scratch (_device.stream_scratch)
         self._csr = None
         self._chunk = None
         if levels is None and use_tree:
@@ -695,9 +695,7 @@ class SparseOperator:
             # node-major batches are solved in case-major chunks (scratch in the workspace)
             need = (int(_capi.load().tpf_sparse_subtree_workspace_bytes(tau, b))
                     if S.stride(1) == 1 or V.stride(1) == 1 else 256)
-            if self._ws is None or self._ws.numel() < need:
-                self._ws = None
-                self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            ws = stream_scratch(self._ws, self.device, need)
             sb, g = self.sub, self.sub_dev
             sn, sc = complex_strides(S)
             vn, vc = complex_strides(V)
@@ -706,11 +704,10 @@ class SparseOperator:
                        g["ell_col"].data_ptr(), g["ell_val"].data_ptr(), S.data_ptr(), sn, sc,
                        self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
                        V.data_ptr(), vn, vc, iters.data_ptr(), 0 if resid is None else resid.data_ptr(),
-                       self._ws.data_ptr(), self._ws.numel(), stream_ptr(self.device))
+                       ws.data_ptr(), ws.numel(), stream_ptr(self.device))
             return V, iters
         if self.tree is not None:
-            if self._ws is None:
-                self._ws = torch.empty(256, dtype=torch.uint8, device=self.device)
+            ws = stream_scratch(self._ws, self.device, 256)
             if tau > TREE_CHUNK and S.stride(1) == 1 and V.stride(1) == 1:
                 return self._solve_tree_chunked(S, opts, V, iters, resid)
             sn, sc = complex_strides(S)
@@ -719,7 +716,7 @@ class SparseOperator:
             head = (tau, b, self.tree.levels, g["level_info"].data_ptr(), g["node_info"].data_ptr(),
                     g["node_coef"].data_ptr(), S.data_ptr(), sn, sc, self.v_flat.real, self.v_flat.imag,
                     float(opts.tolerance), int(opts.max_iterations), V.data_ptr(), vn, vc, iters.data_ptr())
-            tail = (self._ws.data_ptr(), self._ws.numel(), stream_ptr(self.device))
+            tail = (ws.data_ptr(), ws.numel(), stream_ptr(self.device))
             if resid is not None and "ell_w" in g:
                 _capi.call("tpf_sparse_tree_fpi_resid_c128", *head, g["ell_w"], g["ell_col"].data_ptr(),
                            g["ell_val"].data_ptr(), resid.data_ptr(), *tail)
@@ -731,8 +728,7 @@ class SparseOperator:
         c64 = self.dtype == np.complex64
         lib = _capi.load()
         need = int(lib.tpf_sparse_c64_workspace_bytes(tau, b) if c64 else lib.tpf_sparse_workspace_bytes(tau, b))
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        ws = stream_scratch(self._ws, self.device, need)
         sn, sc = complex_strides(S)
         vn, vc = complex_strides(V)
         g = self.dev
@@ -741,7 +737,7 @@ class SparseOperator:
                    g["u_ptr"].data_ptr(), g["u_col"].data_ptr(), g["u_val"].data_ptr(),
                    g["u_diag_inv"].data_ptr(), g["perm"].data_ptr(), g["src"].data_ptr(),
                    self.v_flat.real, self.v_flat.imag, float(opts.tolerance), int(opts.max_iterations),
-                   V.data_ptr(), vn, vc, iters.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                   V.data_ptr(), vn, vc, iters.data_ptr(), ws.data_ptr(), ws.numel(),
                    stream_ptr(self.device))
         if resid is not None:
             self._residual(S, V, resid)

@@ -324,6 +324,39 @@ def test_large_b_beyond_persistent_limit(monkeypatch):
     assert np.abs(V1.cpu().numpy() - V).max() < 1e-11
 
 
+@pytest.mark.parametrize("nb,scale", [(101, 1.0), (1001, 21.0)])
+def test_one_operator_two_streams_concurrently(nb, scale):
+    """One DenseOperator solving on two CUDA streams from two threads at once
+    (b = 100: the shared-memory kernel; b = 1,000: the device loop and the
+    cooperative persistent kernel): per-stream scratch, the sequential bits."""
+    import threading
+    import torch
+    from paper_2403_04578_b200 import DenseOperator, GenSpec, build_network, gen_scenarios
+    m = build_network(GenSpec(n_buses=nb, seed=0, load_scale=scale))
+    S = [torch.from_numpy(np.ascontiguousarray(
+        gen_scenarios(m, 600, GenSpec(n_buses=nb, seed=s, load_scale=scale)).values)).cuda() for s in (1, 2)]
+    op = DenseOperator(m)
+    ref = [op.solve(x) for x in S]
+    torch.cuda.synchronize()
+    out = [None, None]
+
+    def run(i):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for _ in range(4):
+                out[i] = op.solve(S[i])
+            st.synchronize()
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in (0, 1):
+        assert torch.equal(out[i][1], ref[i][1])
+        assert torch.equal(out[i][0].view(torch.int64), ref[i][0].view(torch.int64))
+
+
 @pytest.mark.parametrize("b", [1, 3, 8, 9, 33, 50, 56, 64, 72, 80, 88, 96, 100, 101, 104, 105, 128])
 def test_feeder_sizes_across_kernel_boundaries(b):
     """Every node-block count of the shared-memory kernels (b <= 104) and the
