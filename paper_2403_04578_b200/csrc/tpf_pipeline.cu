@@ -132,6 +132,9 @@ cudaError_t copy_chunk(bool h2d, const HostLayout& L, double* host, double* dev,
                        int64_t chunk, cudaStream_t st) {
   if (L.case_contig) {
     char* h = reinterpret_cast<char*>(host) + size_t(lo) * 16;
+    if (n == L.ld && n == chunk)  // the whole batch in one chunk: one contiguous block
+      return h2d ? cudaMemcpyAsync(dev, h, size_t(n) * b * 16, cudaMemcpyHostToDevice, st)
+                 : cudaMemcpyAsync(h, dev, size_t(n) * b * 16, cudaMemcpyDeviceToHost, st);
     if (h2d)
       return cudaMemcpy2DAsync(dev, size_t(chunk) * 16, h, size_t(L.ld) * 16, size_t(n) * 16, size_t(b),
                                cudaMemcpyHostToDevice, st);
